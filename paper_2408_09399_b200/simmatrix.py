@@ -1,0 +1,175 @@
+"""Similarity matrices and sorted neighbour lists on the B200.
+
+Drop-in for the reference's ``tmfgclust.simmatrix`` hot functions
+(simmatrix.py:105-123 pearson_similarity, 126-139 validate_similarity,
+205-249 SortedNeighborLists / sort_neighbor_lists): same names, arguments,
+return types and exceptions.  The work runs in libtmfg_b200.so; host arrays are
+copied to HBM once and results stay device-resident, with host views
+materialised lazily on first access.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _device as D
+from . import _native as N
+
+
+class DataError(ValueError):
+    """Raised for malformed input files or invalid matrices (simmatrix.py:18-19)."""
+
+
+@dataclass
+class Dataset:
+    """Labeled collection of equal-length series (simmatrix.py:22-54)."""
+
+    labels: np.ndarray
+    series: np.ndarray
+
+    def __post_init__(self):
+        self.labels = np.asarray(self.labels, dtype=np.int64)
+        if not D.is_device(self.series):
+            self.series = np.asarray(self.series, dtype=np.float64)
+        if self.series.ndim != 2:
+            raise DataError("series must be a 2-d array")
+        if self.n < 4:
+            raise DataError(f"dataset too small: need at least 4 objects, got {self.n}")
+        if self.length < 2:
+            raise DataError(f"series too short: need length >= 2, got {self.length}")
+        if self.labels.shape[0] != self.n:
+            raise DataError("labels and series row counts differ")
+
+    @property
+    def n(self) -> int:
+        return int(self.series.shape[0])
+
+    @property
+    def length(self) -> int:
+        return int(self.series.shape[1])
+
+    @property
+    def num_classes(self) -> int:
+        return int(self.labels.max()) + 1 if self.labels.size else 0
+
+
+def pearson_similarity_device(X):
+    """(n, L) series (host or device) -> (n, n) float64 CUDA tensor S."""
+    t = D.torch()
+    Xd = D.to_device(X, t.float64)
+    n, L = (int(s) for s in Xd.shape)
+    S = D.empty((n, n), t.float64)
+    ws = D.Workspace.get(N.size("tg_pearson_workspace_bytes", n, L))
+    N.call("tg_pearson_f64", N.ptr(Xd), n, L, N.ptr(S), N.ptr(ws), ws.numel(), N.stream_ptr())
+    return S
+
+
+def pearson_similarity(data: Dataset, workers: int | None = None):
+    """Dense Pearson correlation matrix of the dataset's rows (simmatrix.py:105-123).
+
+    Returns a host ndarray like the reference; when ``data.series`` is a CUDA
+    tensor the result stays on the device (a torch tensor).
+    ``workers`` is accepted for signature compatibility and ignored.
+    """
+    S = pearson_similarity_device(data.series)
+    if D.is_device(data.series):
+        return S
+    return S.cpu().numpy()
+
+
+_FLAG_MESSAGES = (
+    (N.TG_BAD_NAN, "similarity matrix contains NaN"),
+    (N.TG_BAD_ASYM, "similarity matrix is not symmetric"),
+    (N.TG_BAD_DIAG, "similarity matrix diagonal must be exactly 1"),
+    (N.TG_BAD_RANGE, "similarity values must lie in [-1, 1]"),
+)
+
+
+def validate_device(Sd) -> None:
+    """Run the on-device checks of simmatrix.py:126-139; raise DataError."""
+    t = D.torch()
+    n = int(Sd.shape[0])
+    flags = D.empty((1,), t.int32)
+    N.call("tg_validate_f64", N.ptr(Sd), n, N.ptr(flags), N.stream_ptr())
+    f = int(flags.item())
+    for bit, msg in _FLAG_MESSAGES:
+        if f & bit:
+            raise DataError(msg)
+
+
+def validate_similarity(S):
+    """Check SimilarityMatrix invariants; returns the validated float64 matrix."""
+    shape = tuple(S.shape)
+    if len(shape) != 2 or shape[0] != shape[1]:
+        raise DataError(f"similarity matrix must be square, got shape {shape}")
+    if not D.is_device(S):
+        S = np.asarray(S, dtype=np.float64)
+    validate_device(D.device_matrix(S))
+    return S
+
+
+class SortedNeighborLists:
+    """Per-vertex neighbour ids by (similarity desc, id asc) (simmatrix.py:205-222).
+
+    ``order`` is the (n, n-1) int32 table; on this backend it lives in HBM
+    (``order_device``) and the host copy is made on first access.
+    """
+
+    def __init__(self, S, order, S_device=None, rowsum_device=None):
+        self.S = S
+        self._order = D.LazyHost(dev=order) if D.is_device(order) else D.LazyHost(host=np.asarray(order))
+        self.S_device = S_device
+        self.rowsum_device = rowsum_device
+
+    @property
+    def order(self) -> np.ndarray:
+        return self._order.host
+
+    @order.setter
+    def order(self, value):
+        self._order = D.LazyHost(dev=value) if D.is_device(value) else D.LazyHost(host=np.asarray(value))
+
+    @property
+    def order_device(self):
+        t = D.torch()
+        return self._order.device(t.int32)
+
+    @property
+    def n(self) -> int:
+        return int(self._order.dev.shape[0] if self._order.dev is not None else self._order.host.shape[0])
+
+    def pairs(self, v: int) -> list[tuple[float, int]]:
+        """The (similarity, neighbor) list for vertex v, best first."""
+        S = self.S if not D.is_device(self.S) else self.S[v].cpu().numpy()[None, :]
+        row = S[v] if not D.is_device(self.S) else S[0]
+        return [(float(row[u]), int(u)) for u in self.order[v]]
+
+
+def sort_rows_device(Sd, with_rowsum: bool = True):
+    """(order (n, n-1) int32, rowsum (n,) float64 or None) as CUDA tensors."""
+    t = D.torch()
+    n = int(Sd.shape[0])
+    order = D.empty((n, max(n - 1, 0)), t.int32)
+    rowsum = D.empty((n,), t.float64) if with_rowsum else None
+    if n >= 2:
+        ws = D.Workspace.get(N.size("tg_row_sort_workspace_bytes", n))
+        N.call("tg_row_sort_f64", N.ptr(Sd), n, N.ptr(order), N.ptr(rowsum), N.ptr(ws), ws.numel(),
+               N.stream_ptr())
+    elif rowsum is not None:
+        rowsum.zero_()
+    return order, rowsum
+
+
+def sort_neighbor_lists(S, workers: int | None = None) -> SortedNeighborLists:
+    """Sort every vertex's neighbours by (similarity desc, id asc) (simmatrix.py:225-249).
+
+    One fused pass also produces the initial-clique row sums, kept on the
+    device for build_tmfg.  ``workers`` is accepted and ignored.
+    """
+    if not D.is_device(S):
+        S = np.asarray(S, dtype=np.float64)
+    Sd = D.device_matrix(S)
+    order, rowsum = sort_rows_device(Sd, with_rowsum=True)
+    return SortedNeighborLists(S, order, S_device=Sd, rowsum_device=rowsum)

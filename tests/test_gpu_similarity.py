@@ -1,0 +1,120 @@
+"""GPU parity: similarity, validation, row sort, initial clique vs the CPU oracle.
+
+Bit-exact for the integer outputs (order, clique, row sums); |dS| <= 1e-12 for
+the fp64 DMMA Pearson matrix (north_star tolerance, absolute since |S| <= 1).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SMALL = ["n4_u", "n5_flat", "n6_u", "n20_round", "n30_u", "n40_q", "n60_u", "n120_q", "n50_s", "n200_s",
+         "c1_n300", "c4_n400"]
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_2408_09399_b200 as p
+    p._native.load()
+    return p
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_sort_matches_golden(name, small_cases, pkg):
+    c = small_cases[name]
+    lists = pkg.sort_neighbor_lists(c["S"])
+    assert lists.order.dtype == np.int32
+    assert np.array_equal(lists.order, c["order"])
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_clique_matches_golden(name, small_cases, digests, pkg):
+    S = small_cases[name]["S"]
+    assert list(pkg.select_initial_clique(S)) == digests[name]["clique"]
+
+
+@pytest.mark.parametrize("config", [1, 2, 4])
+def test_sort_configs_match_reference_hash(config, digests, oracle, pkg):
+    from paper_2408_09399_b200 import synth
+    x, _ = synth.generate(config)
+    S = oracle.pearson_similarity(x)          # bit-identical to the reference's S
+    assert oracle.sha(S) == digests[f"config{config}"]["S"]
+    lists = pkg.sort_neighbor_lists(S)
+    assert oracle.sha(lists.order) == digests[f"config{config}"]["order"]
+    assert list(pkg.select_initial_clique(S)) == digests[f"config{config}"]["clique"]
+
+
+@pytest.mark.parametrize("n,L", [(5, 7), (129, 33), (500, 128), (1000, 64), (2000, 256), (777, 3)])
+def test_pearson_within_tolerance(n, L, oracle, pkg):
+    rng = np.random.default_rng(n + L)
+    x = rng.standard_normal((n, L)) * rng.uniform(0.1, 10, size=(n, 1)) + rng.uniform(-5, 5, size=(n, 1))
+    x[min(3, n - 1)] = 2.5  # a constant row correlates 0
+    ref = oracle.pearson_similarity(x)
+    got = pkg.pearson_similarity(pkg.Dataset(labels=np.zeros(n, dtype=np.int64), series=x))
+    assert got.shape == (n, n)
+    assert np.abs(got - ref).max() <= 1e-12
+    assert np.array_equal(got, got.T)
+    assert np.all(np.diag(got) == 1.0)
+    assert got.min() >= -1.0 and got.max() <= 1.0
+    pkg.validate_similarity(got)
+
+
+def test_pearson_config4_integer_series(oracle, pkg):
+    from paper_2408_09399_b200 import synth
+    x, lab = synth.generate(4, n=1500)
+    ref = oracle.pearson_similarity(x)
+    got = pkg.pearson_similarity(pkg.Dataset(labels=lab, series=x))
+    assert np.abs(got - ref).max() <= 1e-12
+
+
+def test_validate_flags(pkg):
+    S = np.full((40, 40), 0.25)
+    np.fill_diagonal(S, 1.0)
+    pkg.validate_similarity(S)
+    bad = S.copy()
+    bad[3, 5] = np.nan
+    with pytest.raises(pkg.DataError, match="NaN"):
+        pkg.validate_similarity(bad)
+    bad = S.copy()
+    bad[3, 5] = 0.3
+    with pytest.raises(pkg.DataError, match="symmetric"):
+        pkg.validate_similarity(bad)
+    bad = S.copy()
+    bad[7, 7] = 0.999
+    with pytest.raises(pkg.DataError, match="diagonal"):
+        pkg.validate_similarity(bad)
+    bad = S.copy()
+    bad[1, 2] = bad[2, 1] = 1.5
+    with pytest.raises(pkg.DataError, match="range"):
+        pkg.validate_similarity(bad)
+
+
+@pytest.mark.parametrize("n", [4, 7, 8, 9, 64, 127, 128, 129, 130, 255, 1000, 4097, 16384, 16385, 20001])
+def test_row_sort_and_sums_sizes(n, oracle, pkg):
+    """Edge sizes, including both sides of the shared-memory limit (16384)."""
+    from paper_2408_09399_b200 import synth
+    S = synth.uniform_matrix(n, seed=n) if n <= 5000 else None
+    if S is None:
+        rng = np.random.default_rng(n)
+        x = rng.standard_normal((n, 16))
+        S = oracle.pearson_similarity(x)
+    lists = pkg.sort_neighbor_lists(S)
+    ref = oracle.sort_neighbor_lists(S)
+    assert np.array_equal(lists.order, ref)
+    assert list(pkg.select_initial_clique(S)) == list(oracle.select_initial_clique(S))
+    rs = lists.rowsum_device.cpu().numpy()
+    assert np.array_equal(rs, S.sum(axis=1) - np.diag(S))
+
+
+def test_row_sort_heavy_ties(oracle, pkg):
+    from paper_2408_09399_b200 import synth
+    for n, lv in [(300, 2), (2000, 3), (3000, 50)]:
+        S = synth.quantized_matrix(n, seed=n, levels=lv)
+        assert np.array_equal(pkg.sort_neighbor_lists(S).order, oracle.sort_neighbor_lists(S))
+    S = np.zeros((500, 500))
+    S[::2, ::2] = -0.0
+    np.fill_diagonal(S, 1.0)
+    assert np.array_equal(pkg.sort_neighbor_lists(S).order, oracle.sort_neighbor_lists(S))
