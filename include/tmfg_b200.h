@@ -79,12 +79,18 @@ int tg_initial_clique(const double *rowsum, int64_t n, int32_t *clique_out, void
 
 /* tmfg.py:344-436 build_tmfg_heap (+ tmfg.py:94-182 bookkeeping).
  * Outputs: trace (n-4, 4), host_fid (n-4) face id each row subdivided,
- * edges (3n-6, 2), faces (2n-4, 3) int32; stats int64[3] =
- * {pops, refreshes, gain_increases}. Persistent single-CTA kernel. */
+ * edges (3n-6, 2), faces (2n-4, 3) int32; stats int64[8] =
+ * {pops, refreshes, gain_increases, status, assert_fid, assert_old_gain_bits,
+ *  assert_new_gain_bits, 0}.  status 0 = ok, 2 = the check_invariants
+ * assertion of tmfg.py:429 fired (check != 0 only).  Persistent single-CTA
+ * kernel; check != 0 adds the brute-force optimality test of tmfg.py:377-399. */
 size_t tg_tmfg_workspace_bytes(int64_t n);
 int tg_tmfg_heap(const double *S, const int32_t *order, int64_t n, const int32_t *clique, int32_t *trace_out,
-                 int32_t *host_fid_out, int32_t *edges_out, int32_t *faces_out, int64_t *stats_out, void *ws,
-                 size_t ws_bytes, void *stream);
+                 int32_t *host_fid_out, int32_t *edges_out, int32_t *faces_out, int64_t *stats_out, int32_t check,
+                 void *ws, size_t ws_bytes, void *stream);
+
+/* tmfg.py:137-143 finalize weights: w[i] = S[edges[i,0], edges[i,1]]. */
+int tg_edge_weights(const double *S, int64_t n, const int32_t *edges, int64_t m, double *w_out, void *stream);
 
 /* ---------------------------------------------------------------------- APSP */
 

@@ -15,6 +15,16 @@ from .simmatrix import (
     sort_neighbor_lists,
     validate_similarity,
 )
-from .tmfg import select_initial_clique
+from .tmfg import (
+    GAIN_EPS,
+    BuildConfig,
+    TmfgGraph,
+    TraceError,
+    build_tmfg,
+    build_tmfg_heap,
+    edge_sum,
+    gain,
+    select_initial_clique,
+)
 
 __version__ = "0.1.0"

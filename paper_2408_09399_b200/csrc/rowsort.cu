@@ -13,10 +13,11 @@
 //      value and equal values (incl. -0.0/+0.0) share a bucket;
 //   3. one shared-memory atomicAdd per key yields its rank inside the bucket;
 //      a block scan gives bucket starts and the ids (u16) are scattered once;
-//   4. every bucket is finished by an exact (value desc, id asc) sort: insertion
-//      sort per thread (<=16 keys), warp rank-sort (<=256), and a block bitonic
-//      fallback for degenerate rows -- so the result is deterministic even though
-//      the atomic ranks are not;
+//   4. every key's exact rank inside its bucket (value desc, id asc) is counted
+//      against the other members (independent loads, cost = bucket size), and
+//      the ids are placed once more -- so the result is deterministic even though
+//      the atomic ranks are not; degenerate rows with huge tie groups stay
+//      correct (quadratic in the group size only);
 //   5. the ids stream out with 16-byte stores; optionally the same pass computes
 //      numpy's pairwise row sum from the staged row (fused initial-clique input).
 // Rows longer than the shared-memory budget (n > 16384) take the global-memory
@@ -224,7 +225,7 @@ __host__ RsPlan rs_plan(int64_t n, int nbuf) {
     p.nbuf = nbuf;
     size_t off = tg_align_up((size_t)nbuf * n * sizeof(double), 16);
     p.off_sidx = off;
-    off = tg_align_up(off + (size_t)pw * sizeof(uint16_t), 16);
+    off = tg_align_up(off + (size_t)n * sizeof(uint16_t), 16);
     p.off_cnt = off;
     off = tg_align_up(off + (size_t)(p.NB + 1) * sizeof(uint32_t), 16);
     p.off_spl = off;
@@ -242,10 +243,6 @@ __host__ RsPlan rs_plan(int64_t n, int nbuf) {
 struct RsMisc {
     double red[64];
     double rmin, rmax;
-    int nbig;
-    int slow;
-    int big_s0[256];
-    int big_n[256];
 };
 
 __device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
@@ -318,7 +315,6 @@ row_sort_smem_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restr
             mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         }
         if (lane == 0) { ms.red[warp] = mn; ms.red[32 + warp] = mx; }
-        if (tid == 0) { ms.nbig = 0; ms.slow = 0; }
         __syncthreads();
         // ---- phase B: splitters (warp 0) and per-bin linear maps
         if (warp == 0) {
@@ -436,82 +432,29 @@ row_sort_smem_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restr
             }
         }
         __syncthreads();
-        // ---- phase F: finish buckets exactly
-        for (int b = tid; b < NB; b += RS_T) {
-            int s0 = (int)cnt[b], s1 = (int)cnt[b + 1];
-            int s = s1 - s0;
-            if (s <= 1) continue;
-            if (s <= 16) {
-                for (int k = s0 + 1; k < s1; k++) {
-                    int key = sidx[k];
-                    double xk = vals[key];
-                    int q = k - 1;
-                    while (q >= s0) {
-                        int o = sidx[q];
-                        if (!rs_before(xk, key, vals[o], o)) break;
-                        sidx[q + 1] = (uint16_t)o;
-                        q--;
+        // ---- phase F: exact rank of every key inside its bucket (value desc, id asc).
+        // Independent loads, no dependent chains: cost per key = its bucket size.
+#pragma unroll
+        for (int e = 0; e < EMAX; e++) {
+            if (pk[e] != 0xffffffffu) {
+                const int j = tid + e * RS_T;
+                const int b = (int)(pk[e] >> 16);
+                const int s0 = (int)cnt[b], s1 = (int)cnt[b + 1];
+                int rank = 0;
+                if (s1 - s0 > 1) {
+                    const double xj = vals[j];
+                    for (int k = s0; k < s1; k++) {
+                        const int o = sidx[k];
+                        rank += rs_before(vals[o], o, xj, j);
                     }
-                    sidx[q + 1] = (uint16_t)key;
                 }
-            } else if (s <= 256) {
-                int slot = atomicAdd(&ms.nbig, 1);
-                if (slot < 256) { ms.big_s0[slot] = s0; ms.big_n[slot] = s; }
-                else ms.slow = 1;
-            } else {
-                ms.slow = 1;
+                pk[e] = (uint32_t)(s0 + rank);
             }
         }
         __syncthreads();
-        if (!ms.slow) {
-            int nbig = ms.nbig;
-            for (int g = warp; g < nbig; g += RS_T / 32) {
-                int s0 = ms.big_s0[g], s = ms.big_n[g];
-                int id[8];
-                double x[8];
-                int rk[8];
 #pragma unroll
-                for (int e = 0; e < 8; e++) {
-                    int k = lane + 32 * e;
-                    id[e] = k < s ? sidx[s0 + k] : 0;
-                    x[e] = k < s ? vals[id[e]] : 0.0;
-                    rk[e] = 0;
-                }
-                for (int l = 0; l < s; l++) {
-                    int il = sidx[s0 + l];
-                    double xl = vals[il];
-#pragma unroll
-                    for (int e = 0; e < 8; e++) rk[e] += rs_before(xl, il, x[e], id[e]);
-                }
-                __syncwarp();
-#pragma unroll
-                for (int e = 0; e < 8; e++)
-                    if (lane + 32 * e < s) sidx[s0 + rk[e]] = (uint16_t)id[e];
-                __syncwarp();
-            }
-        } else {
-            // degenerate row (huge tie groups): block bitonic over the whole row
-            const int pw = pl.pow2;
-            for (int k = m + tid; k < pw; k += RS_T) sidx[k] = 0xffff;
-            __syncthreads();
-            for (int kk = 2; kk <= pw; kk <<= 1) {
-                for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-                    for (int i = tid; i < pw; i += RS_T) {
-                        int ixj = i ^ jj;
-                        if (ixj > i) {
-                            int a = sidx[i], b = sidx[ixj];
-                            bool a_first;
-                            if (a == 0xffff) a_first = false;
-                            else if (b == 0xffff) a_first = true;
-                            else a_first = rs_before(vals[a], a, vals[b], b);
-                            bool up = (i & kk) == 0;
-                            if (up ? !a_first : a_first) { sidx[i] = (uint16_t)b; sidx[ixj] = (uint16_t)a; }
-                        }
-                    }
-                    __syncthreads();
-                }
-            }
-        }
+        for (int e = 0; e < EMAX; e++)
+            if (pk[e] != 0xffffffffu) sidx[pk[e]] = (uint16_t)(tid + e * RS_T);
         __syncthreads();
         // ---- phase G: write ids (16-byte stores on the aligned body)
         {
@@ -551,8 +494,6 @@ row_sort_global_kernel(const double *__restrict__ S, int64_t n64, int32_t *__res
     uint32_t *cnt = reinterpret_cast<uint32_t *>(rs_smem);   // NB+1 (if it fits) else global
     __shared__ double spl[RS_PMAX], ub[RS_PMAX + 1], scl[RS_PMAX + 1];
     __shared__ double red[64];
-    __shared__ int nbig, slow;
-    __shared__ int big_s0[256], big_n[256];
     __shared__ PwTree<PW_MAXNODES> tree;
     __shared__ double pwval[PW_MAXNODES];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -579,7 +520,6 @@ row_sort_global_kernel(const double *__restrict__ S, int64_t n64, int32_t *__res
             mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         }
         if (lane == 0) { red[warp] = mn; red[32 + warp] = mx; }
-        if (tid == 0) { nbig = 0; slow = 0; }
         __syncthreads();
         if (warp == 0) {
             double a = red[lane], b = red[32 + lane];
@@ -687,79 +627,26 @@ row_sort_global_kernel(const double *__restrict__ S, int64_t n64, int32_t *__res
             out[gcnt[grank[j]] + (uint32_t)gidx[j]] = j;
         }
         __syncthreads();
-        for (int b = tid; b < NB; b += RS_T) {
-            int s0 = (int)gcnt[b], s1 = (int)gcnt[b + 1];
-            int s = s1 - s0;
-            if (s <= 1) continue;
-            if (s <= 16) {
-                for (int k = s0 + 1; k < s1; k++) {
-                    int key = out[k];
-                    double xk = __ldg(row + key);
-                    int q = k - 1;
-                    while (q >= s0) {
-                        int o = out[q];
-                        if (!rs_before(xk, key, __ldg(row + o), o)) break;
-                        out[q + 1] = o;
-                        q--;
-                    }
-                    out[q + 1] = key;
+        for (int j = tid; j < n; j += RS_T) {
+            if (j == v) continue;
+            const int b = (int)grank[j];
+            const int s0 = (int)gcnt[b], s1 = (int)gcnt[b + 1];
+            int rank = 0;
+            if (s1 - s0 > 1) {
+                const double xj = __ldg(row + j);
+                for (int k = s0; k < s1; k++) {
+                    const int o = out[k];
+                    rank += rs_before(__ldg(row + o), o, xj, j);
                 }
-            } else if (s <= 256) {
-                int slot = atomicAdd(&nbig, 1);
-                if (slot < 256) { big_s0[slot] = s0; big_n[slot] = s; }
-                else atomicExch(&slow, 1);
-            } else {
-                atomicExch(&slow, 1);
             }
+            gidx[j] = s0 + rank;
         }
         __syncthreads();
-        if (!slow) {
-            for (int g = warp; g < nbig; g += RS_T / 32) {
-                int s0 = big_s0[g], s = big_n[g];
-                int id[8];
-                double x[8];
-                int rk[8];
-#pragma unroll
-                for (int e = 0; e < 8; e++) {
-                    int k = lane + 32 * e;
-                    id[e] = k < s ? out[s0 + k] : 0;
-                    x[e] = k < s ? __ldg(row + id[e]) : 0.0;
-                    rk[e] = 0;
-                }
-                for (int l = 0; l < s; l++) {
-                    int il = out[s0 + l];
-                    double xl = __ldg(row + il);
-#pragma unroll
-                    for (int e = 0; e < 8; e++) rk[e] += rs_before(xl, il, x[e], id[e]);
-                }
-                __syncwarp();
-#pragma unroll
-                for (int e = 0; e < 8; e++)
-                    if (lane + 32 * e < s) out[s0 + rk[e]] = id[e];
-                __syncwarp();
-            }
-        } else {
-            // degenerate row: rank every big bucket by brute force over the bucket
-            for (int b = warp; b < NB; b += RS_T / 32) {
-                int s0 = (int)gcnt[b], s1 = (int)gcnt[b + 1];
-                int s = s1 - s0;
-                if (s <= 16) continue;
-                for (int k0 = 0; k0 < s; k0 += 32) {
-                    int k = k0 + lane;
-                    int id = k < s ? out[s0 + k] : 0;
-                    double x = k < s ? __ldg(row + id) : 0.0;
-                    int rk = 0;
-                    for (int l = 0; l < s; l++) {
-                        int il = out[s0 + l];
-                        rk += rs_before(__ldg(row + il), il, x, id);
-                    }
-                    if (k < s) gidx[s0 + rk] = id;
-                }
-                __syncwarp();
-                for (int k = lane; k < s; k += 32) out[s0 + k] = gidx[s0 + k];
-                __syncwarp();
-            }
+        for (int j = tid; j < n; j += RS_T) {
+            if (j == v) continue;
+            out[gidx[j]] = j;
         }
+        __syncthreads();
         if (rowsum) {
             double root = pw_eval(tree, pwval, [&](int i) { return __ldg(row + i); });
             if (tid == 0) rowsum[v] = __dsub_rn(root, row[v]);

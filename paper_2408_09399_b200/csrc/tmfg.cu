@@ -1,0 +1,738 @@
+// tmfg.cu -- the lazy-gain (heap) TMFG insertion loop as one persistent CTA.
+//
+// Replaces tmfg.py:344-436 build_tmfg_heap with its helpers tmfg.py:94-144
+// (_GraphAccum), 147-182 (TmfgState, refresh_max_corr), 266-277
+// (_best_candidate).  Output is bit-identical: the same trace, edges, faces and
+// debug counters as heapq over (-gain, fid, cand).
+//
+// Why the result is exact although work is speculative:
+//   * every heap entry is (g, fid, cand) with fid unique among live entries, so
+//     the pop sequence depends only on the SET of keys (g desc, fid asc): any
+//     priority structure with that order pops the same sequence;
+//   * refresh_max_corr(w) = first uninserted id of order[w] (cursors only skip
+//     inserted ids), a pure function of the inserted set I.  Hence the
+//     refreshed entry of a face, entry(face, I), is pure too: between two
+//     insertions I is fixed and all stale entries near the top of the heap can
+//     be refreshed IN PARALLEL, then the sequential pop/re-push sequence is
+//     replayed exactly by a short scan (a stale pop pushes a fresh entry; the
+//     first fresh thing on top wins).
+//
+// One round = [parallel] refresh the top-K stale entries and build the entries
+// of the 3 faces created by the last insertion (cursor scans: one 128-byte
+// warp load of order[w] + a ballot against the inserted bitmap in shared
+// memory; gains: 9 fp64 loads of S, summed (S[a,u]+S[b,u])+S[c,u] with
+// __dadd_rn) -> [one thread] replay the pops -> [block] update the queue and
+// insert the winner.  About two dependent global-load latencies per insertion.
+//
+// Priority queue: the top B entries live sorted in shared memory (double
+// buffered, merge-path insertion); the rest sit unsorted in a global pool whose
+// keys are all below the buffer's; the buffer is refilled by a radix select
+// over the pool when it runs short.
+#include "common.cuh"
+
+namespace {
+
+constexpr int TM_T = 1024;
+constexpr int TM_WARPS = TM_T / 32;
+constexpr int TM_NEW_WARPS = 4;                 // warps that build new-face entries
+constexpr int TM_K = 2 * (TM_WARPS - TM_NEW_WARPS);  // top-K speculated per round (56)
+constexpr int TM_B = 1024;                      // shared-memory queue capacity
+constexpr int TM_BATCH = TM_K + 8;
+
+struct Ent {
+    double g;
+    int fid;
+    int cand;
+    int a, b, c;
+    int opt;     // check mode: g >= max over uninserted u of the face gain - 1e-12
+};
+
+__device__ __forceinline__ bool ent_gt(const Ent &x, const Ent &y) {
+    // x pops before y: heapq order of (-g, fid)
+    return x.g > y.g || (x.g == y.g && x.fid < y.fid);
+}
+
+struct Ctl {
+    int size;        // entries in the shared buffer
+    int sel;         // which half of the double buffer is current
+    int rem;         // uninserted vertices
+    int nt;          // trace rows written
+    int nf;          // faces created
+    int ne_count;    // fresh entries built last round (not yet queued)
+    int ne_fid[4];
+    int ne_v[4][3];
+    int L_count;
+    int removed;     // buffer head entries consumed by the scan
+    int nbatch;
+    int nbuf_new;    // batch entries headed for the buffer
+    int exhausted;
+    int winner;      // 0 none, 1 yes
+    Ent win;
+    long long pops, refreshes, gain_inc;
+    int pool_count;
+    int pool_has_max;
+    Ent pool_max;
+    int refill_take;
+    int psel;        // which pool array is current
+    int nsurv;
+    int stop;
+    unsigned long long sel_prefix;
+    int sel_room;
+    int hist[256];
+    int done;
+    int bad;
+};
+
+struct TmArgs {
+    const double *S;
+    const int32_t *order;
+    int n;
+    const int32_t *clique;
+    int32_t *trace;
+    int32_t *host_fid;
+    int32_t *edges;
+    int32_t *faces;
+    int64_t *stats;
+    int4 *fv;            // face vertices (a, b, c) + alive flag, 3n entries
+    Ent *pool;           // global pool, capacity 3n (two arrays, swapped on compaction)
+    Ent *pool2;
+    int32_t *gcursor;    // global cursors when n > 65536
+    int check;           // check_invariants mode (tmfg.py:375-399)
+};
+
+__device__ __forceinline__ bool is_ins(const uint32_t *bits, int v) { return (bits[v >> 5] >> (v & 31)) & 1u; }
+
+template <bool SMEM_CURSORS>
+__device__ __forceinline__ int cur_get(const uint16_t *sc, const int32_t *gc, int w) {
+    if (SMEM_CURSORS) return sc[w];
+    return gc[w];
+}
+template <bool SMEM_CURSORS>
+__device__ __forceinline__ void cur_set(uint16_t *sc, int32_t *gc, int w, int c) {
+    if (SMEM_CURSORS) sc[w] = (uint16_t)c;
+    else gc[w] = c;
+}
+
+// One warp builds up to two entries: refresh the 3 vertices of each face
+// (first uninserted id of order[w]) and pick the best candidate.
+template <bool SMEM_CURSORS>
+__device__ void warp_entries(const TmArgs &A, const uint32_t *bits, uint16_t *sc, int cnt, const int (*fverts)[3],
+                             const int *fids, Ent *out) {
+    const int lane = threadIdx.x & 31;
+    const int n = A.n, m = n - 1;
+    int vv[6], cur[6], found[6];
+    const int nv = 3 * cnt;
+#pragma unroll
+    for (int k = 0; k < 6; k++) {
+        vv[k] = k < nv ? fverts[k / 3][k % 3] : 0;
+        cur[k] = k < nv ? cur_get<SMEM_CURSORS>(sc, A.gcursor, vv[k]) : 0;
+        found[k] = -1;
+    }
+    unsigned pending = (1u << nv) - 1u;
+    while (pending) {
+        int val[6];
+#pragma unroll
+        for (int k = 0; k < 6; k++) {
+            val[k] = -1;
+            if ((pending >> k) & 1u) {
+                int idx = cur[k] + lane;
+                if (idx < m) val[k] = __ldg(A.order + (int64_t)vv[k] * m + idx);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 6; k++) {
+            if ((pending >> k) & 1u) {
+                bool ok = val[k] >= 0 && !is_ins(bits, val[k]);
+                unsigned b = __ballot_sync(0xffffffffu, ok);
+                if (b) {
+                    int f = __ffs(b) - 1;
+                    found[k] = __shfl_sync(0xffffffffu, val[k], f);
+                    cur[k] += f;
+                    pending &= ~(1u << k);
+                } else {
+                    cur[k] += 32;
+                    if (cur[k] >= m) pending &= ~(1u << k);  // cannot happen while rem > 0
+                }
+            }
+        }
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < 6; k++)
+            if (k < nv) cur_set<SMEM_CURSORS>(sc, A.gcursor, vv[k], cur[k]);
+    }
+    // 9 similarity loads per entry: lane = e*9 + ci*3 + vi
+    double sv = 0.0;
+    if (lane < 9 * cnt) {
+        int e = lane / 9, r = lane % 9, ci = r / 3, vi = r % 3;
+        int u = found[e * 3 + ci];
+        int w = vv[e * 3 + vi];
+        sv = (u >= 0) ? __ldg(A.S + (int64_t)w * n + u) : 0.0;
+    }
+    double s[18];
+#pragma unroll
+    for (int q = 0; q < 18; q++) s[q] = __shfl_sync(0xffffffffu, sv, q);
+    if (lane == 0) {
+        for (int e = 0; e < cnt; e++) {
+            double best_g = -INFINITY;
+            int best_v = -1;
+            for (int ci = 0; ci < 3; ci++) {
+                int u = found[e * 3 + ci];
+                double g = __dadd_rn(__dadd_rn(s[e * 9 + ci * 3 + 0], s[e * 9 + ci * 3 + 1]), s[e * 9 + ci * 3 + 2]);
+                if (g > best_g || (g == best_g && u < best_v)) { best_g = g; best_v = u; }
+            }
+            Ent x;
+            x.g = best_g;
+            x.fid = fids[e];
+            x.cand = best_v;
+            x.a = fverts[e][0];
+            x.b = fverts[e][1];
+            x.c = fverts[e][2];
+            x.opt = 0;
+            out[e] = x;
+        }
+    }
+    if (A.check) {
+        // tmfg.py:377-380 true_best_gain: brute force over every uninserted vertex
+        for (int e = 0; e < cnt; e++) {
+            const double *Sa = A.S + (int64_t)fverts[e][0] * n;
+            const double *Sb = A.S + (int64_t)fverts[e][1] * n;
+            const double *Sc = A.S + (int64_t)fverts[e][2] * n;
+            double best = -INFINITY;
+            for (int u = lane; u < n; u += 32) {
+                if (is_ins(bits, u)) continue;
+                double g = __dadd_rn(__dadd_rn(Sa[u], Sb[u]), Sc[u]);
+                best = fmax(best, g);
+            }
+            for (int o = 16; o; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
+            __syncwarp();
+            if (lane == 0) out[e].opt = out[e].g >= __dsub_rn(best, 1e-12);
+            __syncwarp();
+        }
+    }
+}
+
+__device__ __forceinline__ void sort3(int &x, int &y, int &z) {
+    int t;
+    if (y < x) { t = x; x = y; y = t; }
+    if (z < y) { t = y; y = z; z = t; }
+    if (y < x) { t = x; x = y; y = t; }
+}
+
+__device__ __forceinline__ unsigned long long ent_key_hi(const Ent &e) { return tg_order_key(e.g); }
+__device__ __forceinline__ unsigned long long ent_key_lo(const Ent &e) { return ~(unsigned long long)(unsigned)e.fid; }
+
+
+// Move the largest pool entries into the (short) shared buffer.  Threshold by
+// a most-significant-digit radix walk over the 96-bit key (gain, ~fid): stop at
+// the first digit boundary whose "all keys above" set is non-empty and fits.
+// Keys are unique, the pool order is irrelevant, so the result is exact.
+template <int NT>
+__device__ void refill(const TmArgs &A, Ctl &ctl, Ent *cur, Ent *scratch, Ent *red_e, int *red_ok) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    Ent *pool = ctl.psel ? A.pool2 : A.pool;
+    Ent *other = ctl.psel ? A.pool : A.pool2;
+    const int P = ctl.pool_count;
+    const int room = min(TM_B - ctl.size, TM_B / 2);
+    unsigned long long thr_hi = 0ull, thr_lo = 0ull;
+    bool take_all = P <= room;
+    if (!take_all) {
+        if (tid == 0) { ctl.sel_prefix = 0ull; ctl.sel_room = room; ctl.stop = 0; }
+        __syncthreads();
+        for (int pass = 0; pass < 16; pass++) {
+            const bool lo_part = pass >= 8;
+            const int p = pass & 7;
+            const int shift = 56 - 8 * p;
+            for (int i = tid; i < 256; i += NT) ctl.hist[i] = 0;
+            __syncthreads();
+            const unsigned long long pref = ctl.sel_prefix;
+            for (int i = tid; i < P; i += NT) {
+                Ent x = pool[i];
+                unsigned long long kh = ent_key_hi(x), kl = ent_key_lo(x);
+                unsigned long long key = lo_part ? kl : kh;
+                bool match = lo_part ? (kh == thr_hi) : true;
+                if (p > 0) match = match && ((key >> (64 - 8 * p)) == (pref >> (64 - 8 * p)));
+                if (match) atomicAdd(&ctl.hist[(key >> shift) & 255], 1);
+            }
+            __syncthreads();
+            if (tid == 0) {
+                int acc = 0, d = 255, last_fit = -1;
+                for (; d >= 0; d--) {
+                    if (acc + ctl.hist[d] > ctl.sel_room) break;
+                    acc += ctl.hist[d];
+                    if (ctl.hist[d]) last_fit = d;
+                }
+                if (acc > 0) {
+                    // take every key whose digit here is >= last_fit (within the prefix group)
+                    ctl.sel_prefix = pref | ((unsigned long long)last_fit << shift);
+                    ctl.stop = 1;
+                } else {
+                    // the top non-empty bin alone is too large: refine inside it
+                    ctl.sel_prefix = pref | ((unsigned long long)d << shift);
+                }
+            }
+            __syncthreads();
+            if (ctl.stop) {
+                if (!lo_part) { thr_hi = ctl.sel_prefix; thr_lo = 0ull; }
+                else thr_lo = ctl.sel_prefix;
+                break;
+            }
+            if (pass == 7) {
+                thr_hi = ctl.sel_prefix;
+                __syncthreads();
+                if (tid == 0) ctl.sel_prefix = 0ull;
+                __syncthreads();
+            }
+        }
+        if (!ctl.stop) thr_lo = ctl.sel_prefix;
+    }
+    __syncthreads();
+    if (tid == 0) { ctl.refill_take = 0; ctl.nsurv = 0; }
+    __syncthreads();
+    Ent best;
+    bool ok = false;
+    for (int i = tid; i < P; i += NT) {
+        Ent x = pool[i];
+        unsigned long long kh = ent_key_hi(x), kl = ent_key_lo(x);
+        bool take = take_all || kh > thr_hi || (kh == thr_hi && kl >= thr_lo);
+        if (take) {
+            scratch[atomicAdd(&ctl.refill_take, 1)] = x;
+        } else {
+            other[atomicAdd(&ctl.nsurv, 1)] = x;
+            if (!ok || ent_gt(x, best)) { best = x; ok = true; }
+        }
+    }
+    for (int o = 16; o; o >>= 1) {
+        Ent y;
+        y.g = __shfl_xor_sync(0xffffffffu, best.g, o);
+        y.fid = __shfl_xor_sync(0xffffffffu, best.fid, o);
+        int yok = __shfl_xor_sync(0xffffffffu, (int)ok, o);
+        if (yok && (!ok || ent_gt(y, best))) { best.g = y.g; best.fid = y.fid; ok = true; }
+    }
+    if (lane == 0) { red_e[warp] = best; red_ok[warp] = ok; }
+    __syncthreads();
+    const int nt = ctl.refill_take;
+    const int sz = ctl.size;
+    for (int i = tid; i < nt; i += NT) {
+        Ent x = scratch[i];
+        int rank = 0;
+        for (int j = 0; j < nt; j++) rank += ent_gt(scratch[j], x);
+        cur[sz + rank] = x;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        ctl.size = sz + nt;
+        ctl.pool_count = ctl.nsurv;
+        ctl.psel ^= 1;
+        bool any = false;
+        Ent b;
+        for (int w = 0; w < NT / 32; w++)
+            if (red_ok[w] && (!any || ent_gt(red_e[w], b))) { b = red_e[w]; any = true; }
+        ctl.pool_has_max = any;
+        if (any) ctl.pool_max = b;
+    }
+    __syncthreads();
+}
+
+template <bool SMEM_CURSORS>
+__global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
+    extern __shared__ __align__(16) unsigned char tm_smem[];
+    const int n = A.n;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __shared__ Ctl ctl;
+    __shared__ Ent L[TM_K];
+    __shared__ Ent Lref[TM_K];
+    __shared__ int Lstale[TM_K];
+    __shared__ Ent NE[4];
+    __shared__ Ent batch[TM_BATCH];
+    __shared__ Ent tobuf[TM_BATCH];
+    __shared__ Ent red_e[TM_WARPS];
+    __shared__ int red_ok[TM_WARPS];
+
+    Ent *buf0 = reinterpret_cast<Ent *>(tm_smem);
+    Ent *buf1 = buf0 + TM_B;
+    uint32_t *bits = reinterpret_cast<uint32_t *>(buf1 + TM_B);
+    const int nwords = (n + 31) >> 5;
+    uint16_t *sc = reinterpret_cast<uint16_t *>(bits + nwords);
+
+    for (int i = tid; i < nwords; i += TM_T) bits[i] = 0u;
+    if (SMEM_CURSORS) {
+        for (int i = tid; i < n; i += TM_T) sc[i] = 0;
+    } else {
+        for (int i = tid; i < n; i += TM_T) A.gcursor[i] = 0;
+    }
+    for (int i = tid; i < 3 * n; i += TM_T) A.fv[i] = make_int4(0, 0, 0, 0);
+    __syncthreads();
+    if (tid == 0) {
+        int a = A.clique[0], b = A.clique[1], c = A.clique[2], d = A.clique[3];
+        int e0[6][2] = {{a, b}, {a, c}, {a, d}, {b, c}, {b, d}, {c, d}};
+        for (int k = 0; k < 6; k++) { A.edges[2 * k] = e0[k][0]; A.edges[2 * k + 1] = e0[k][1]; }
+        int fcs[4][3] = {{a, b, c}, {a, b, d}, {a, c, d}, {b, c, d}};
+        for (int f = 0; f < 4; f++) {
+            A.fv[f] = make_int4(fcs[f][0], fcs[f][1], fcs[f][2], 1);
+            ctl.ne_fid[f] = f;
+            for (int q = 0; q < 3; q++) ctl.ne_v[f][q] = fcs[f][q];
+        }
+        bits[a >> 5] |= 1u << (a & 31);
+        bits[b >> 5] |= 1u << (b & 31);
+        bits[c >> 5] |= 1u << (c & 31);
+        bits[d >> 5] |= 1u << (d & 31);
+        ctl.size = 0;
+        ctl.sel = 0;
+        ctl.rem = n - 4;
+        ctl.nt = 0;
+        ctl.nf = 4;
+        ctl.ne_count = (n > 4) ? 4 : 0;
+        ctl.L_count = 0;
+        ctl.pops = ctl.refreshes = ctl.gain_inc = 0;
+        ctl.pool_count = 0;
+        ctl.pool_has_max = 0;
+        ctl.psel = 0;
+        ctl.done = (n <= 4);
+        ctl.bad = 0;
+    }
+    __syncthreads();
+
+    while (!ctl.done) {
+        // ================= parallel phase: new-face entries + speculative refresh of the top-K
+        {
+            Ent *cur = ctl.sel ? buf1 : buf0;
+            if (warp < TM_NEW_WARPS) {
+                if (warp < ctl.ne_count) {
+                    int fids[1] = {ctl.ne_fid[warp]};
+                    int fvv[1][3] = {{ctl.ne_v[warp][0], ctl.ne_v[warp][1], ctl.ne_v[warp][2]}};
+                    warp_entries<SMEM_CURSORS>(A, bits, sc, 1, fvv, fids, &NE[warp]);
+                }
+            } else {
+                int base = 2 * (warp - TM_NEW_WARPS);
+                int cntL = ctl.L_count;
+                int idx[2];
+                int cnt = 0;
+                int fids[2];
+                int fvv[2][3];
+                for (int q = 0; q < 2; q++) {
+                    int i = base + q;
+                    if (i < cntL) {
+                        Ent h = cur[i];
+                        bool stale = is_ins(bits, h.cand);
+                        if (lane == 0) { L[i] = h; Lstale[i] = stale; }
+                        if (stale) {
+                            idx[cnt] = i;
+                            fids[cnt] = h.fid;
+                            fvv[cnt][0] = h.a;
+                            fvv[cnt][1] = h.b;
+                            fvv[cnt][2] = h.c;
+                            cnt++;
+                        }
+                    }
+                }
+                if (cnt) {
+                    Ent outs[2];
+                    warp_entries<SMEM_CURSORS>(A, bits, sc, cnt, fvv, fids, outs);
+                    if (lane == 0)
+                        for (int q = 0; q < cnt; q++) Lref[idx[q]] = outs[q];
+                }
+            }
+        }
+        __syncthreads();
+        // ================= replay the pops (one thread)
+        if (tid == 0) {
+            int nec = ctl.ne_count;
+            // new entries sorted in pop order
+            for (int i = 1; i < nec; i++) {
+                Ent x = NE[i];
+                int j = i - 1;
+                while (j >= 0 && ent_gt(x, NE[j])) { NE[j + 1] = NE[j]; j--; }
+                NE[j + 1] = x;
+            }
+            int ne_ptr = 0;
+            bool ev = false;
+            Ent eb;
+            int eb_idx = -1;
+            int removed = 0;
+            int kind = 0;  // 1 = L entry, 2 = refreshed entry, 3 = new entry
+            int widx = -1;
+            long long pops = 0, refr = 0, ginc = 0;
+            const int Lc = ctl.L_count;
+            for (int i = 0; i < Lc; i++) {
+                Ent h = L[i];
+                int k = 1;
+                Ent top = h;
+                if (ne_ptr < nec && ent_gt(NE[ne_ptr], top)) { top = NE[ne_ptr]; k = 3; }
+                if (ev && ent_gt(eb, top)) { top = eb; k = 2; }
+                pops++;
+                if (k == 3) { kind = 3; widx = ne_ptr; break; }
+                if (k == 2) { kind = 2; widx = eb_idx; break; }
+                removed++;
+                if (!Lstale[i]) { kind = 1; widx = i; break; }
+                refr++;
+                Ent r = Lref[i];
+                if (r.g > __dadd_rn(h.g, 1e-12)) {
+                    ginc++;
+                    if (A.check && r.opt && !ctl.bad) {
+                        // tmfg.py:429 assertion: a refreshed optimal pair gained
+                        ctl.bad = 2;
+                        A.stats[4] = r.fid;
+                        A.stats[5] = __double_as_longlong(h.g);
+                        A.stats[6] = __double_as_longlong(r.g);
+                        ctl.pops += pops;
+                        ctl.refreshes += refr;
+                        ctl.gain_inc += ginc;
+                        pops = refr = ginc = 0;
+                        kind = -1;
+                        break;
+                    }
+                }
+                if (!ev || ent_gt(r, eb)) { eb = r; eb_idx = i; ev = true; }
+            }
+            bool more = (ctl.size > Lc) || (ctl.pool_count > 0);
+            if (kind == -1) kind = 0;
+            else if (kind == 0 && !more) {
+                // queue exhausted: the best of the refreshed and new entries pops
+                bool have_ne = ne_ptr < nec;
+                if (have_ne && (!ev || ent_gt(NE[ne_ptr], eb))) { kind = 3; widx = ne_ptr; }
+                else if (ev) { kind = 2; widx = eb_idx; }
+                if (kind) pops++;
+                else ctl.bad = 1;
+            }
+            ctl.pops += pops;
+            ctl.refreshes += refr;
+            ctl.gain_inc += ginc;
+            ctl.removed = removed;
+            ctl.exhausted = (kind == 0);
+            ctl.winner = (kind != 0);
+            if (kind == 1) ctl.win = L[widx];
+            else if (kind == 2) ctl.win = Lref[widx];
+            else if (kind == 3) ctl.win = NE[widx];
+            // batch of entries to (re)queue
+            int nb = 0;
+            for (int i = 0; i < removed; i++)
+                if (Lstale[i] && !(kind == 2 && i == widx)) batch[nb++] = Lref[i];
+            for (int i = 0; i < nec; i++)
+                if (!(kind == 3 && i == widx)) batch[nb++] = NE[i];
+            // split: above the pool max -> shared buffer, else -> pool
+            int nbuf = 0;
+            for (int i = 0; i < nb; i++) {
+                if (!ctl.pool_has_max || ent_gt(batch[i], ctl.pool_max)) {
+                    Ent x = batch[i];
+                    int j = nbuf - 1;
+                    while (j >= 0 && ent_gt(x, tobuf[j])) { tobuf[j + 1] = tobuf[j]; j--; }
+                    tobuf[j + 1] = x;
+                    nbuf++;
+                } else {
+                    (ctl.psel ? A.pool2 : A.pool)[ctl.pool_count++] = batch[i];
+                }
+            }
+            ctl.nbuf_new = nbuf;
+            ctl.nbatch = nb;
+        }
+        __syncthreads();
+        // ================= merge: buffer[removed..size) + tobuf -> other half
+        {
+            Ent *cur = ctl.sel ? buf1 : buf0;
+            Ent *nxt = ctl.sel ? buf0 : buf1;
+            const int r = ctl.removed, sz = ctl.size, nb = ctl.nbuf_new;
+            const int old = sz - r;
+            for (int i = tid; i < old; i += TM_T) {
+                Ent x = cur[r + i];
+                int lo = 0, hi = nb;  // # of tobuf entries popping before x
+                while (lo < hi) {
+                    int mid = (lo + hi) >> 1;
+                    if (ent_gt(tobuf[mid], x)) lo = mid + 1;
+                    else hi = mid;
+                }
+                int pos = i + lo;
+                if (pos < TM_B) nxt[pos] = x;
+                else {
+                    Ent *pool = ctl.psel ? A.pool2 : A.pool;
+                    pool[atomicAdd(&ctl.pool_count, 1)] = x;
+                    if (pos == TM_B) { ctl.pool_max = x; ctl.pool_has_max = 1; }
+                }
+            }
+            for (int k = tid; k < nb; k += TM_T) {
+                Ent x = tobuf[k];
+                int lo = 0, hi = old;  // # of old entries popping before x
+                while (lo < hi) {
+                    int mid = (lo + hi) >> 1;
+                    if (ent_gt(cur[r + mid], x)) lo = mid + 1;
+                    else hi = mid;
+                }
+                int pos = k + lo;
+                if (pos < TM_B) nxt[pos] = x;
+                else {
+                    Ent *pool = ctl.psel ? A.pool2 : A.pool;
+                    pool[atomicAdd(&ctl.pool_count, 1)] = x;
+                    if (pos == TM_B) { ctl.pool_max = x; ctl.pool_has_max = 1; }
+                }
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int total = ctl.size - ctl.removed + ctl.nbuf_new;
+            if (total > TM_B) {
+                // spilled entries are the smallest of the buffer: the pool max is
+                // the largest spilled one, i.e. the entry right after the kept tail
+                total = TM_B;
+            }
+            ctl.size = total;
+            ctl.sel ^= 1;
+        }
+        __syncthreads();
+        // ================= insert the winner
+        if (tid == 0) {
+            ctl.ne_count = 0;
+            if (ctl.winner) {
+                Ent w = ctl.win;
+                int v = w.cand, fid = w.fid;
+                int a = w.a, b = w.b, c = w.c;
+                int t = ctl.nt;
+                A.trace[4 * t] = v;
+                A.trace[4 * t + 1] = a;
+                A.trace[4 * t + 2] = b;
+                A.trace[4 * t + 3] = c;
+                A.host_fid[t] = fid;
+                int e = 6 + 3 * t;
+                int wv[3] = {a, b, c};
+                for (int q = 0; q < 3; q++) {
+                    A.edges[2 * (e + q)] = min(wv[q], v);
+                    A.edges[2 * (e + q) + 1] = max(wv[q], v);
+                }
+                int4 old = A.fv[fid];
+                A.fv[fid] = make_int4(old.x, old.y, old.z, 0);
+                int f0 = ctl.nf;
+                int ch[3][3] = {{v, a, b}, {v, a, c}, {v, b, c}};
+                for (int q = 0; q < 3; q++) {
+                    int x = ch[q][0], y = ch[q][1], z = ch[q][2];
+                    sort3(x, y, z);
+                    A.fv[f0 + q] = make_int4(x, y, z, 1);
+                    ctl.ne_fid[q] = f0 + q;
+                    ctl.ne_v[q][0] = x;
+                    ctl.ne_v[q][1] = y;
+                    ctl.ne_v[q][2] = z;
+                }
+                ctl.nf = f0 + 3;
+                bits[v >> 5] |= 1u << (v & 31);
+                ctl.nt = t + 1;
+                ctl.rem -= 1;
+                if (ctl.rem == 0) ctl.done = 1;
+                else ctl.ne_count = 3;
+            }
+            if (ctl.bad) ctl.done = 1;
+        }
+        __syncthreads();
+        if (ctl.done) break;
+        // ================= refill the shared buffer from the pool when short
+        if (ctl.size < TM_K && ctl.pool_count > 0) {
+            refill<TM_T>(A, ctl, ctl.sel ? buf1 : buf0, ctl.sel ? buf0 : buf1, red_e, red_ok);
+        }
+        if (tid == 0) ctl.L_count = min(TM_K, ctl.size);
+        __syncthreads();
+    }
+    __syncthreads();
+    // ================= alive faces in creation order
+    {
+        const int nf = ctl.nf;
+        __shared__ int wsum[TM_WARPS];
+        __shared__ int carry;
+        if (tid == 0) carry = 0;
+        __syncthreads();
+        for (int base = 0; base < nf; base += TM_T) {
+            int f = base + tid;
+            int4 x = f < nf ? A.fv[f] : make_int4(0, 0, 0, 0);
+            int alive = (f < nf) ? x.w : 0;
+            unsigned bal = __ballot_sync(0xffffffffu, alive);
+            int pre = __popc(bal & ((1u << lane) - 1u));
+            if (lane == 0) wsum[warp] = __popc(bal);
+            __syncthreads();
+            int off = carry;
+            for (int w = 0; w < warp; w++) off += wsum[w];
+            if (alive) {
+                int k = off + pre;
+                A.faces[3 * k] = x.x;
+                A.faces[3 * k + 1] = x.y;
+                A.faces[3 * k + 2] = x.z;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                int s = 0;
+                for (int w = 0; w < TM_WARPS; w++) s += wsum[w];
+                carry += s;
+            }
+            __syncthreads();
+        }
+    }
+    if (tid == 0) {
+        A.stats[0] = ctl.pops;
+        A.stats[1] = ctl.refreshes;
+        A.stats[2] = ctl.gain_inc;
+        A.stats[3] = ctl.bad;
+    }
+}
+
+size_t tm_smem_bytes(int64_t n, bool smem_cursors) {
+    size_t b = (size_t)2 * TM_B * sizeof(Ent);
+    b += (size_t)((n + 31) / 32) * 4;
+    if (smem_cursors) b += (size_t)n * 2;
+    return tg_align_up(b, 16) + 64;
+}
+
+__global__ void edge_weights_kernel(const double *__restrict__ S, int64_t n, const int32_t *__restrict__ edges,
+                                    int64_t m, double *__restrict__ w) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) w[i] = S[(int64_t)edges[2 * i] * n + edges[2 * i + 1]];
+}
+
+}  // namespace
+
+TG_API int tg_edge_weights(const double *S, int64_t n, const int32_t *edges, int64_t m, double *w, void *stream) {
+    if (!S || !edges || !w || m < 0) return TG_ERR_ARG;
+    if (m == 0) return TG_OK;
+    edge_weights_kernel<<<(unsigned)((m + 255) / 256), 256, 0, tg_stream(stream)>>>(S, n, edges, m, w);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+TG_API size_t tg_tmfg_workspace_bytes(int64_t n) {
+    size_t b = 0;
+    b += tg_align_up((size_t)3 * n * sizeof(int4), 256);
+    b += tg_align_up((size_t)(3 * n + TM_B + 64) * sizeof(Ent), 256);
+    b += tg_align_up((size_t)n * sizeof(int32_t), 256);
+    b += tg_align_up((size_t)(3 * n + TM_B + 64) * sizeof(Ent), 256);
+    return b + 1024;
+}
+
+TG_API int tg_tmfg_heap(const double *S, const int32_t *order, int64_t n, const int32_t *clique, int32_t *trace,
+                        int32_t *host_fid, int32_t *edges, int32_t *faces, int64_t *stats, int32_t check,
+                        void *ws, size_t ws_bytes, void *stream) {
+    if (n < 4 || !S || !order || !clique || !edges || !faces || !stats) return TG_ERR_ARG;
+    if (ws_bytes < tg_tmfg_workspace_bytes(n)) return TG_ERR_WORKSPACE;
+    TgArena ar(ws, ws_bytes);
+    TmArgs A;
+    A.S = S;
+    A.order = order;
+    A.n = (int)n;
+    A.clique = clique;
+    A.trace = trace;
+    A.host_fid = host_fid;
+    A.edges = edges;
+    A.faces = faces;
+    A.stats = stats;
+    A.check = check;
+    A.fv = ar.take<int4>((size_t)3 * n);
+    A.pool = ar.take<Ent>((size_t)3 * n + TM_B + 64);
+    A.pool2 = ar.take<Ent>((size_t)3 * n + TM_B + 64);
+    A.gcursor = ar.take<int32_t>((size_t)n);
+    if (!A.fv || !A.pool || !A.pool2 || !A.gcursor) return TG_ERR_WORKSPACE;
+    cudaStream_t st = tg_stream(stream);
+    bool smem_cur = n <= 65536;
+    size_t smem = tm_smem_bytes(n, smem_cur);
+    if (smem_cur) {
+        TG_CUDA_CHECK(cudaFuncSetAttribute(tmfg_heap_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        tmfg_heap_kernel<true><<<1, TM_T, smem, st>>>(A);
+    } else {
+        TG_CUDA_CHECK(cudaFuncSetAttribute(tmfg_heap_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        tmfg_heap_kernel<false><<<1, TM_T, smem, st>>>(A);
+    }
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}

@@ -88,7 +88,7 @@ def test_validate_flags(pkg):
         pkg.validate_similarity(bad)
     bad = S.copy()
     bad[1, 2] = bad[2, 1] = 1.5
-    with pytest.raises(pkg.DataError, match="range"):
+    with pytest.raises(pkg.DataError, match="lie in"):
         pkg.validate_similarity(bad)
 
 

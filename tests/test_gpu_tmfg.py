@@ -1,0 +1,75 @@
+"""GPU parity: the persistent heap-TMFG kernel vs the reference goldens and the oracle.
+
+Bit-exact: trace, edges, faces, weights, initial clique and debug_stats.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SMALL = ["n4_u", "n5_flat", "n6_u", "n20_round", "n30_u", "n40_q", "n60_u", "n120_q", "n50_s", "n200_s",
+         "c1_n300", "c4_n400"]
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_2408_09399_b200 as p
+    p._native.load()
+    return p
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_tmfg_matches_golden(name, small_cases, digests, pkg):
+    c = small_cases[name]
+    S = c["S"]
+    lists = pkg.sort_neighbor_lists(S)
+    g = pkg.build_tmfg_heap(S, lists)
+    for key in ("edges", "weights", "trace", "faces", "initial_clique"):
+        assert np.array_equal(getattr(g, key), c[f"tmfg_{key}"]), key
+    rec = digests[name]
+    if "tmfg_stats" in rec:
+        g2 = pkg.build_tmfg_heap(S, lists, check_invariants=True)
+        assert g2.debug_stats == rec["tmfg_stats"]
+        assert np.array_equal(g2.trace, g.trace)
+    elif "tmfg_check_error" in rec:
+        with pytest.raises(AssertionError) as ei:
+            pkg.build_tmfg_heap(S, lists, check_invariants=True)
+        assert str(ei.value) == rec["tmfg_check_error"]
+
+
+@pytest.mark.parametrize("config", [1, 2, 4])
+def test_tmfg_configs_match_reference_hash(config, digests, oracle, pkg):
+    from paper_2408_09399_b200 import synth
+    rec = digests[f"config{config}"]
+    x, _ = synth.generate(config)
+    S = oracle.pearson_similarity(x)
+    lists = pkg.sort_neighbor_lists(S)
+    g = pkg.build_tmfg_heap(S, lists)
+    for key in ("edges", "weights", "trace", "faces"):
+        assert oracle.sha(getattr(g, key)) == rec[f"tmfg_{key}"], key
+
+
+@pytest.mark.parametrize("n,seed", [(7, 1), (33, 2), (257, 3), (1500, 4), (6000, 5)])
+def test_tmfg_vs_oracle_stats(n, seed, oracle, pkg):
+    from paper_2408_09399_b200 import synth
+    x, _ = synth.generate(3, n=n, seed=seed) if n >= 40 else (np.random.default_rng(seed).standard_normal((n, 16)), 0)
+    S = oracle.pearson_similarity(x)
+    ref = oracle.build_tmfg_heap(S, oracle.sort_neighbor_lists(S))
+    lists = pkg.sort_neighbor_lists(S)
+    g = pkg.build_tmfg_heap(S, lists, check_invariants=n <= 1500)
+    for key in ("edges", "trace", "faces"):
+        assert np.array_equal(getattr(g, key), ref[key]), key
+    if g.debug_stats is not None:
+        assert g.debug_stats == ref["stats"]
+
+
+def test_tmfg_nan_raises(pkg):
+    from paper_2408_09399_b200 import synth
+    S = synth.uniform_matrix(30, 1)
+    S[3, 4] = S[4, 3] = np.nan
+    lists = pkg.sort_neighbor_lists(S)
+    with pytest.raises(pkg.DataError, match="NaN"):
+        pkg.build_tmfg_heap(S, lists)
