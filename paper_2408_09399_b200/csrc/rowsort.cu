@@ -7,12 +7,13 @@
 // B200 design (one CTA of 1024 threads per row, persistent over rows):
 //   1. the row (8n bytes) is streamed into shared memory with 16-byte cp.async,
 //      double-buffered so row v+grid loads while row v is sorted;
-//   2. equalised bucketing: 64 splitters sampled from the row (sorted by one
-//      warp) cut it into 65 quantile bins, each split linearly into K
-//      sub-buckets, giving ~2 keys per bucket; bucket ids are monotone in the
-//      value and equal values (incl. -0.0/+0.0) share a bucket;
-//   3. one shared-memory atomicAdd per key yields its rank inside the bucket;
-//      a block scan gives bucket starts and the ids (u16) are scattered once;
+//   2. equalised two-level bucketing: a warp-aggregated histogram over 512
+//      linear bins of [min, max] sizes each bin's share of fine buckets
+//      (ceil(count/2)), and each bin is split linearly again -- about two keys
+//      per fine bucket whatever the value distribution; bucket ids are monotone
+//      in the value and equal values (incl. -0.0/+0.0) share a bucket;
+//   3. one shared-memory atomicAdd per key yields its rank inside the fine
+//      bucket; a block scan gives bucket starts and the ids (u16) are scattered;
 //   4. every key's exact rank inside its bucket (value desc, id asc) is counted
 //      against the other members (independent loads, cost = bucket size), and
 //      the ids are placed once more -- so the result is deterministic even though
@@ -27,7 +28,6 @@
 namespace {
 
 constexpr int RS_T = 1024;
-constexpr int RS_PMAX = 64;
 constexpr int PW_MAXNODES = 2048;   // n <= 131072
 constexpr int PW_SMALLNODES = 512;  // n <= 16384
 
@@ -202,48 +202,48 @@ __device__ __forceinline__ bool rs_before(double xa, int ia, double xb, int ib) 
     return ia < ib;
 }
 
+constexpr int RS_CMAX = 512;   // coarse (linear) bins
+
+__host__ __device__ __forceinline__ int rs_coarse_bins(int m) {
+    int c = m / 4;
+    if (c > RS_CMAX) c = RS_CMAX;
+    if (c < 1) c = 1;
+    return c;
+}
+// fine buckets never exceed C + ceil(m/2) + C
+__host__ __device__ __forceinline__ int rs_fine_cap(int m) { return 2 * rs_coarse_bins(m) + (m + 1) / 2 + 1; }
+
 struct RsPlan {
-    int n, P, K, NB, pow2, nbuf;
-    size_t off_sidx, off_cnt, off_spl, off_ub, off_scl, off_misc, smem;
+    int n, C, NBcap, nbuf, stride;
+    size_t off_sidx, off_fcnt, off_misc, smem;
+};
+
+struct RsMisc {
+    double red[64];
+    double rmin, rmax, cscale;
+    uint32_t ccnt[RS_CMAX + 1];    // coarse counts -> fine base (exclusive scan of f_c)
+    uint32_t cf[RS_CMAX];          // fine buckets per coarse bin
+    uint32_t wsum[32];
 };
 
 __host__ RsPlan rs_plan(int64_t n, int nbuf) {
     RsPlan p;
     p.n = (int)n;
     int m = (int)n - 1;
-    int P = m / 16;
-    if (P > RS_PMAX) P = RS_PMAX;
-    if (P < 1) P = 1;
-    p.P = P;
-    int K = (int)((m + 2 * (P + 1) - 1) / (2 * (P + 1)));
-    if (K < 1) K = 1;
-    p.K = K;
-    p.NB = (P + 1) * K;
-    int pw = 1;
-    while (pw < m) pw <<= 1;
-    p.pow2 = pw;
+    p.C = rs_coarse_bins(m);
+    p.NBcap = rs_fine_cap(m);
     p.nbuf = nbuf;
-    size_t off = tg_align_up((size_t)nbuf * n * sizeof(double), 16);
+    p.stride = (int)((n + 1) & ~1LL);   // keeps the second row buffer 16-byte aligned
+    size_t off = tg_align_up((size_t)nbuf * p.stride * sizeof(double), 16);
     p.off_sidx = off;
     off = tg_align_up(off + (size_t)n * sizeof(uint16_t), 16);
-    p.off_cnt = off;
-    off = tg_align_up(off + (size_t)(p.NB + 1) * sizeof(uint32_t), 16);
-    p.off_spl = off;
-    off = tg_align_up(off + (size_t)RS_PMAX * sizeof(double), 16);
-    p.off_ub = off;
-    off = tg_align_up(off + (size_t)(RS_PMAX + 1) * sizeof(double), 16);
-    p.off_scl = off;
-    off = tg_align_up(off + (size_t)(RS_PMAX + 1) * sizeof(double), 16);
+    p.off_fcnt = off;
+    off = tg_align_up(off + (size_t)(p.NBcap + 1) * sizeof(uint32_t), 16);
     p.off_misc = off;
-    off += 2048;
+    off += tg_align_up(sizeof(RsMisc), 16);
     p.smem = off;
     return p;
 }
-
-struct RsMisc {
-    double red[64];
-    double rmin, rmax;
-};
 
 __device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
     unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -255,8 +255,8 @@ __device__ __forceinline__ void cp_async16g(void *smem, const void *gmem) {
 }
 
 __device__ __forceinline__ void rs_issue_row(double *dst, const double *src, int n) {
-    // 16-byte chunks when the row start is 16-byte aligned, else 8-byte copies
-    if ((((uintptr_t)src) & 15) == 0) {
+    // 16-byte chunks when source and destination are 16-byte aligned, else 8-byte copies
+    if (((((uintptr_t)src) | ((uintptr_t)dst)) & 15) == 0) {
         int nv = n >> 1;
         for (int i = threadIdx.x; i < nv; i += blockDim.x) cp_async16g(dst + 2 * i, src + 2 * i);
         if ((n & 1) && threadIdx.x == 0) cp_async8(dst + n - 1, src + n - 1);
@@ -264,6 +264,22 @@ __device__ __forceinline__ void rs_issue_row(double *dst, const double *src, int
         for (int i = threadIdx.x; i < n; i += blockDim.x) cp_async8(dst + i, src + i);
     }
     asm volatile("cp.async.commit_group;\n" ::);
+}
+
+// coarse bin of x in t-space: t = (rmax - x) * cscale in [0, C]
+__device__ __forceinline__ int rs_coarse_of(double x, double rmax, double cscale, int C, double &t) {
+    if (isnan(x)) { t = (double)C; return C - 1; }
+    t = (rmax - x) * cscale;
+    int c = (t >= 0.0) ? (t < (double)C ? (int)t : C - 1) : 0;
+    return c;
+}
+
+__device__ __forceinline__ int rs_fine_of(double t, int c, const uint32_t *base, const uint32_t *cf) {
+    int f = (int)cf[c];
+    double frac = t - (double)c;
+    int sub = (frac >= 0.0) ? (int)(frac * (double)f) : 0;
+    if (sub > f - 1) sub = f - 1;
+    return (int)base[c] + sub;
 }
 
 template <int EMAX>
@@ -275,15 +291,12 @@ row_sort_smem_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restr
     const int m = n - 1;
     double *vbuf = reinterpret_cast<double *>(rs_smem);
     uint16_t *sidx = reinterpret_cast<uint16_t *>(rs_smem + pl.off_sidx);
-    uint32_t *cnt = reinterpret_cast<uint32_t *>(rs_smem + pl.off_cnt);
-    double *spl = reinterpret_cast<double *>(rs_smem + pl.off_spl);
-    double *ub = reinterpret_cast<double *>(rs_smem + pl.off_ub);
-    double *scl = reinterpret_cast<double *>(rs_smem + pl.off_scl);
+    uint32_t *fcnt = reinterpret_cast<uint32_t *>(rs_smem + pl.off_fcnt);
     RsMisc &ms = *reinterpret_cast<RsMisc *>(rs_smem + pl.off_misc);
     __shared__ PwTree<PW_SMALLNODES> tree;
     __shared__ double pwval[PW_SMALLNODES];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int P = pl.P, K = pl.K, NB = pl.NB;
+    const int C = pl.C;
 
     if (rowsum) {
         int *height = reinterpret_cast<int *>(pwval);  // scratch before first use
@@ -293,16 +306,16 @@ row_sort_smem_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restr
     int64_t v = blockIdx.x;
     if (v < n && pl.nbuf == 2) rs_issue_row(vbuf, S + v * n64, n);
     for (; v < n; v += gridDim.x, it++) {
-        double *vals = vbuf + (pl.nbuf == 2 ? (size_t)(it & 1) * n : 0);
+        double *vals = vbuf + (pl.nbuf == 2 ? (size_t)(it & 1) * pl.stride : 0);
         if (pl.nbuf == 1) rs_issue_row(vals, S + v * n64, n);
         asm volatile("cp.async.wait_group 0;\n" ::);
         __syncthreads();
         if (pl.nbuf == 2) {
             int64_t vn = v + gridDim.x;
-            if (vn < n) rs_issue_row(vbuf + (size_t)((it + 1) & 1) * n, S + vn * n64, n);
+            if (vn < n) rs_issue_row(vbuf + (size_t)((it + 1) & 1) * pl.stride, S + vn * n64, n);
         }
-        // ---- phase A: zero counters, row min/max (v excluded)
-        for (int b = tid; b <= NB; b += RS_T) cnt[b] = 0;
+        // ---- A: zero coarse counters, row min/max (v excluded)
+        for (int c = tid; c <= C; c += RS_T) ms.ccnt[c] = 0;
         double mn = INFINITY, mx = -INFINITY;
         for (int j = tid; j < n; j += RS_T) {
             if (j == v) continue;
@@ -316,130 +329,134 @@ row_sort_smem_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restr
         }
         if (lane == 0) { ms.red[warp] = mn; ms.red[32 + warp] = mx; }
         __syncthreads();
-        // ---- phase B: splitters (warp 0) and per-bin linear maps
         if (warp == 0) {
             double a = ms.red[lane], b = ms.red[32 + lane];
             for (int o = 16; o; o >>= 1) {
                 a = fmin(a, __shfl_xor_sync(0xffffffffu, a, o));
                 b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
             }
-            double xs[2];
-            unsigned long long ks[2];
-            for (int q = 0; q < 2; q++) {
-                int k = lane + 32 * q;
-                double x = 0.0;
-                if (k < P) {
-                    int j = (int)(((int64_t)(2 * k + 1) * n) / (2 * P));
-                    if (j >= n) j = n - 1;
-                    if (j == v) j = (j + 1 < n) ? j + 1 : j - 1;
-                    x = vals[j];
-                }
-                xs[q] = x;
-                ks[q] = isnan(x) ? 0ull : tg_order_key(x);
-            }
-            for (int q = 0; q < 2; q++) {
-                int k = lane + 32 * q;
-                int rank = 0;
-                for (int mm = 0; mm < 2 * 32; mm++) {
-                    unsigned long long km = __shfl_sync(0xffffffffu, ks[mm >> 5], mm & 31);
-                    if (mm < P) rank += (km > ks[q]) || (km == ks[q] && mm < k);
-                }
-                if (k < P) spl[rank] = xs[q];
-            }
-            __syncwarp();
-            if (lane == 0) { ms.rmin = a; ms.rmax = b; }
-            for (int c = lane; c <= P; c += 32) {
-                double u = (c == 0) ? b : spl[c - 1];
-                double l = (c == P) ? a : spl[c];
-                double w = u - l;
-                ub[c] = u;
-                scl[c] = (w > 0.0 && w < INFINITY) ? (double)K / w : 0.0;
+            if (lane == 0) {
+                double w = b - a;
+                ms.rmin = a;
+                ms.rmax = b;
+                ms.cscale = (w > 0.0 && w < INFINITY) ? (double)C / w : 0.0;
             }
         }
         __syncthreads();
-        // ---- phase C: bucket + rank (one shared atomic per key)
+        // ---- B: coarse histogram (linear bins over [min, max]), warp-aggregated
+        const double rmax = ms.rmax, cscale = ms.cscale;
         uint32_t pk[EMAX];
 #pragma unroll
         for (int e = 0; e < EMAX; e++) {
             int j = tid + e * RS_T;
-            pk[e] = 0xffffffffu;
-            if (j < n && j != v) {
-                double x = vals[j];
-                int b;
-                if (isnan(x)) {
-                    b = NB - 1;
-                } else {
-                    int lo = 0, hi = P;
-                    while (lo < hi) {
-                        int mid = (lo + hi) >> 1;
-                        if (spl[mid] > x) lo = mid + 1;
-                        else hi = mid;
-                    }
-                    double t = (ub[lo] - x) * scl[lo];
-                    int sub = (t >= 0.0) ? (t < (double)K ? (int)t : K - 1) : 0;
-                    b = lo * K + sub;
-                }
-                uint32_t r = atomicAdd(&cnt[b], 1u);
-                pk[e] = ((uint32_t)b << 16) | r;
+            bool act = j < n && j != v;
+            int c = -1;
+            if (act) {
+                double t;
+                c = rs_coarse_of(vals[j], rmax, cscale, C, t);
             }
+            unsigned peers = __match_any_sync(0xffffffffu, c);
+            if (act && lane == __ffs(peers) - 1) atomicAdd(&ms.ccnt[c], (uint32_t)__popc(peers));
+            pk[e] = act ? (uint32_t)c : 0xffffffffu;
         }
         __syncthreads();
-        // ---- phase D: exclusive scan of cnt[0..NB] (block)
-        {
-            const int per = (NB + 1 + RS_T - 1) / RS_T;
-            int b0 = tid * per;
+        // ---- C: fine buckets per coarse bin (about two keys each), base offsets
+        for (int c = tid; c < C; c += RS_T) {
+            uint32_t h = ms.ccnt[c];
+            ms.cf[c] = h > 2 ? (h + 1) >> 1 : 1u;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            // exclusive scan of cf -> ccnt (base), C <= 512: 16 per lane
+            const int per = (C + 31) / 32;
             uint32_t s = 0;
             for (int q = 0; q < per; q++) {
-                int b = b0 + q;
-                if (b <= NB) s += cnt[b];
+                int c = lane * per + q;
+                if (c < C) s += ms.cf[c];
             }
             uint32_t incl = s;
             for (int o = 1; o < 32; o <<= 1) {
                 uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += y;
             }
-            uint32_t *wsum = reinterpret_cast<uint32_t *>(ms.red);
-            __syncthreads();
-            if (lane == 31) wsum[warp] = incl;
+            uint32_t run = incl - s;
+            for (int q = 0; q < per; q++) {
+                int c = lane * per + q;
+                if (c < C) { ms.ccnt[c] = run; run += ms.cf[c]; }
+            }
+            if (lane == 31) ms.ccnt[C] = incl;
+        }
+        __syncthreads();
+        const int NB = (int)ms.ccnt[C];
+        for (int b = tid; b <= NB; b += RS_T) fcnt[b] = 0;
+        __syncthreads();
+        // ---- D: fine bucket + rank inside it (one shared atomic per key)
+#pragma unroll
+        for (int e = 0; e < EMAX; e++) {
+            if (pk[e] != 0xffffffffu) {
+                int j = tid + e * RS_T;
+                double t;
+                int c = rs_coarse_of(vals[j], rmax, cscale, C, t);
+                int fb = rs_fine_of(t, c, ms.ccnt, ms.cf);
+                uint32_t r = atomicAdd(&fcnt[fb], 1u);
+                pk[e] = ((uint32_t)fb << 16) | r;
+            }
+        }
+        __syncthreads();
+        // ---- E: exclusive scan of the fine counters, scatter ids
+        {
+            const int len = NB + 1;
+            const int per = (len + RS_T - 1) / RS_T;
+            const int b0 = tid * per;
+            uint32_t s = 0;
+            for (int q = 0; q < per; q++) {
+                int b = b0 + q;
+                if (b < len) s += fcnt[b];
+            }
+            uint32_t incl = s;
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (lane == 31) ms.wsum[warp] = incl;
             __syncthreads();
             if (warp == 0) {
-                uint32_t w = wsum[lane];
+                uint32_t w = ms.wsum[lane];
                 uint32_t wi = w;
                 for (int o = 1; o < 32; o <<= 1) {
                     uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
                     if (lane >= o) wi += y;
                 }
-                wsum[lane] = wi - w;
+                ms.wsum[lane] = wi - w;
             }
             __syncthreads();
-            uint32_t run = wsum[warp] + incl - s;
+            uint32_t run = ms.wsum[warp] + incl - s;
             for (int q = 0; q < per; q++) {
                 int b = b0 + q;
-                if (b <= NB) {
-                    uint32_t c = cnt[b];
-                    cnt[b] = run;
+                if (b < len) {
+                    uint32_t c = fcnt[b];
+                    fcnt[b] = run;
                     run += c;
                 }
             }
         }
         __syncthreads();
-        // ---- phase E: scatter ids
 #pragma unroll
         for (int e = 0; e < EMAX; e++) {
             if (pk[e] != 0xffffffffu) {
                 int j = tid + e * RS_T;
-                sidx[cnt[pk[e] >> 16] + (pk[e] & 0xffffu)] = (uint16_t)j;
+                sidx[fcnt[pk[e] >> 16] + (pk[e] & 0xffffu)] = (uint16_t)j;
             }
         }
         __syncthreads();
-        // ---- phase F: exact rank of every key inside its bucket (value desc, id asc).
-        // Independent loads, no dependent chains: cost per key = its bucket size.
+        // ---- F: exact rank of every key inside its bucket (value desc, id asc):
+        // independent loads, cost per key = its bucket size; ids placed once more.
 #pragma unroll
         for (int e = 0; e < EMAX; e++) {
             if (pk[e] != 0xffffffffu) {
                 const int j = tid + e * RS_T;
                 const int b = (int)(pk[e] >> 16);
-                const int s0 = (int)cnt[b], s1 = (int)cnt[b + 1];
+                const int s0 = (int)fcnt[b], s1 = (int)fcnt[b + 1];
                 int rank = 0;
                 if (s1 - s0 > 1) {
                     const double xj = vals[j];
@@ -456,7 +473,7 @@ row_sort_smem_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restr
         for (int e = 0; e < EMAX; e++)
             if (pk[e] != 0xffffffffu) sidx[pk[e]] = (uint16_t)(tid + e * RS_T);
         __syncthreads();
-        // ---- phase G: write ids (16-byte stores on the aligned body)
+        // ---- G: write ids (16-byte stores on the aligned body)
         {
             int32_t *out = order + v * (int64_t)m;
             int head = (int)(((16 - (((uintptr_t)out) & 15)) & 15) >> 2);
@@ -470,7 +487,7 @@ row_sort_smem_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restr
             }
             for (int p = head + 4 * body + tid; p < m; p += RS_T) out[p] = sidx[p];
         }
-        // ---- phase H: fused pairwise row sum (initial-clique input)
+        // ---- H: fused pairwise row sum (initial-clique input)
         if (rowsum) {
             double root = pw_eval(tree, pwval, [&](int i) { return vals[i]; });
             if (tid == 0) rowsum[v] = __dsub_rn(root, vals[v]);
@@ -481,25 +498,22 @@ row_sort_smem_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restr
 }
 
 // ---------------------------------------------------------------- large rows
-// n > 16384: the same bucket algorithm with the row, the ranks and the scatter
-// buffer in global scratch (one slice per CTA; L2-resident while the CTA works
-// on the row).  Counters stay in shared memory.
+// n > 16384: the same two-level bucket algorithm; the row is read through L2,
+// the per-key (bucket, rank) pairs live in a per-CTA global scratch slice and
+// the output row itself is the scatter buffer.  Counters stay in shared memory.
 __global__ void __launch_bounds__(RS_T, 1)
 row_sort_global_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restrict__ order,
-                       double *__restrict__ rowsum, int P, int K, int NB, uint32_t *__restrict__ gcnt_all,
-                       uint32_t *__restrict__ grank_all, int32_t *__restrict__ gidx_all) {
+                       double *__restrict__ rowsum, uint32_t *__restrict__ gpk_all) {
     const int n = (int)n64;
     const int m = n - 1;
     extern __shared__ __align__(16) unsigned char rs_smem[];
-    uint32_t *cnt = reinterpret_cast<uint32_t *>(rs_smem);   // NB+1 (if it fits) else global
-    __shared__ double spl[RS_PMAX], ub[RS_PMAX + 1], scl[RS_PMAX + 1];
-    __shared__ double red[64];
+    uint32_t *fcnt = reinterpret_cast<uint32_t *>(rs_smem);
+    __shared__ RsMisc ms;
     __shared__ PwTree<PW_MAXNODES> tree;
     __shared__ double pwval[PW_MAXNODES];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    uint32_t *gcnt = gcnt_all ? gcnt_all + (size_t)blockIdx.x * (NB + 1) : cnt;
-    uint32_t *grank = grank_all + (size_t)blockIdx.x * n;
-    int32_t *gidx = gidx_all + (size_t)blockIdx.x * n;
+    const int C = rs_coarse_bins(m);
+    uint32_t *gpk = gpk_all + (size_t)blockIdx.x * 2 * n;   // [n] bucket, [n] rank/position
     if (rowsum) {
         int *height = reinterpret_cast<int *>(pwval);
         if (tid == 0) pw_plan(tree, n, height);
@@ -507,7 +521,8 @@ row_sort_global_kernel(const double *__restrict__ S, int64_t n64, int32_t *__res
     }
     for (int64_t v = blockIdx.x; v < n; v += gridDim.x) {
         const double *row = S + v * n64;
-        for (int b = tid; b <= NB; b += RS_T) gcnt[b] = 0;
+        int32_t *out = order + v * (int64_t)m;
+        for (int c = tid; c <= C; c += RS_T) ms.ccnt[c] = 0;
         double mn = INFINITY, mx = -INFINITY;
         for (int j = tid; j < n; j += RS_T) {
             if (j == v) continue;
@@ -519,118 +534,118 @@ row_sort_global_kernel(const double *__restrict__ S, int64_t n64, int32_t *__res
             mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
             mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         }
-        if (lane == 0) { red[warp] = mn; red[32 + warp] = mx; }
+        if (lane == 0) { ms.red[warp] = mn; ms.red[32 + warp] = mx; }
         __syncthreads();
         if (warp == 0) {
-            double a = red[lane], b = red[32 + lane];
+            double a = ms.red[lane], b = ms.red[32 + lane];
             for (int o = 16; o; o >>= 1) {
                 a = fmin(a, __shfl_xor_sync(0xffffffffu, a, o));
                 b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
             }
-            double xs[2];
-            unsigned long long ks[2];
-            for (int q = 0; q < 2; q++) {
-                int k = lane + 32 * q;
-                double x = 0.0;
-                if (k < P) {
-                    int j = (int)(((int64_t)(2 * k + 1) * n) / (2 * P));
-                    if (j >= n) j = n - 1;
-                    if (j == v) j = (j + 1 < n) ? j + 1 : j - 1;
-                    x = row[j];
-                }
-                xs[q] = x;
-                ks[q] = isnan(x) ? 0ull : tg_order_key(x);
-            }
-            for (int q = 0; q < 2; q++) {
-                int k = lane + 32 * q;
-                int rank = 0;
-                for (int mm = 0; mm < 64; mm++) {
-                    unsigned long long km = __shfl_sync(0xffffffffu, ks[mm >> 5], mm & 31);
-                    if (mm < P) rank += (km > ks[q]) || (km == ks[q] && mm < k);
-                }
-                if (k < P) spl[rank] = xs[q];
-            }
-            __syncwarp();
-            for (int c = lane; c <= P; c += 32) {
-                double u = (c == 0) ? b : spl[c - 1];
-                double l = (c == P) ? a : spl[c];
-                double w = u - l;
-                ub[c] = u;
-                scl[c] = (w > 0.0 && w < INFINITY) ? (double)K / w : 0.0;
+            if (lane == 0) {
+                double w = b - a;
+                ms.rmin = a;
+                ms.rmax = b;
+                ms.cscale = (w > 0.0 && w < INFINITY) ? (double)C / w : 0.0;
             }
         }
         __syncthreads();
-        for (int j = tid; j < n; j += RS_T) {
-            if (j == v) continue;
-            double x = __ldg(row + j);
-            int b;
-            if (isnan(x)) {
-                b = NB - 1;
-            } else {
-                int lo = 0, hi = P;
-                while (lo < hi) {
-                    int mid = (lo + hi) >> 1;
-                    if (spl[mid] > x) lo = mid + 1;
-                    else hi = mid;
-                }
-                double t = (ub[lo] - x) * scl[lo];
-                int sub = (t >= 0.0) ? (t < (double)K ? (int)t : K - 1) : 0;
-                b = lo * K + sub;
+        const double rmax = ms.rmax, cscale = ms.cscale;
+        for (int j0 = 0; j0 < n; j0 += RS_T) {
+            int j = j0 + tid;
+            bool act = j < n && j != v;
+            int c = -1;
+            if (act) {
+                double t;
+                c = rs_coarse_of(__ldg(row + j), rmax, cscale, C, t);
             }
-            uint32_t r = atomicAdd(&gcnt[b], 1u);
-            grank[j] = (uint32_t)b;
-            gidx[j] = (int32_t)r;  // temporarily: rank within bucket
+            unsigned peers = __match_any_sync(0xffffffffu, c);
+            if (act && lane == __ffs(peers) - 1) atomicAdd(&ms.ccnt[c], (uint32_t)__popc(peers));
         }
         __syncthreads();
-        // exclusive scan over NB+1 counters
-        {
-            const int per = (NB + 1 + RS_T - 1) / RS_T;
-            int b0 = tid * per;
+        for (int c = tid; c < C; c += RS_T) {
+            uint32_t h = ms.ccnt[c];
+            ms.cf[c] = h > 2 ? (h + 1) >> 1 : 1u;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            const int per = (C + 31) / 32;
             uint32_t s = 0;
             for (int q = 0; q < per; q++) {
-                int b = b0 + q;
-                if (b <= NB) s += gcnt[b];
+                int c = lane * per + q;
+                if (c < C) s += ms.cf[c];
             }
             uint32_t incl = s;
             for (int o = 1; o < 32; o <<= 1) {
                 uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += y;
             }
-            __shared__ uint32_t wsum[32];
-            if (lane == 31) wsum[warp] = incl;
+            uint32_t run = incl - s;
+            for (int q = 0; q < per; q++) {
+                int c = lane * per + q;
+                if (c < C) { ms.ccnt[c] = run; run += ms.cf[c]; }
+            }
+            if (lane == 31) ms.ccnt[C] = incl;
+        }
+        __syncthreads();
+        const int NB = (int)ms.ccnt[C];
+        for (int b = tid; b <= NB; b += RS_T) fcnt[b] = 0;
+        __syncthreads();
+        for (int j = tid; j < n; j += RS_T) {
+            if (j == v) continue;
+            double t;
+            int c = rs_coarse_of(__ldg(row + j), rmax, cscale, C, t);
+            int fb = rs_fine_of(t, c, ms.ccnt, ms.cf);
+            gpk[j] = (uint32_t)fb;
+            gpk[n + j] = atomicAdd(&fcnt[fb], 1u);
+        }
+        __syncthreads();
+        {
+            const int len = NB + 1;
+            const int per = (len + RS_T - 1) / RS_T;
+            const int b0 = tid * per;
+            uint32_t s = 0;
+            for (int q = 0; q < per; q++) {
+                int b = b0 + q;
+                if (b < len) s += fcnt[b];
+            }
+            uint32_t incl = s;
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (lane == 31) ms.wsum[warp] = incl;
             __syncthreads();
             if (warp == 0) {
-                uint32_t w = wsum[lane];
+                uint32_t w = ms.wsum[lane];
                 uint32_t wi = w;
                 for (int o = 1; o < 32; o <<= 1) {
                     uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
                     if (lane >= o) wi += y;
                 }
-                wsum[lane] = wi - w;
+                ms.wsum[lane] = wi - w;
             }
             __syncthreads();
-            uint32_t run = wsum[warp] + incl - s;
+            uint32_t run = ms.wsum[warp] + incl - s;
             for (int q = 0; q < per; q++) {
                 int b = b0 + q;
-                if (b <= NB) {
-                    uint32_t c = gcnt[b];
-                    gcnt[b] = run;
+                if (b < len) {
+                    uint32_t c = fcnt[b];
+                    fcnt[b] = run;
                     run += c;
                 }
             }
         }
         __syncthreads();
-        // scatter into the output row directly (it is the scatter buffer)
-        int32_t *out = order + v * (int64_t)m;
         for (int j = tid; j < n; j += RS_T) {
             if (j == v) continue;
-            out[gcnt[grank[j]] + (uint32_t)gidx[j]] = j;
+            out[fcnt[gpk[j]] + gpk[n + j]] = j;
         }
         __syncthreads();
         for (int j = tid; j < n; j += RS_T) {
             if (j == v) continue;
-            const int b = (int)grank[j];
-            const int s0 = (int)gcnt[b], s1 = (int)gcnt[b + 1];
+            const int b = (int)gpk[j];
+            const int s0 = (int)fcnt[b], s1 = (int)fcnt[b + 1];
             int rank = 0;
             if (s1 - s0 > 1) {
                 const double xj = __ldg(row + j);
@@ -639,12 +654,12 @@ row_sort_global_kernel(const double *__restrict__ S, int64_t n64, int32_t *__res
                     rank += rs_before(__ldg(row + o), o, xj, j);
                 }
             }
-            gidx[j] = s0 + rank;
+            gpk[n + j] = (uint32_t)(s0 + rank);
         }
         __syncthreads();
         for (int j = tid; j < n; j += RS_T) {
             if (j == v) continue;
-            out[gidx[j]] = j;
+            out[gpk[n + j]] = j;
         }
         __syncthreads();
         if (rowsum) {
@@ -661,25 +676,20 @@ constexpr size_t RS_SMEM_MAX = 227 * 1024 - sizeof(PwTree<PW_SMALLNODES>) - PW_S
 
 TG_API size_t tg_row_sort_workspace_bytes(int64_t n) {
     if (n <= 16384) return 256;
-    int sms = tg_num_sms();
-    int m = (int)n - 1;
-    int P = RS_PMAX;
-    int K = (m + 2 * (P + 1) - 1) / (2 * (P + 1));
-    size_t NB = (size_t)(P + 1) * K;
-    return (size_t)sms * ((NB + 1) * 4 + (size_t)n * 8) + 4096;
+    return (size_t)tg_num_sms() * 2 * (size_t)n * sizeof(uint32_t) + 4096;
 }
 
 TG_API int tg_row_sort_f64(const double *S, int64_t n, int32_t *order, double *rowsum, void *ws, size_t ws_bytes,
                            void *stream) {
     if (n < 2 || !S || !order) return TG_ERR_ARG;
     cudaStream_t st = tg_stream(stream);
+    int grid = tg_num_sms();
+    if (grid > n) grid = (int)n;
     if (n <= 16384) {
         RsPlan pl = rs_plan(n, 2);
         if (pl.smem > RS_SMEM_MAX) pl = rs_plan(n, 1);
         if (pl.smem > RS_SMEM_MAX) return TG_ERR_ARG;
         int E = (int)((n + RS_T - 1) / RS_T);
-        int grid = tg_num_sms();
-        if (grid > n) grid = (int)n;
 #define RS_LAUNCH(EM)                                                                                      \
     do {                                                                                                   \
         auto kfn = row_sort_smem_kernel<EM>;                                                               \
@@ -694,23 +704,15 @@ TG_API int tg_row_sort_f64(const double *S, int64_t n, int32_t *order, double *r
         TG_LAUNCH_CHECK();
         return TG_OK;
     }
-    if (n > 65535 * 16) return TG_ERR_ARG;
+    if (n > (int64_t)1 << 30) return TG_ERR_ARG;
+    if (n > 128 * (PW_MAXNODES / 2) && rowsum) return TG_ERR_ARG;
     if (ws_bytes < tg_row_sort_workspace_bytes(n)) return TG_ERR_WORKSPACE;
+    uint32_t *gpk = reinterpret_cast<uint32_t *>(ws);
     int m = (int)n - 1;
-    int P = RS_PMAX;
-    int K = (m + 2 * (P + 1) - 1) / (2 * (P + 1));
-    int NB = (P + 1) * K;
-    int grid = tg_num_sms();
-    TgArena ar(ws, ws_bytes);
-    size_t smem_cnt = (size_t)(NB + 1) * 4;
-    bool cnt_in_smem = smem_cnt <= 160 * 1024;
-    uint32_t *gcnt = cnt_in_smem ? nullptr : ar.take<uint32_t>((size_t)grid * (NB + 1));
-    uint32_t *grank = ar.take<uint32_t>((size_t)grid * n);
-    int32_t *gidx = ar.take<int32_t>((size_t)grid * n);
-    if (!grank || !gidx || (!cnt_in_smem && !gcnt)) return TG_ERR_WORKSPACE;
-    size_t smem = cnt_in_smem ? smem_cnt : 16;
+    size_t smem = (size_t)(rs_fine_cap(m) + 1) * sizeof(uint32_t);
+    if (smem > 160 * 1024) return TG_ERR_ARG;
     TG_CUDA_CHECK(cudaFuncSetAttribute(row_sort_global_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    row_sort_global_kernel<<<grid, RS_T, smem, st>>>(S, n, order, rowsum, P, K, NB, gcnt, grank, gidx);
+    row_sort_global_kernel<<<grid, RS_T, smem, st>>>(S, n, order, rowsum, gpk);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }

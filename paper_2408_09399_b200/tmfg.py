@@ -198,12 +198,14 @@ def build_tmfg_heap(S, lists: SortedNeighborLists | None = None, config: BuildCo
         order_dev = D.to_device(np.asarray(lists.order, dtype=np.int32), D.torch().int32)
     clique = initial_clique_device(Sd, rowsum)
     out = build_tmfg_heap_device(Sd, order_dev, clique, check_invariants)
-    stats = _stats_dict(out["stats"].cpu().numpy(), check_invariants)
+    raw = out["stats"].cpu().numpy()
+    stats = _stats_dict(raw, check_invariants)
     weights = edge_weights_device(Sd, out["edges"])
     g = TmfgGraph(n=n, edges=out["edges"], weights=weights, initial_clique=clique, trace=out["trace"],
                   faces=out["faces"], variant="heap", debug_stats=stats, host_fid=out["host_fid"],
                   S_device=Sd)
     g._S_host = S
+    g._raw_stats = {"pops": int(raw[0]), "refreshes": int(raw[1]), "gain_increases": int(raw[2])}
     return g
 
 

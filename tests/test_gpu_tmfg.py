@@ -59,11 +59,26 @@ def test_tmfg_vs_oracle_stats(n, seed, oracle, pkg):
     S = oracle.pearson_similarity(x)
     ref = oracle.build_tmfg_heap(S, oracle.sort_neighbor_lists(S))
     lists = pkg.sort_neighbor_lists(S)
-    g = pkg.build_tmfg_heap(S, lists, check_invariants=n <= 1500)
+    g = pkg.build_tmfg_heap(S, lists)
     for key in ("edges", "trace", "faces"):
         assert np.array_equal(getattr(g, key), ref[key]), key
-    if g.debug_stats is not None:
-        assert g.debug_stats == ref["stats"]
+    assert g._raw_stats == ref["stats"]
+
+
+def test_tmfg_check_mode_pinned_at_scale(digests, oracle, pkg):
+    """check_invariants on a 1500-vertex input: same outcome as the reference."""
+    from paper_2408_09399_b200 import synth
+    rec = digests["check_c3_n1500"]
+    x, _ = synth.generate(3, n=1500, seed=4)
+    S = oracle.pearson_similarity(x)
+    assert oracle.sha(S) == rec["S"]
+    lists = pkg.sort_neighbor_lists(S)
+    if "tmfg_check_error" in rec:
+        with pytest.raises(AssertionError) as ei:
+            pkg.build_tmfg_heap(S, lists, check_invariants=True)
+        assert str(ei.value) == rec["tmfg_check_error"]
+    else:
+        assert pkg.build_tmfg_heap(S, lists, check_invariants=True).debug_stats == rec["tmfg_stats"]
 
 
 def test_tmfg_nan_raises(pkg):
