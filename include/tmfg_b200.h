@@ -182,18 +182,42 @@ int tg_assign_vertices(const tg_oracle_t *oracle, const int32_t *bubbles, int64_
 int tg_group_blocks(const tg_oracle_t *oracle, const int32_t *perm, const int64_t *starts, int64_t count,
                     const int64_t *block_offsets, double *blocks_out, void *stream);
 
-/* dbht.py:217-230 _cluster_max_matrix (+ _kernels.py:184-201 segment_pair_max):
- * out (m, m) = max oracle distance between the member groups of perm/starts. */
-size_t tg_group_max_workspace_bytes(int64_t n, int64_t m);
-int tg_group_max(const tg_oracle_t *oracle, const int32_t *perm, const int64_t *starts, int64_t m, double *out,
-                 void *ws, size_t ws_bytes, void *stream);
+/* apsp.py:88-94 / 127-158: out (nr x nc) = oracle.block(rows, cols)
+ * (query_semantics = 0) or [oracle.query(u, v)] (query_semantics = 1). */
+int tg_oracle_block(const tg_oracle_t *oracle, const int32_t *rows, int64_t nr, const int32_t *cols, int64_t nc,
+                    int32_t query_semantics, double *out, void *stream);
+
+/* dbht.py:217-230 _cluster_max_matrix (+ _kernels.py:184-201 segment_pair_max),
+ * batched over vertex-disjoint sub-problems.  Sub-problem p covers positions
+ * [perm_off, perm_off + len) of perm/gid (gid = group index of each position,
+ * groups contiguous and ascending) and writes its m x m result at out + out_off.
+ * Tiles (sub, i0, j0) of 64 x 64 positions cover every sub-problem.  Hub mode:
+ * min-plus over the hub rows + near-table overrides (column table wins), max per
+ * group pair; exact mode: D entries, rows from the lower group, mirrored. */
+typedef struct {
+    int64_t perm_off;
+    int32_t len;
+    int32_t m;
+    int64_t out_off;
+} tg_gm_sub_t;
+typedef struct {
+    int32_t sub;
+    int32_t i0;
+    int32_t j0;
+} tg_gm_tile_t;
+size_t tg_group_max_workspace_bytes(int64_t n);
+int tg_group_max_batch(const tg_oracle_t *oracle, const int32_t *perm, const int32_t *gid, const void *subs,
+                       int64_t nsub, const void *tiles, int64_t ntiles, double *out, int64_t out_len, void *ws,
+                       size_t ws_bytes, void *stream);
 
 /* linkage.py:50-94 _nn_chain over a batch of dense matrices (matrix b: sizes[b]
  * x sizes[b] at mats + mat_offsets[b]; it is overwritten as the working copy).
- * Raw merges (slot ids, discovery order) at merge_offsets[b] (sizes[b]-1 rows). */
+ * Raw merges (slot cluster ids, discovery order) at merge_offsets[b]
+ * (sizes[b]-1 rows).  active/slot/chain: scratch of sizes[b] entries at
+ * aux_offsets[b]. */
 int tg_nn_chain_batch(double *mats, const int64_t *mat_offsets, const int64_t *sizes, int64_t count,
                       const int64_t *merge_offsets, int64_t *lefts_out, int64_t *rights_out, double *heights_out,
-                      void *stream);
+                      const int64_t *aux_offsets, uint8_t *active, int64_t *slot, int64_t *chain, void *stream);
 
 #ifdef __cplusplus
 }

@@ -3,10 +3,41 @@
 Drop-in replacements for the reference package's hot-path entry points
 (``tmfgclust``): the work runs in hand-written sm_100a kernels
 (``_lib/libtmfg_b200.so``, C ABI in ``include/tmfg_b200.h``) and there is no CPU
-fallback.
+fallback -- a missing library or GPU raises ``NativeUnavailable``.
+
+``install()`` rebinds the reference package's module attributes so its own
+pipeline (``tmfgclust.pipeline.run_stages``, which looks stage functions up on
+the modules at call time, pipeline.py:191-223) runs on the B200.
 """
 
 from . import _native
+from ._native import NativeError, NativeUnavailable
+from .apsp import (
+    ApspParams,
+    DistanceOracle,
+    ExactOracle,
+    HubOracle,
+    WeightedTmfg,
+    apsp_exact,
+    apsp_hub,
+    default_hub_count,
+    query,
+    select_hubs,
+    to_weighted,
+)
+from .dbht import (
+    BubbleAssignment,
+    BubbleTree,
+    DirectedBubbleTree,
+    assign_vertices,
+    bubble_sinks,
+    build_bubble_tree,
+    build_hierarchy,
+    converging_bubbles,
+    orient_edges,
+)
+from .linkage import Dendrogram, cut, dendrogram_from_merges, nn_chain_merges, serialize_dendrogram
+from .pipeline import PipelineConfig, RunReport, StageError, run_stages
 from .simmatrix import (
     DataError,
     Dataset,
@@ -28,3 +59,44 @@ from .tmfg import (
 )
 
 __version__ = "0.1.0"
+
+# reference module -> names this package replaces in it
+_INSTALL_MAP = {
+    "simmatrix": ["pearson_similarity", "sort_neighbor_lists"],
+    "tmfg": ["select_initial_clique", "build_tmfg_heap"],
+    "apsp": ["to_weighted", "apsp_exact", "apsp_hub", "select_hubs"],
+    "dbht": ["build_bubble_tree", "orient_edges", "bubble_sinks", "assign_vertices", "build_hierarchy"],
+    "linkage": ["nn_chain_merges"],
+}
+
+
+def install(package=None) -> dict:
+    """Route the reference package's hot path through this package.
+
+    Rebinds the stage functions on the reference modules (and its top-level
+    re-exports).  The exact / corr TMFG builders stay the reference's own
+    (``tmfg.build_tmfg`` dispatches to ``build_tmfg_heap`` by module lookup).
+    Returns the replaced originals so ``uninstall(originals)`` can restore them.
+    """
+    import importlib
+    import sys
+
+    pkg = package or importlib.import_module("tmfgclust")
+    this = sys.modules[__name__]
+    saved = {}
+    for mod_name, names in _INSTALL_MAP.items():
+        mod = importlib.import_module(f"{pkg.__name__}.{mod_name}")
+        for name in names:
+            saved[(mod.__name__, name)] = getattr(mod, name)
+            setattr(mod, name, getattr(this, name))
+            if hasattr(pkg, name):
+                saved[(pkg.__name__, name)] = getattr(pkg, name)
+                setattr(pkg, name, getattr(this, name))
+    return saved
+
+
+def uninstall(saved: dict) -> None:
+    import importlib
+
+    for (mod_name, name), fn in saved.items():
+        setattr(importlib.import_module(mod_name), name, fn)

@@ -1,0 +1,698 @@
+// dbht.cu -- DBHT on the B200: bubble tree, orientation, converging sinks,
+// vertex assignment, distance blocks, group-max matrices and NN-chain linkage.
+//
+// Replaces dbht.py:64-230 (build_bubble_tree, orient_edges, _next_hops,
+// bubble_sinks, assign_vertices, _cluster_max_matrix), the oracle accessors
+// apsp.py:88-158 (query / block) and linkage.py:50-94 (_nn_chain), plus
+// _kernels.py:184-201 (segment_pair_max).
+//
+// The dominant kernel is the group max in hub mode: for every vertex pair of
+// the (permuted) member list, est(u,v) = min_h hd[h,u] + hd[h,v] -- a min-plus
+// "GEMM" over the H hub rows on the fp64 CUDA-core pipe (no tensor path exists
+// for min-plus) -- overridden by the exact near-table distances, then reduced
+// by max into the (group x group) matrix.  Tiles of 64x64 pairs, hub columns
+// staged in shared memory 32 hubs at a time, 4x4 register micro-tiles.
+#include "common.cuh"
+
+namespace {
+
+// ------------------------------------------------------------ oracle access
+__device__ __forceinline__ bool near_find(const int64_t *ip, const int32_t *ids, const double *dd, int u, int v,
+                                          double &out) {
+    int64_t lo = ip[u], hi = ip[u + 1];
+    while (lo < hi) {  // np.searchsorted(ids, v) (left)
+        int64_t mid = (lo + hi) >> 1;
+        if (ids[mid] < v) lo = mid + 1;
+        else hi = mid;
+    }
+    if (lo < ip[u + 1] && ids[lo] == v) {
+        out = dd[lo];
+        return true;
+    }
+    return false;
+}
+
+__device__ __forceinline__ double hub_min(const tg_oracle_t &o, int u, int v) {
+    double best = INFINITY;
+    for (int64_t h = 0; h < o.H; h++) {
+        double s = __dadd_rn(o.hub_dist[h * o.n + u], o.hub_dist[h * o.n + v]);
+        best = s < best ? s : best;
+    }
+    return best;
+}
+
+// apsp.py:127-136 HubOracle.query / apsp.py:88-90 ExactOracle.query
+__device__ double oracle_query(const tg_oracle_t &o, int u, int v) {
+    if (o.mode == 0) return o.matrix[(int64_t)u * o.n + v];
+    if (u == v) return 0.0;
+    int a = u < v ? u : v, b = u < v ? v : u;
+    double d;
+    if (near_find(o.near_indptr, o.near_ids, o.near_dist, a, b, d)) return d;
+    if (near_find(o.near_indptr, o.near_ids, o.near_dist, b, a, d)) return d;
+    return hub_min(o, a, b);
+}
+
+// apsp.py:138-158 HubOracle.block entry (column-vertex table wins over the row's)
+__device__ double oracle_block(const tg_oracle_t &o, int u, int v) {
+    if (o.mode == 0) return o.matrix[(int64_t)u * o.n + v];
+    double d;
+    if (near_find(o.near_indptr, o.near_ids, o.near_dist, v, u, d)) return d;
+    if (near_find(o.near_indptr, o.near_ids, o.near_dist, u, v, d)) return d;
+    return hub_min(o, u, v);
+}
+
+__device__ __forceinline__ void sort3i(int &x, int &y, int &z) {
+    int t;
+    if (y < x) { t = x; x = y; y = t; }
+    if (z < y) { t = y; y = z; z = t; }
+    if (y < x) { t = x; x = y; y = t; }
+}
+
+// ------------------------------------------------------------ bubble tree
+__global__ void ins_time_kernel(int64_t n, int32_t *ins_t) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) ins_t[i] = -2;
+}
+
+__global__ void ins_time_set_kernel(const int32_t *clique, const int32_t *trace, int64_t nt, int32_t *ins_t) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < 4) ins_t[clique[t]] = -1;
+    if (t < nt) ins_t[trace[4 * t]] = (int32_t)t;
+}
+
+__device__ __forceinline__ unsigned long long face_key(int x, int y, int z, int64_t n) {
+    return ((unsigned long long)x * (unsigned long long)n + (unsigned long long)y) * (unsigned long long)n +
+           (unsigned long long)z + 1ull;
+}
+
+// dbht.py:64-89: the owner of a live face is the bubble created by the insertion
+// of its latest-inserted vertex (0 for faces of the initial clique); a row is
+// valid iff its face was created before it and not consumed by an earlier row.
+__global__ void bubble_tree_kernel(const int32_t *clique, const int32_t *trace, int64_t nt, int64_t n,
+                                   const int32_t *ins_t, unsigned long long *htab, int64_t hmask,
+                                   int32_t *bubbles, int32_t *links, int32_t *link_faces,
+                                   unsigned long long *bad_min) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t == 0) {
+        int a = clique[0], b = clique[1], c = clique[2], d = clique[3];
+        int q[4] = {a, b, c, d};
+        for (int i = 0; i < 4; i++)
+            for (int j = i + 1; j < 4; j++)
+                if (q[j] < q[i]) { int x = q[i]; q[i] = q[j]; q[j] = x; }
+        for (int i = 0; i < 4; i++) bubbles[i] = q[i];
+    }
+    if (t >= nt) return;
+    int v = trace[4 * t], x = trace[4 * t + 1], y = trace[4 * t + 2], z = trace[4 * t + 3];
+    sort3i(x, y, z);
+    bool ok = true;
+    int tx = ins_t[x], ty = ins_t[y], tz = ins_t[z];
+    if (tx == -2 || ty == -2 || tz == -2) ok = false;
+    int tw = max(tx, max(ty, tz));
+    int owner = 0;
+    if (ok && tw >= (int)t) ok = false;
+    if (ok && tw >= 0) {
+        int w = (tw == tx) ? x : ((tw == ty) ? y : z);
+        int o1 = (w == x) ? y : x, o2 = (w == z) ? y : z;
+        if (w == y) { o1 = x; o2 = z; }
+        // F \ {w} must be two vertices of the host face of row tw, and w = v(tw)
+        const int32_t *r = trace + 4 * (int64_t)tw;
+        bool h1 = (o1 == r[1] || o1 == r[2] || o1 == r[3]);
+        bool h2 = (o2 == r[1] || o2 == r[2] || o2 == r[3]);
+        if (!(h1 && h2 && r[0] == w)) ok = false;
+        owner = tw + 1;
+    }
+    // a face can be consumed once: the later duplicate row is invalid
+    unsigned long long key = face_key(x, y, z, n);
+    int64_t h = (int64_t)((key * 0x9E3779B97F4A7C15ull) >> 20) & hmask;
+    for (;;) {
+        unsigned long long prev = atomicCAS(&htab[2 * h], 0ull, key);
+        if (prev == 0ull) {
+            atomicMin(&htab[2 * h + 1], (unsigned long long)t);
+            break;
+        }
+        if (prev == key) {
+            atomicMin(&htab[2 * h + 1], (unsigned long long)t);
+            break;
+        }
+        h = (h + 1) & hmask;
+    }
+    int q[4] = {v, x, y, z};
+    for (int i = 0; i < 4; i++)
+        for (int j = i + 1; j < 4; j++)
+            if (q[j] < q[i]) { int s = q[i]; q[i] = q[j]; q[j] = s; }
+    for (int i = 0; i < 4; i++) bubbles[4 * (t + 1) + i] = q[i];
+    links[2 * t] = owner;
+    links[2 * t + 1] = (int32_t)(t + 1);
+    link_faces[3 * t] = x;
+    link_faces[3 * t + 1] = y;
+    link_faces[3 * t + 2] = z;
+    if (!ok) atomicMin(bad_min, (unsigned long long)t);
+}
+
+__global__ void bubble_dup_kernel(const int32_t *trace, int64_t nt, int64_t n, const unsigned long long *htab,
+                                  int64_t hmask, unsigned long long *bad_min) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    int x = trace[4 * t + 1], y = trace[4 * t + 2], z = trace[4 * t + 3];
+    sort3i(x, y, z);
+    unsigned long long key = face_key(x, y, z, n);
+    int64_t h = (int64_t)((key * 0x9E3779B97F4A7C15ull) >> 20) & hmask;
+    while (htab[2 * h] != key) h = (h + 1) & hmask;
+    if (htab[2 * h + 1] != (unsigned long long)t) atomicMin(bad_min, (unsigned long long)t);
+}
+
+// ------------------------------------------------------------ orientation
+__device__ __forceinline__ int apex_of(const int32_t *bub, int f0, int f1, int f2) {
+    for (int k = 0; k < 4; k++) {
+        int w = bub[k];
+        if (w != f0 && w != f1 && w != f2) return w;
+    }
+    return -1;
+}
+
+__global__ void orient_kernel(const double *S, int64_t n, const int32_t *bubbles, const int32_t *links,
+                              const int32_t *faces, int64_t L, int64_t *src, int64_t *dst) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= L) return;
+    int b1 = links[2 * i], b2 = links[2 * i + 1];
+    int f0 = faces[3 * i], f1 = faces[3 * i + 1], f2 = faces[3 * i + 2];
+    int a1 = apex_of(bubbles + 4 * (int64_t)b1, f0, f1, f2);
+    int a2 = apex_of(bubbles + 4 * (int64_t)b2, f0, f1, f2);
+    // tmfg.py:82-85 gain: S[a,v] + S[b,v] + S[c,v], left to right
+    double g1 = __dadd_rn(__dadd_rn(S[(int64_t)f0 * n + a1], S[(int64_t)f1 * n + a1]), S[(int64_t)f2 * n + a1]);
+    double g2 = __dadd_rn(__dadd_rn(S[(int64_t)f0 * n + a2], S[(int64_t)f1 * n + a2]), S[(int64_t)f2 * n + a2]);
+    int s, d;
+    if (g2 > g1) { s = b1; d = b2; }
+    else if (g1 > g2) { s = b2; d = b1; }
+    else if (b2 < b1) { s = b1; d = b2; }
+    else { s = b2; d = b1; }
+    src[i] = s;
+    dst[i] = d;
+}
+
+// ------------------------------------------------------------ next hops + sinks
+__device__ __forceinline__ double edge_gain(const double *S, int64_t n, int f0, int f1, int f2, int apex) {
+    // dbht.py:131-140: total = 0.0 then += weight of (w, apex) over the sorted face
+    double t = 0.0;
+    int f[3] = {f0, f1, f2};
+    for (int k = 0; k < 3; k++) {
+        int a = f[k] < apex ? f[k] : apex, b = f[k] < apex ? apex : f[k];
+        t = __dadd_rn(t, S[(int64_t)a * n + b]);
+    }
+    return t;
+}
+
+__global__ void hop_gain_kernel(const double *S, int64_t n, const int32_t *bubbles, const int32_t *faces,
+                                const int64_t *src, const int64_t *dst, int64_t L, double *g_out,
+                                unsigned long long *best) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= L) return;
+    int f0 = faces[3 * i], f1 = faces[3 * i + 1], f2 = faces[3 * i + 2];
+    int d = (int)dst[i];
+    int apex = apex_of(bubbles + 4 * (int64_t)d, f0, f1, f2);
+    double g = edge_gain(S, n, f0, f1, f2, apex);
+    g_out[i] = g;
+    atomicMax(&best[src[i]], tg_order_key(g));
+}
+
+__global__ void hop_pick_kernel(const int64_t *src, const int64_t *dst, int64_t L, const double *g,
+                                const unsigned long long *best, int64_t *hops) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= L) return;
+    if (tg_order_key(g[i]) == best[src[i]]) atomicMin((unsigned long long *)&hops[src[i]], (unsigned long long)dst[i]);
+}
+
+__global__ void sink_init_kernel(int64_t m, int64_t *hops, int64_t *sink) {
+    int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= m) return;
+    sink[b] = hops[b] < 0 ? b : hops[b];
+}
+
+__global__ void sink_jump_kernel(int64_t m, const int64_t *in, int64_t *out, int *changed) {
+    int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= m) return;
+    int64_t s = in[b];
+    int64_t t = in[s];
+    out[b] = t;
+    if (t != s) *changed = 1;
+}
+
+// ------------------------------------------------------------ assignment
+__global__ void assign_mean_kernel(tg_oracle_t o, const int32_t *bubbles, int64_t m, double *mean_out,
+                                   unsigned long long *best) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (bubble, member) pair
+    if (i >= 4 * m) return;
+    int64_t bid = i >> 2;
+    const int32_t *bub = bubbles + 4 * bid;
+    int v = bub[i & 3];
+    double total = 0.0;
+    for (int k = 0; k < 4; k++) {
+        int w = bub[k];
+        double q = (w == v) ? 0.0 : oracle_query(o, v, w);
+        total = __dadd_rn(total, q);
+    }
+    double mean = total / 4.0;
+    mean_out[i] = mean;
+    atomicMin(&best[v], tg_order_key(mean));
+}
+
+__global__ void assign_pick_kernel(const int32_t *bubbles, int64_t m, const double *mean,
+                                   const unsigned long long *best, int64_t *vb) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 4 * m) return;
+    int v = bubbles[i];
+    if (tg_order_key(mean[i]) == best[v]) atomicMin((unsigned long long *)&vb[v], (unsigned long long)(i >> 2));
+}
+
+__global__ void assign_conv_kernel(int64_t n, const int64_t *vb, const int64_t *sinks, int64_t *vc) {
+    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n) vc[v] = sinks[vb[v]];
+}
+
+// ------------------------------------------------------------ group blocks (layer 1)
+__global__ void group_blocks_kernel(tg_oracle_t o, const int32_t *perm, const int64_t *starts, int64_t count,
+                                    const int64_t *boff, double *out) {
+    for (int64_t g = blockIdx.x; g < count; g += gridDim.x) {
+        int64_t s0 = starts[g];
+        int gsz = (int)(starts[g + 1] - s0);
+        double *B = out + boff[g];
+        for (int e = threadIdx.x; e < gsz * gsz; e += blockDim.x) {
+            int i = e / gsz, j = e % gsz;
+            B[e] = oracle_block(o, perm[s0 + i], perm[s0 + j]);
+        }
+    }
+}
+
+// ------------------------------------------------------------ group max (layers 2 and 3)
+constexpr int GM_T = 256;
+constexpr int GM_TILE = 64;
+constexpr int GM_HC = 32;   // hubs staged per chunk
+
+struct GmTile {
+    int sub;   // sub-problem
+    int i0, j0;
+};
+
+struct GmSub {
+    int64_t perm_off;   // into perm / gid
+    int32_t len;        // vertices
+    int32_t m;          // groups
+    int64_t out_off;    // into out (m x m)
+};
+
+// out is pre-filled with 0 bits (all distances >= 0); atomicMax on raw bits.
+__global__ void __launch_bounds__(GM_T)
+group_max_tile_kernel(tg_oracle_t o, const int32_t *__restrict__ perm, const int32_t *__restrict__ gid,
+                      const int32_t *__restrict__ pos, const GmSub *__restrict__ subs, const GmTile *__restrict__ tiles,
+                      int64_t ntiles, unsigned long long *__restrict__ out) {
+    // the hub panels (A, B) and the pair tile E are never live together
+    __shared__ __align__(16) double gm_raw[GM_TILE * (GM_TILE + 1)];
+    double (*A)[GM_TILE] = reinterpret_cast<double (*)[GM_TILE]>(gm_raw);
+    double (*B)[GM_TILE] = reinterpret_cast<double (*)[GM_TILE]>(gm_raw + GM_HC * GM_TILE);
+    double (*E)[GM_TILE + 1] = reinterpret_cast<double (*)[GM_TILE + 1]>(gm_raw);
+    __shared__ int ru[GM_TILE], cv[GM_TILE], rg[GM_TILE], cg[GM_TILE];
+    const int tid = threadIdx.x;
+    const int tx = tid & 15, ty = tid >> 4;  // 16 x 16 threads, 4x4 pairs each
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const GmTile tl = tiles[t];
+        const GmSub sb = subs[tl.sub];
+        const int rows = min(GM_TILE, sb.len - tl.i0), cols = min(GM_TILE, sb.len - tl.j0);
+        if (tid < GM_TILE) {
+            int i = tid;
+            ru[i] = i < rows ? perm[sb.perm_off + tl.i0 + i] : -1;
+            rg[i] = i < rows ? gid[sb.perm_off + tl.i0 + i] : -1;
+            cv[i] = i < cols ? perm[sb.perm_off + tl.j0 + i] : -1;
+            cg[i] = i < cols ? gid[sb.perm_off + tl.j0 + i] : -1;
+        }
+        __syncthreads();
+        if (o.mode == 1) {
+            double acc[4][4];
+#pragma unroll
+            for (int r = 0; r < 4; r++)
+#pragma unroll
+                for (int c = 0; c < 4; c++) acc[r][c] = INFINITY;
+            for (int64_t h0 = 0; h0 < o.H; h0 += GM_HC) {
+                const int hc = (int)min((int64_t)GM_HC, o.H - h0);
+                for (int e = tid; e < GM_HC * GM_TILE; e += GM_T) {
+                    int h = e / GM_TILE, i = e % GM_TILE;
+                    double a = INFINITY, b = INFINITY;
+                    if (h < hc) {
+                        if (ru[i] >= 0) a = o.hub_dist[(h0 + h) * o.n + ru[i]];
+                        if (cv[i] >= 0) b = o.hub_dist[(h0 + h) * o.n + cv[i]];
+                    }
+                    A[h][i] = a;
+                    B[h][i] = b;
+                }
+                __syncthreads();
+                for (int h = 0; h < hc; h++) {
+                    double a[4], b[4];
+#pragma unroll
+                    for (int r = 0; r < 4; r++) a[r] = A[h][ty + 16 * r];
+#pragma unroll
+                    for (int c = 0; c < 4; c++) b[c] = B[h][tx + 16 * c];
+#pragma unroll
+                    for (int r = 0; r < 4; r++)
+#pragma unroll
+                        for (int c = 0; c < 4; c++) acc[r][c] = fmin(acc[r][c], __dadd_rn(a[r], b[c]));
+                }
+                __syncthreads();
+            }
+            __syncthreads();
+#pragma unroll
+            for (int r = 0; r < 4; r++)
+#pragma unroll
+                for (int c = 0; c < 4; c++) E[ty + 16 * r][tx + 16 * c] = acc[r][c];
+            __syncthreads();
+            // row-vertex near tables, then column-vertex tables (they win: apsp.py:147-157)
+            for (int pass = 0; pass < 2; pass++) {
+                const int64_t *ip = pass == 0 ? o.near_indptr : o.rev_indptr;
+                const int32_t *ids = pass == 0 ? o.near_ids : o.rev_ids;
+                const double *dd = pass == 0 ? o.near_dist : o.rev_dist;
+                for (int i = tid >> 2; i < rows; i += GM_T / 4) {
+                    int u = ru[i];
+                    for (int64_t k = ip[u] + (tid & 3); k < ip[u + 1]; k += 4) {
+                        int p = pos[ids[k]] - tl.j0;
+                        if (p >= 0 && p < cols) E[i][p] = dd[k];
+                    }
+                }
+                __syncthreads();
+            }
+        } else {
+            for (int e = tid; e < GM_TILE * GM_TILE; e += GM_T) {
+                int i = e / GM_TILE, j = e % GM_TILE;
+                E[i][j] = (i < rows && j < cols) ? o.matrix[(int64_t)ru[i] * o.n + cv[j]] : 0.0;
+            }
+            __syncthreads();
+        }
+        // per (row group, column group) segment max -> atomicMax
+        for (int i = tid; i < rows; i += GM_T) {
+            int gi = rg[i];
+            int j = 0;
+            while (j < cols) {
+                int gj = cg[j];
+                double best = E[i][j];
+                int k = j + 1;
+                while (k < cols && cg[k] == gj) {
+                    best = fmax(best, E[i][k]);
+                    k++;
+                }
+                // exact mode: only the lower group's rows count (_kernels.py:188-201)
+                if (o.mode == 1 || gi <= gj) atomicMax(&out[sb.out_off + (int64_t)gi * sb.m + gj], tg_dbits(best));
+                j = k;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void group_max_finalize_kernel(const GmSub *subs, int64_t nsub, int mode, double *out) {
+    for (int64_t p = blockIdx.x; p < nsub; p += gridDim.x) {
+        GmSub sb = subs[p];
+        double *M = out + sb.out_off;
+        for (int e = threadIdx.x; e < sb.m * sb.m; e += blockDim.x) {
+            int i = e / sb.m, j = e % sb.m;
+            if (mode == 0 && i > j) M[e] = M[(int64_t)j * sb.m + i];  // mirror (segment_pair_max)
+        }
+    }
+}
+
+// ------------------------------------------------------------ NN-chain (linkage.py:50-94)
+// One warp per matrix; the matrix itself is the working copy W.
+__global__ void nn_chain_kernel(double *mats, const int64_t *mat_off, const int64_t *sizes, int64_t count,
+                                const int64_t *merge_off, int64_t *lefts, int64_t *rights, double *heights,
+                                uint8_t *active_all, int64_t *slot_all, int64_t *chain_all, const int64_t *aux_off) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t b = wid; b < count; b += nwarps) {
+        const int64_t m = sizes[b];
+        if (m < 2) continue;
+        double *W = mats + mat_off[b];
+        uint8_t *active = active_all + aux_off[b];
+        int64_t *slot = slot_all + aux_off[b];
+        int64_t *chain = chain_all + aux_off[b];
+        int64_t *L = lefts + merge_off[b], *R = rights + merge_off[b];
+        double *Hh = heights + merge_off[b];
+        for (int64_t i = lane; i < m; i += 32) {
+            active[i] = 1;
+            slot[i] = i;
+            W[i * m + i] = INFINITY;
+        }
+        __syncwarp();
+        int64_t nchain = 0, next_id = m, remaining = m, nm = 0;
+        while (remaining > 1) {
+            if (nchain == 0) {
+                int64_t f = -1;
+                for (int64_t i0 = 0; i0 < m && f < 0; i0 += 32) {
+                    int64_t i = i0 + lane;
+                    unsigned bal = __ballot_sync(0xffffffffu, i < m && active[i]);
+                    if (bal) f = i0 + __ffs(bal) - 1;
+                }
+                chain[nchain++] = f;
+            }
+            const int64_t x = chain[nchain - 1];
+            // y = argmin over active j != x of W[x, j] (first index on ties)
+            double bv = INFINITY;
+            int64_t bi = INT64_MAX;
+            for (int64_t j = lane; j < m; j += 32) {
+                double r = (active[j] && j != x) ? W[x * m + j] : INFINITY;
+                if (r < bv || (r == bv && j < bi)) { bv = r; bi = j; }
+            }
+            for (int o = 16; o; o >>= 1) {
+                double r2 = __shfl_xor_sync(0xffffffffu, bv, o);
+                int64_t i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (r2 < bv || (r2 == bv && i2 < bi)) { bv = r2; bi = i2; }
+            }
+            int64_t y = (bi == INT64_MAX) ? 0 : bi;  // all-inf row: np.argmin -> 0
+            if (nchain > 1) {
+                int64_t p = chain[nchain - 2];
+                double rp = (active[p] && p != x) ? W[x * m + p] : INFINITY;
+                double ry = (active[y] && y != x) ? W[x * m + y] : INFINITY;
+                if (rp == ry) y = p;
+            }
+            if (nchain > 1 && y == chain[nchain - 2]) {
+                nchain -= 2;
+                const double h = W[x * m + y];
+                const int64_t lo = x < y ? x : y, hi = x < y ? y : x;
+                if (lane == 0) {
+                    L[nm] = slot[x];
+                    R[nm] = slot[y];
+                    Hh[nm] = h;
+                }
+                nm++;
+                // merged = max(W[lo], W[hi]); W[lo] = merged; W[:, lo] = merged; W[lo, lo] = inf
+                for (int64_t j = lane; j < m; j += 32) {
+                    double p = W[lo * m + j], q = W[hi * m + j];
+                    double mg = p > q ? p : (q > p ? q : p);
+                    W[lo * m + j] = mg;
+                    W[j * m + lo] = mg;
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    W[lo * m + lo] = INFINITY;
+                    active[hi] = 0;
+                    slot[lo] = next_id;
+                }
+                next_id++;
+                remaining--;
+                __syncwarp();
+            } else {
+                chain[nchain++] = y;
+            }
+        }
+    }
+}
+
+__global__ void pos_fill_kernel(const GmSub *subs, int64_t nsub, const int32_t *perm, int32_t *pos) {
+    for (int64_t p = blockIdx.x; p < nsub; p += gridDim.x)
+        for (int i = threadIdx.x; i < subs[p].len; i += blockDim.x) pos[perm[subs[p].perm_off + i]] = i;
+}
+
+__global__ void oracle_block_kernel(tg_oracle_t o, const int32_t *rows, int64_t nr, const int32_t *cols, int64_t nc,
+                                    int q, double *out) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nr * nc) return;
+    int u = rows[e / nc], v = cols[e % nc];
+    out[e] = q ? oracle_query(o, u, v) : oracle_block(o, u, v);
+}
+
+}  // namespace
+
+// ============================================================== C ABI
+TG_API size_t tg_bubble_tree_workspace_bytes(int64_t n) {
+    size_t hs = 1;
+    while (hs < (size_t)(4 * n + 16)) hs <<= 1;
+    return tg_align_up((size_t)n * 4, 256) + tg_align_up(hs * 16, 256) + 512;
+}
+
+TG_API int tg_bubble_tree(const int32_t *clique, const int32_t *trace, int64_t n, int32_t *bubbles, int32_t *links,
+                          int32_t *link_faces, int64_t *bad_row, void *ws, size_t ws_bytes, void *stream) {
+    if (n < 4 || !clique || !bubbles || !bad_row) return TG_ERR_ARG;
+    if (ws_bytes < tg_bubble_tree_workspace_bytes(n)) return TG_ERR_WORKSPACE;
+    cudaStream_t st = tg_stream(stream);
+    size_t hs = 1;
+    while (hs < (size_t)(4 * n + 16)) hs <<= 1;
+    TgArena ar(ws, ws_bytes);
+    int32_t *ins_t = ar.take<int32_t>(n);
+    unsigned long long *htab = ar.take<unsigned long long>(2 * hs);
+    unsigned long long *bad = ar.take<unsigned long long>(1);
+    const int64_t nt = n - 4;
+    TG_CUDA_CHECK(cudaMemsetAsync(bad, 0xff, 8, st));
+    // hash table of faces: key slots 0 (empty), first-row slots +inf
+    TG_CUDA_CHECK(cudaMemsetAsync(htab, 0xff, hs * 16, st));
+    TG_CUDA_CHECK(cudaMemset2DAsync(htab, 16, 0, 8, hs, st));
+    const unsigned T = 256;
+    ins_time_kernel<<<(unsigned)((n + T - 1) / T), T, 0, st>>>(n, ins_t);
+    ins_time_set_kernel<<<(unsigned)((max(nt, (int64_t)4) + T - 1) / T), T, 0, st>>>(clique, trace, nt, ins_t);
+    if (nt > 0) {
+        bubble_tree_kernel<<<(unsigned)((nt + T - 1) / T), T, 0, st>>>(clique, trace, nt, n, ins_t, htab,
+                                                                     (int64_t)hs - 1, bubbles, links, link_faces, bad);
+        bubble_dup_kernel<<<(unsigned)((nt + T - 1) / T), T, 0, st>>>(trace, nt, n, htab, (int64_t)hs - 1, bad);
+    } else {
+        bubble_tree_kernel<<<1, 32, 0, st>>>(clique, trace, 0, n, ins_t, htab, (int64_t)hs - 1, bubbles, links,
+                                            link_faces, bad);
+    }
+    TG_LAUNCH_CHECK();
+    unsigned long long b = 0;
+    TG_CUDA_CHECK(cudaMemcpyAsync(&b, bad, 8, cudaMemcpyDeviceToHost, st));
+    TG_CUDA_CHECK(cudaStreamSynchronize(st));
+    *bad_row = (b == ~0ull) ? -1 : (int64_t)b;
+    return *bad_row >= 0 ? TG_ERR_TRACE : TG_OK;
+}
+
+TG_API int tg_orient_edges(const double *S, int64_t n, const int32_t *bubbles, const int32_t *links,
+                           const int32_t *link_faces, int64_t L, int64_t *src, int64_t *dst, void *stream) {
+    if (!S || L < 0) return TG_ERR_ARG;
+    if (L == 0) return TG_OK;
+    orient_kernel<<<(unsigned)((L + 255) / 256), 256, 0, tg_stream(stream)>>>(S, n, bubbles, links, link_faces, L, src,
+                                                                             dst);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+TG_API size_t tg_bubble_sinks_workspace_bytes(int64_t m) {
+    return tg_align_up((size_t)(m + 1) * 8, 256) * 4 + tg_align_up((size_t)(m + 1) * 8, 256) + 512;
+}
+
+TG_API int tg_bubble_sinks(const double *S, int64_t n, const int32_t *bubbles, int64_t m, const int32_t *link_faces,
+                           const int64_t *src, const int64_t *dst, int64_t L, int64_t *sinks, void *ws,
+                           size_t ws_bytes, void *stream) {
+    if (!S || m < 1 || !sinks) return TG_ERR_ARG;
+    if (ws_bytes < tg_bubble_sinks_workspace_bytes(m)) return TG_ERR_WORKSPACE;
+    cudaStream_t st = tg_stream(stream);
+    TgArena ar(ws, ws_bytes);
+    unsigned long long *best = ar.take<unsigned long long>(m);
+    int64_t *hops = ar.take<int64_t>(m);
+    int64_t *tmp = ar.take<int64_t>(m);
+    double *g = ar.take<double>(L + 1);
+    int *changed = ar.take<int>(2);
+    TG_CUDA_CHECK(cudaMemsetAsync(best, 0, m * 8, st));
+    TG_CUDA_CHECK(cudaMemsetAsync(hops, 0xff, m * 8, st));   // -1: no outgoing link (a sink)
+    const unsigned T = 256;
+    if (L > 0) {
+        hop_gain_kernel<<<(unsigned)((L + T - 1) / T), T, 0, st>>>(S, n, bubbles, link_faces, src, dst, L, g, best);
+        // unsigned atomicMin: the unset value 0xff..ff is the largest
+        hop_pick_kernel<<<(unsigned)((L + T - 1) / T), T, 0, st>>>(src, dst, L, g, best, hops);
+    }
+    sink_init_kernel<<<(unsigned)((m + T - 1) / T), T, 0, st>>>(m, hops, sinks);
+    int64_t *a = sinks, *b = tmp;
+    for (int it = 0; it < 64; it++) {
+        TG_CUDA_CHECK(cudaMemsetAsync(changed, 0, 4, st));
+        sink_jump_kernel<<<(unsigned)((m + T - 1) / T), T, 0, st>>>(m, a, b, changed);
+        int h = 0;
+        TG_CUDA_CHECK(cudaMemcpyAsync(&h, changed, 4, cudaMemcpyDeviceToHost, st));
+        TG_CUDA_CHECK(cudaStreamSynchronize(st));
+        int64_t *t = a;
+        a = b;
+        b = t;
+        if (!h) break;
+    }
+    if (a != sinks) TG_CUDA_CHECK(cudaMemcpyAsync(sinks, a, m * 8, cudaMemcpyDeviceToDevice, st));
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+TG_API size_t tg_assign_workspace_bytes(int64_t n, int64_t m) {
+    return tg_align_up((size_t)4 * m * 8, 256) + tg_align_up((size_t)n * 8, 256) + 512;
+}
+
+TG_API int tg_assign_vertices(const tg_oracle_t *o, const int32_t *bubbles, int64_t m, const int64_t *sinks,
+                              int64_t *vb, int64_t *vc, void *ws, size_t ws_bytes, void *stream) {
+    if (!o || !bubbles || m < 1 || !vb || !vc) return TG_ERR_ARG;
+    const int64_t n = o->n;
+    if (ws_bytes < tg_assign_workspace_bytes(n, m)) return TG_ERR_WORKSPACE;
+    cudaStream_t st = tg_stream(stream);
+    TgArena ar(ws, ws_bytes);
+    double *mean = ar.take<double>(4 * m);
+    unsigned long long *best = ar.take<unsigned long long>(n);
+    TG_CUDA_CHECK(cudaMemsetAsync(best, 0xff, n * 8, st));
+    TG_CUDA_CHECK(cudaMemsetAsync(vb, 0x7f, n * 8, st));
+    const unsigned T = 256;
+    assign_mean_kernel<<<(unsigned)((4 * m + T - 1) / T), T, 0, st>>>(*o, bubbles, m, mean, best);
+    assign_pick_kernel<<<(unsigned)((4 * m + T - 1) / T), T, 0, st>>>(bubbles, m, mean, best, vb);
+    assign_conv_kernel<<<(unsigned)((n + T - 1) / T), T, 0, st>>>(n, vb, sinks, vc);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+TG_API int tg_group_blocks(const tg_oracle_t *o, const int32_t *perm, const int64_t *starts, int64_t count,
+                           const int64_t *boff, double *out, void *stream) {
+    if (!o || count < 0) return TG_ERR_ARG;
+    if (count == 0) return TG_OK;
+    int grid = (int)min((int64_t)tg_num_sms() * 16, count);
+    group_blocks_kernel<<<grid, 128, 0, tg_stream(stream)>>>(*o, perm, starts, count, boff, out);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+TG_API size_t tg_group_max_workspace_bytes(int64_t n) { return tg_align_up((size_t)n * 4, 256) + 256; }
+
+TG_API int tg_group_max_batch(const tg_oracle_t *o, const int32_t *perm, const int32_t *gid, const void *subs_v,
+                              int64_t nsub, const void *tiles_v, int64_t ntiles, double *out, int64_t out_len,
+                              void *ws, size_t ws_bytes, void *stream) {
+    if (!o || !perm || !gid || !subs_v || !tiles_v || !out || nsub < 0 || ntiles < 0) return TG_ERR_ARG;
+    const int64_t n = o->n;
+    if (ws_bytes < tg_group_max_workspace_bytes(n)) return TG_ERR_WORKSPACE;
+    const GmSub *subs = reinterpret_cast<const GmSub *>(subs_v);
+    const GmTile *tiles = reinterpret_cast<const GmTile *>(tiles_v);
+    cudaStream_t st = tg_stream(stream);
+    int32_t *pos = reinterpret_cast<int32_t *>(ws);
+    TG_CUDA_CHECK(cudaMemsetAsync(out, 0, (size_t)out_len * 8, st));
+    if (nsub == 0) return TG_OK;
+    TG_CUDA_CHECK(cudaMemsetAsync(pos, 0xff, (size_t)n * 4, st));
+    pos_fill_kernel<<<(unsigned)min(nsub, (int64_t)65535), 256, 0, st>>>(subs, nsub, perm, pos);
+    if (ntiles > 0) {
+        int grid = (int)min((int64_t)tg_num_sms() * 8, ntiles);
+        group_max_tile_kernel<<<grid, GM_T, 0, st>>>(*o, perm, gid, pos, subs, tiles, ntiles,
+                                                   reinterpret_cast<unsigned long long *>(out));
+    }
+    group_max_finalize_kernel<<<(unsigned)min(nsub, (int64_t)65535), 256, 0, st>>>(subs, nsub, o->mode, out);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+TG_API int tg_nn_chain_batch(double *mats, const int64_t *mat_off, const int64_t *sizes, int64_t count,
+                             const int64_t *merge_off, int64_t *lefts, int64_t *rights, double *heights,
+                             const int64_t *aux_off, uint8_t *active, int64_t *slot, int64_t *chain, void *stream) {
+    if (count < 0 || !mats) return TG_ERR_ARG;
+    if (count == 0) return TG_OK;
+    int64_t warps = count;
+    int threads = 128;
+    int64_t blocks = (warps * 32 + threads - 1) / threads;
+    if (blocks > (int64_t)tg_num_sms() * 32) blocks = (int64_t)tg_num_sms() * 32;
+    nn_chain_kernel<<<(unsigned)blocks, threads, 0, tg_stream(stream)>>>(mats, mat_off, sizes, count, merge_off, lefts,
+                                                                       rights, heights, active, slot, chain, aux_off);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+// public block / query accessors (apsp.py:88-94, 127-158)
+TG_API int tg_oracle_block(const tg_oracle_t *o, const int32_t *rows, int64_t nr, const int32_t *cols, int64_t nc,
+                           int32_t query_semantics, double *out, void *stream) {
+    if (!o || nr < 0 || nc < 0 || !out) return TG_ERR_ARG;
+    if (nr * nc == 0) return TG_OK;
+    oracle_block_kernel<<<(unsigned)((nr * nc + 255) / 256), 256, 0, tg_stream(stream)>>>(*o, rows, nr, cols, nc,
+                                                                                          query_semantics, out);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}

@@ -1,0 +1,109 @@
+"""GPU parity for APSP + DBHT + the whole pipeline vs the reference goldens.
+
+Every array is compared bit-exactly (distances included: the label-correcting
+searches reach the same fp64 fixed point as binary-heap Dijkstra), and the
+dendrogram parity fingerprint is the sha256 of serialize_dendrogram
+(pipeline.py:226-227).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SMALL = ["n4_u", "n5_flat", "n6_u", "n20_round", "n30_u", "n40_q", "n60_u", "n120_q", "n50_s", "n200_s",
+         "c1_n300", "c4_n400"]
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_2408_09399_b200 as p
+    p._native.load()
+    return p
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_stages_match_golden(name, small_cases, digests, pkg):
+    c = small_cases[name]
+    rec = digests[name]
+    S = c["S"]
+    lists = pkg.sort_neighbor_lists(S)
+    g = pkg.build_tmfg_heap(S, lists)
+    w = pkg.to_weighted(g, S)
+    for key in ("indptr", "neighbors", "lengths", "strength"):
+        assert np.array_equal(getattr(w, key), c[f"w_{key}"]), key
+    tree = pkg.build_bubble_tree(g)
+    for key in ("bubbles", "links", "link_faces"):
+        assert np.array_equal(getattr(tree, key), c[f"tree_{key}"]), key
+    dtree = pkg.orient_edges(tree, S)
+    assert np.array_equal(dtree.sources, c["dtree_sources"])
+    assert np.array_equal(dtree.targets, c["dtree_targets"])
+    assert np.array_equal(pkg.bubble_sinks(dtree, g), c["sinks"])
+    for mode in ("exact", "hub"):
+        o = pkg.apsp_exact(w) if mode == "exact" else pkg.apsp_hub(w)
+        if mode == "exact":
+            assert np.array_equal(o.matrix, c["exact_D"])
+        else:
+            for key in ("hubs", "hub_dist", "nearest_hub", "nearest_dist", "radii", "near_indptr", "near_ids",
+                        "near_dist"):
+                assert np.array_equal(getattr(o, key), c[f"hub_{key}"]), key
+        asg = pkg.assign_vertices(g, dtree, o)
+        assert np.array_equal(asg.vertex_bubble, c[f"{mode}_vertex_bubble"]), mode
+        assert np.array_equal(asg.vertex_converging, c[f"{mode}_vertex_converging"]), mode
+        d = pkg.build_hierarchy(asg, dtree, o)
+        for key in ("lefts", "rights", "heights", "sizes"):
+            assert np.array_equal(getattr(d, key), c[f"{mode}_dend_{key}"]), (mode, key)
+        import hashlib
+        assert hashlib.sha256(pkg.serialize_dendrogram(d).encode()).hexdigest() == rec[f"{mode}_digest"]
+        assert np.array_equal(pkg.cut(d, rec["k"]), c[f"{mode}_labels"])
+
+
+@pytest.mark.parametrize("config,mode", [(1, "exact"), (1, "hub"), (2, "exact"), (2, "hub"), (4, "exact"),
+                                         (4, "hub"), (3, "hub")])
+def test_pipeline_digest_configs(config, mode, digests, oracle, pkg):
+    """Full BASELINE configs on the reference's own S: same dendrogram digest and labels."""
+    from paper_2408_09399_b200 import synth
+    rec = digests[f"config{config}"]
+    x, labels = synth.generate(config)
+    S = oracle.pearson_similarity(x)
+    assert oracle.sha(S) == rec["S"]
+    report, graph, dend, flat = pkg.run_stages(pkg.PipelineConfig(apsp_mode=mode, k=rec["k"]), S, labels)
+    assert report.digest == rec[f"{mode}_digest"]
+    assert oracle.sha(flat) == rec[f"{mode}_labels"]
+    assert report.num_converging == rec[f"{mode}_num_converging"]
+
+
+def test_hub_query_and_block_semantics(small_cases, pkg):
+    c = small_cases["n200_s"]
+    S = c["S"]
+    g = pkg.build_tmfg_heap(S, pkg.sort_neighbor_lists(S))
+    o = pkg.apsp_hub(pkg.to_weighted(g, S))
+    rows = np.array([0, 3, 7, 29, 150])
+    cols = np.array([1, 3, 15, 199])
+    blk = o.block(rows, cols)
+    hd = o.hub_dist
+    for i, u in enumerate(rows):
+        for j, v in enumerate(cols):
+            e = float(np.min(hd[:, u] + hd[:, v]))
+            a = o._near_lookup(int(u), int(v))
+            b = o._near_lookup(int(v), int(u))
+            want_block = b if b is not None else (a if a is not None else e)
+            assert blk[i, j] == want_block
+            lo, hi = min(u, v), max(u, v)
+            q1, q2 = o._near_lookup(int(lo), int(hi)), o._near_lookup(int(hi), int(lo))
+            want_q = 0.0 if u == v else (q1 if q1 is not None else (q2 if q2 is not None else e))
+            assert o.query(int(u), int(v)) == want_q
+
+
+def test_corrupt_trace_raises(small_cases, pkg):
+    S = small_cases["n30_u"]["S"]
+    g = pkg.build_tmfg_heap(S, pkg.sort_neighbor_lists(S))
+    bad = g.trace.copy()
+    v, x, y, _ = bad[2]
+    bad[2, 1:] = sorted((int(v), int(x), int(y)))
+    g2 = pkg.TmfgGraph(n=g.n, edges=g.edges, weights=g.weights, initial_clique=g.initial_clique, trace=bad,
+                       faces=g.faces)
+    with pytest.raises(pkg.TraceError):
+        pkg.build_bubble_tree(g2)
