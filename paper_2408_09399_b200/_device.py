@@ -115,6 +115,7 @@ class LazyHost:
         self.dev = dev
         self._host = host
         self.dtype = dtype
+        self._conv = {}
 
     @property
     def host(self) -> np.ndarray:
@@ -126,8 +127,11 @@ class LazyHost:
         return self._host
 
     def device(self, dtype=None):
+        """Device tensor (converted copies are cached so raw pointers stay valid)."""
         if self.dev is None:
             self.dev = to_device(self._host)
         if dtype is not None and self.dev.dtype != dtype:
-            return self.dev.to(dtype)
+            if dtype not in self._conv:
+                self._conv[dtype] = self.dev.to(dtype).contiguous()
+            return self._conv[dtype]
         return self.dev

@@ -371,7 +371,8 @@ group_max_tile_kernel(tg_oracle_t o, const int32_t *__restrict__ perm, const int
                 for (int i = tid >> 2; i < rows; i += GM_T / 4) {
                     int u = ru[i];
                     for (int64_t k = ip[u] + (tid & 3); k < ip[u + 1]; k += 4) {
-                        int p = pos[ids[k]] - tl.j0;
+                        // positions are global: only vertices of this sub-problem's column range hit
+                        int p = pos[ids[k]] - (int)(sb.perm_off + tl.j0);
                         if (p >= 0 && p < cols) E[i][p] = dd[k];
                     }
                 }
@@ -505,7 +506,8 @@ __global__ void nn_chain_kernel(double *mats, const int64_t *mat_off, const int6
 
 __global__ void pos_fill_kernel(const GmSub *subs, int64_t nsub, const int32_t *perm, int32_t *pos) {
     for (int64_t p = blockIdx.x; p < nsub; p += gridDim.x)
-        for (int i = threadIdx.x; i < subs[p].len; i += blockDim.x) pos[perm[subs[p].perm_off + i]] = i;
+        for (int i = threadIdx.x; i < subs[p].len; i += blockDim.x)
+            pos[perm[subs[p].perm_off + i]] = (int32_t)(subs[p].perm_off + i);  // global position
 }
 
 __global__ void oracle_block_kernel(tg_oracle_t o, const int32_t *rows, int64_t nr, const int32_t *cols, int64_t nc,

@@ -163,7 +163,9 @@ def bubble_sinks(dtree: DirectedBubbleTree, graph) -> np.ndarray:
 def assign_vertices(graph, dtree: DirectedBubbleTree, oracle) -> BubbleAssignment:
     """Assign each vertex to its closest containing bubble (dbht.py:178-214)."""
     t = D.torch()
-    Sd = getattr(dtree, "_S_device", None) or getattr(graph, "S_device", None)
+    Sd = getattr(dtree, "_S_device", None)
+    if Sd is None:
+        Sd = getattr(graph, "S_device", None)
     sinks = bubble_sinks_device(dtree, Sd)
     b, _, _ = dtree.tree.dev()
     m = dtree.num_bubbles
@@ -281,8 +283,11 @@ def build_hierarchy(assignment: BubbleAssignment, dtree: DirectedBubbleTree, ora
         np.cumsum(sizes * sizes, out=boff[1:])
         blocks = D.empty((int(boff[-1]),), t.float64)
         s = _oracle_struct(oracle)
-        N.call("tg_group_blocks", s, N.ptr(D.to_device(perm, t.int32)), N.ptr(D.to_device(gstarts, t.int64)),
-               len(multi), N.ptr(D.to_device(boff, t.int64)), N.ptr(blocks), N.stream_ptr())
+        perm_d = D.to_device(perm, t.int32)
+        gst_d = D.to_device(gstarts, t.int64)
+        boff_d = D.to_device(boff, t.int64)
+        N.call("tg_group_blocks", s, N.ptr(perm_d), N.ptr(gst_d), len(multi), N.ptr(boff_d), N.ptr(blocks),
+               N.stream_ptr())
         roots, rows = _run_linkages(oracle, blocks, sizes, boff[:-1], [list(groups[b]) for b in multi], records, n)
         for b, r, rr in zip(multi, roots, rows):
             group_root[b] = r
