@@ -1,0 +1,364 @@
+"""bench.py -- TMFG-DBHT on B200: one pipeline pass per step (BASELINE.json config 3).
+
+Workload (BASELINE.json configs[2], the headline size): n = 10,000 clustered time
+series of length L = 512 (20 Dirichlet(1) clusters, random-walk prototypes,
+N(0,1) x U(0.5,2) noise, z-normalised; seeded synthetic data standing in for the
+paper's UCR workloads), hub-approximate APSP.
+
+A step = fp64 Pearson similarity -> validation -> per-row neighbour sort (+ fused
+clique row sums) -> heap TMFG -> CSR -> hub APSP -> bubble tree / orientation /
+assignment -> 3-layer complete-linkage dendrogram -> cut; the dendrogram and the
+labels are read back to the host.
+
+  value  : device-resident step time (series already in HBM), ms, lower is better
+  e2e    : the same through the public API with HOST buffers (H2D of the series,
+           D2H of dendrogram + labels inside the timed region)
+  roofline: the row-sort kernel (the metric's second half) against measured HBM
+  cpu_baseline: the CPU oracle (C + numpy restatement of the reference) on this
+           host's cores, one full step
+Multi-GPU: the path does not shard (the TMFG insertion chain is serial), so
+`--gpus N` runs N independent replicas (different seeds), no collective in the
+data path ("replicas only"); value is the max over ranks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+import numpy as np  # noqa: E402
+
+METRIC = "TMFG-DBHT wall ms at n=10k; row-sort Gkeys/s & fraction of HBM roofline"
+UNIT = "ms"
+
+
+def _peaks():
+    p = REPO / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6458.1)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._proc = None
+
+    def start(self):
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self._proc = None
+        return self
+
+    def _read(self):
+        for line in self._proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 6:
+                self.rows.append(parts)
+
+    def stop(self) -> dict:
+        if self._proc is not None:
+            time.sleep(0.25)
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=2)
+            except Exception:
+                self._proc.kill()
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def _max_over_ranks(x: float, world: int, device) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ------------------------------------------------------------------ B200 arm
+def run_b200(args, world, rank, local):
+    import torch
+
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=device)
+    import paper_2408_09399_b200 as P
+    from paper_2408_09399_b200 import _native as N
+    from paper_2408_09399_b200 import apsp, dbht, linkage, simmatrix, synth, tmfg
+    from paper_2408_09399_b200.pipeline import run_series
+
+    N.load()
+    cfg = args.config
+    x_host, labels = synth.generate(cfg, n=args.n, seed=synth.DEFAULT_SEED + rank)
+    n, L = x_host.shape
+    k = synth.num_clusters(cfg)
+    mode = "hub" if cfg in (3, 5) else args.apsp
+    X = torch.from_numpy(x_host).to(device)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=device)  # > L2 (126 MB)
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+
+    def step(record: dict | None):
+        """One device-resident pipeline pass with per-stage CUDA events."""
+        marks = [ev() for _ in range(8)]
+        marks[0].record()
+        S = simmatrix.pearson_similarity_device(X)
+        marks[1].record()
+        simmatrix.validate_device(S)
+        order, rowsum = simmatrix.sort_rows_device(S, with_rowsum=True)
+        marks[2].record()
+        clique = tmfg.initial_clique_device(S, rowsum)
+        out = tmfg.build_tmfg_heap_device(S, order, clique)
+        marks[3].record()
+        graph = tmfg.TmfgGraph(n=n, edges=out["edges"], weights=tmfg.edge_weights_device(S, out["edges"]),
+                               initial_clique=clique, trace=out["trace"], faces=out["faces"], variant="heap",
+                               host_fid=out["host_fid"], S_device=S)
+        graph._S_host = S
+        ip, nb, ln, st = apsp.to_weighted_device(S, out["edges"], n)
+        w = apsp.WeightedTmfg(n=n, indptr=ip, neighbors=nb, lengths=ln, strength=st)
+        oracle = apsp.apsp_hub(w) if mode == "hub" else apsp.apsp_exact(w)
+        marks[4].record()
+        tree = dbht.build_bubble_tree(graph)
+        dtree = dbht.orient_edges(tree, S)
+        asg = dbht.assign_vertices(graph, dtree, oracle)
+        marks[5].record()
+        d = dbht.build_hierarchy(asg, dtree, oracle)
+        flat = linkage.cut(d, k)
+        marks[6].record()
+        torch.cuda.synchronize()
+        if record is not None:
+            names = ["similarity", "validate+sort", "tmfg_insertion", "apsp", "dbht_assign", "linkage"]
+            for i, nm in enumerate(names):
+                record.setdefault(nm, []).append(marks[i].elapsed_time(marks[i + 1]))
+        return d, flat, S, order
+
+    # warm-up (also the sort-kernel timing source below)
+    for _ in range(max(args.warmup, 0)):
+        step(None)
+    torch.cuda.synchronize()
+
+    # ---- timed region (device-resident)
+    sampler = ClockSampler(local).start() if rank == 0 else None
+    stage = {}
+    per_step = []
+    launches0 = N.load().tg_launch_count()
+    _barrier(world)
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    for _ in range(args.steps):
+        flush.zero_()  # L2 flush between timed steps (not inside a step's events)
+        a, b = ev(), ev()
+        a.record()
+        d, flat, S, order = step(stage)
+        b.record()
+        torch.cuda.synchronize()
+        per_step.append(a.elapsed_time(b))
+    torch.cuda.synchronize()
+    _barrier(world)
+    wall = time.perf_counter() - wall0
+    launches = int(N.load().tg_launch_count() - launches0)
+    clocks = sampler.stop() if sampler else None
+    ms = float(np.mean(per_step))
+    ms_max = _max_over_ranks(ms, world, device)
+
+    # ---- row-sort roofline: kernel timed alone on the stream it runs on
+    sort_ms = []
+    for _ in range(5):
+        flush.zero_()
+        a, b = ev(), ev()
+        a.record()
+        simmatrix.sort_rows_device(S, with_rowsum=True)
+        b.record()
+        torch.cuda.synchronize()
+        sort_ms.append(a.elapsed_time(b))
+    sort_avg = float(np.mean(sort_ms))
+    sort_bytes = 8 * n * n + 4 * n * (n - 1)
+    hbm_peak, peak_kind = _peaks()
+    achieved = sort_bytes / (sort_avg * 1e-3) / 1e9
+    traffic = None
+    tp = REPO / "profiles" / "round1_sort_traffic.json"
+    if tp.exists():
+        try:
+            traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    # fp64 similarity (secondary kernel)
+    sim_ms = float(np.mean(stage["similarity"]))
+    sim_flops = n * (n + 1) * L
+
+    # ---- e2e through the public API with host buffers
+    e2e_ms = []
+    h2d = x_host.nbytes
+    d2h = 0
+    for _ in range(max(1, min(args.steps, 3))):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep, dend, lab_out = run_series(x_host, k=k, apsp_mode=mode)
+        torch.cuda.synchronize()
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        d2h = dend.lefts.nbytes + dend.rights.nbytes + dend.heights.nbytes + dend.sizes.nbytes + lab_out.nbytes
+    e2e = float(np.mean(e2e_ms))
+    e2e = _max_over_ranks(e2e, world, device)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample(cfg, args.n)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(ms_max, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_max, 3), "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"BASELINE config {cfg}: n={n} series, L={L}, {mode} APSP, heap TMFG",
+                       "n": n, "L": L, "apsp": mode, "k": k, "parallelism": f"replicas{world}",
+                       "l2": "flushed (256 MB write) between timed steps; S (8n^2 B) exceeds L2"},
+            "stage_ms": {kk: round(float(np.mean(vv)), 3) for kk, vv in stage.items()},
+            "roofline": {"bound": "hbm", "kernel": "row_sort_smem_kernel (per-row neighbour sort)",
+                         "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                         "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
+                         "algorithmic_bytes": sort_bytes, "kernel_ms": round(sort_avg, 4),
+                         "gkeys_per_s": round(n * (n - 1) / (sort_avg * 1e-3) / 1e9, 2),
+                         "peak_kind": peak_kind},
+            "similarity": {"ms": round(sim_ms, 3), "tflops_alg": round(sim_flops / (sim_ms * 1e-3) / 1e12, 2),
+                           "flops_alg": sim_flops},
+            "e2e": {"value": round(e2e, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": launches // max(args.steps, 1),
+            "gpu_launches_timed_total": launches,
+            "wall_s_timed": round(wall, 3),
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def cpu_baseline_sample(cfg, n_override=None) -> dict:
+    """The CPU oracle on this host's cores: one full pipeline step of the same workload."""
+    from oracle import oracle as orc
+    from paper_2408_09399_b200 import synth
+
+    x, labels = synth.generate(cfg, n=n_override)
+    k = synth.num_clusters(cfg)
+    mode = "hub" if cfg in (3, 5) else "exact"
+    orc.set_threads(os.cpu_count() or 1)
+    t0 = time.perf_counter()
+    S = orc.pearson_similarity(x)
+    orc.run_stages(S, k, mode)
+    dt = (time.perf_counter() - t0) * 1e3
+    return {"value": round(dt, 1), "unit": UNIT, "cores": orc.num_threads(), "kind": "port",
+            "sample": f"one full step (Pearson + sort + heap TMFG + {mode} APSP + DBHT + cut) of config {cfg}, "
+                      f"n={x.shape[0]}, C/OpenMP + numpy oracle"}
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args, world, rank):
+    """The reference's CPU path, restated by the oracle (the reference itself is a
+    Python package that is not installed on the GPU box), on all host threads."""
+    if world > 1 and rank != 0:
+        return
+    from oracle import oracle as orc
+    from paper_2408_09399_b200 import synth
+
+    cfg = args.config
+    x, labels = synth.generate(cfg, n=args.n)
+    k = synth.num_clusters(cfg)
+    mode = "hub" if cfg in (3, 5) else args.apsp
+    orc.set_threads(os.cpu_count() or 1)
+    xs, _ = synth.generate(1, n=200)
+    for _ in range(max(args.warmup, 0)):
+        Ss = orc.pearson_similarity(xs)
+        orc.run_stages(Ss, 5, mode)
+    times = []
+    steps = max(1, min(args.steps, 5))
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        S = orc.pearson_similarity(x)
+        orc.run_stages(S, k, mode)
+        times.append((time.perf_counter() - t0) * 1e3)
+    v = float(np.mean(times))
+    line = {
+        "metric": METRIC, "value": round(v, 1), "unit": UNIT, "n_gpus": world, "steps": steps,
+        "warmup": args.warmup, "ms_per_step": round(v, 1), "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"BASELINE config {cfg}: n={x.shape[0]} series, L={x.shape[1]}, {mode} APSP, "
+                               "heap TMFG", "n": int(x.shape[0]), "L": int(x.shape[1]), "apsp": mode, "k": k,
+                   "parallelism": "host threads"},
+        "cpu_baseline": {"value": round(v, 1), "unit": UNIT, "cores": orc.num_threads(), "kind": "port",
+                         "sample": f"{steps} full steps of config {cfg} (C/OpenMP + numpy restatement of the "
+                                   "reference, bit-identical outputs)"},
+        "e2e": {"value": round(v, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--apsp", default="hub", choices=["exact", "hub"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_b200(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

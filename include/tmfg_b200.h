@@ -45,6 +45,8 @@ extern "C" {
 
 int tg_abi_version(void);
 const char *tg_last_error(void);
+/* kernels launched by this library so far (process-wide counter) */
+long long tg_launch_count(void);
 
 /* ---------------------------------------------------------------- similarity */
 

@@ -37,7 +37,7 @@ from .dbht import (
     orient_edges,
 )
 from .linkage import Dendrogram, cut, dendrogram_from_merges, nn_chain_merges, serialize_dendrogram
-from .pipeline import PipelineConfig, RunReport, StageError, run_stages
+from .pipeline import PipelineConfig, RunReport, StageError, run_series, run_stages
 from .simmatrix import (
     DataError,
     Dataset,

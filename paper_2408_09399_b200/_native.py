@@ -58,6 +58,7 @@ class TgOracle(ctypes.Structure):
 _PROTOS = {
     "tg_abi_version": (ctypes.c_int, []),
     "tg_last_error": (ctypes.c_char_p, []),
+    "tg_launch_count": (ctypes.c_longlong, []),
     "tg_pearson_workspace_bytes": (c_sz, [c_i64, c_i64]),
     "tg_pearson_f64": (ctypes.c_int, [c_p, c_i64, c_i64, c_p, c_p, c_sz, c_p]),
     "tg_validate_f64": (ctypes.c_int, [c_p, c_i64, c_p, c_p]),

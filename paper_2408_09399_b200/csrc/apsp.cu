@@ -568,14 +568,14 @@ TG_API int tg_to_weighted(const double *S, int64_t n, const int32_t *edges, int6
     cudaStream_t st = tg_stream(stream);
     TG_CUDA_CHECK(cudaMemsetAsync(deg, 0, n * 4, st));
     TG_CUDA_CHECK(cudaMemsetAsync(cursor, 0, n * 4, st));
-    if (m > 0) deg_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(edges, m, deg);
-    scan_i32_to_i64_kernel<<<1, 1024, 0, st>>>(deg, n, indptr);
-    if (m > 0) scatter_edges_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(edges, m, indptr, cursor, slot_edge);
+    if (m > 0) deg_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(edges, m, deg); tg_count_launch(1);
+    scan_i32_to_i64_kernel<<<1, 1024, 0, st>>>(deg, n, indptr); tg_count_launch(1);
+    if (m > 0) scatter_edges_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(edges, m, indptr, cursor, slot_edge); tg_count_launch(1);
     int grid = tg_num_sms() * 8;
     if (grid > n) grid = (int)n;
     const int cap = 4096;  // incident-edge ids cached in shared memory; larger degrees read global
     size_t smem = (size_t)cap * sizeof(int32_t);
-    fill_csr_kernel<<<grid, 128, smem, st>>>(S, n, edges, indptr, slot_edge, nbr, len, strength, cap);
+    fill_csr_kernel<<<grid, 128, smem, st>>>(S, n, edges, indptr, slot_edge, nbr, len, strength, cap); tg_count_launch(1);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
@@ -600,7 +600,7 @@ TG_API int tg_sssp_rows(const int64_t *indptr, const int32_t *nbr, const double 
         int64_t grid = (int64_t)tg_num_sms() * per_sm;
         if (grid > n_src) grid = n_src;
         sssp_rows_kernel<true><<<(unsigned)grid, SS_T, smem, st>>>(indptr, nbr, len, n, sources, n_src, dist, nullptr,
-                                                                   nullptr);
+                                                                   nullptr); tg_count_launch(1);
     } else {
         if (ws_bytes < tg_sssp_workspace_bytes(n, n_src)) return TG_ERR_WORKSPACE;
         int64_t grid = (int64_t)tg_num_sms() * 2;
@@ -609,7 +609,7 @@ TG_API int tg_sssp_rows(const int64_t *indptr, const int32_t *nbr, const double 
         uint32_t *stamp = ar.take<uint32_t>((size_t)grid * n);
         int32_t *q = ar.take<int32_t>((size_t)grid * 2 * n);
         if (!stamp || !q) return TG_ERR_WORKSPACE;
-        sssp_rows_kernel<false><<<(unsigned)grid, SS_T, 0, st>>>(indptr, nbr, len, n, sources, n_src, dist, stamp, q);
+        sssp_rows_kernel<false><<<(unsigned)grid, SS_T, 0, st>>>(indptr, nbr, len, n, sources, n_src, dist, stamp, q); tg_count_launch(1);
     }
     TG_LAUNCH_CHECK();
     return TG_OK;
@@ -621,7 +621,7 @@ TG_API int tg_select_hubs(const double *strength, int64_t n, int64_t H, int64_t 
                           void *stream) {
     if (n < 1 || H < 1 || H > n || !strength || !hubs) return TG_ERR_ARG;
     if (ws_bytes < tg_select_hubs_workspace_bytes(n)) return TG_ERR_WORKSPACE;
-    select_hubs_kernel<<<1, 1024, 0, tg_stream(stream)>>>(strength, n, H, hubs, reinterpret_cast<int32_t *>(ws));
+    select_hubs_kernel<<<1, 1024, 0, tg_stream(stream)>>>(strength, n, H, hubs, reinterpret_cast<int32_t *>(ws)); tg_count_launch(1);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
@@ -630,7 +630,7 @@ TG_API int tg_nearest_hub(const double *hub_dist, const int64_t *hubs, int64_t H
                           int64_t *nh, double *nd, double *radii, void *stream) {
     if (n < 1 || H < 1 || !hub_dist || !hubs) return TG_ERR_ARG;
     nearest_hub_kernel<<<(unsigned)((n + 255) / 256), 256, 0, tg_stream(stream)>>>(hub_dist, hubs, H, n, radius_factor,
-                                                                                   nh, nd, radii);
+                                                                                   nh, nd, radii); tg_count_launch(1);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
@@ -680,9 +680,9 @@ TG_API int tg_truncated(const int64_t *indptr, const int32_t *nbr, const double 
     size_t smem = (size_t)((n + 31) / 32) * 4;
     TG_CUDA_CHECK(cudaFuncSetAttribute(truncated_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     truncated_kernel<<<grid, TR_T, smem, st>>>(indptr, nbr, len, n, radii, gd, gs, gq, gt, ctr, ctr + 1, capacity,
-                                               pool_ids, pool_dist, src_off, counts);
+                                               pool_ids, pool_dist, src_off, counts); tg_count_launch(1);
     TG_LAUNCH_CHECK();
-    scan_i64_kernel<<<1, 1024, 0, st>>>(counts, n, near_indptr);
+    scan_i64_kernel<<<1, 1024, 0, st>>>(counts, n, near_indptr); tg_count_launch(1);
     TG_LAUNCH_CHECK();
     int64_t total = 0;
     TG_CUDA_CHECK(cudaMemcpyAsync(&total, near_indptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -690,7 +690,7 @@ TG_API int tg_truncated(const int64_t *indptr, const int32_t *nbr, const double 
     *total_out = total;
     if (total > capacity) return TG_ERR_CAPACITY;
     compact_pool_kernel<<<tg_num_sms() * 8, 256, 0, st>>>(n, src_off, near_indptr, pool_ids, pool_dist, near_ids,
-                                                         near_dist);
+                                                         near_dist); tg_count_launch(1);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
@@ -710,9 +710,9 @@ TG_API int tg_near_transpose(int64_t n, const int64_t *ip, const int32_t *ids, c
     TG_CUDA_CHECK(cudaStreamSynchronize(st));
     TG_CUDA_CHECK(cudaMemsetAsync(cnt, 0, n * 4, st));
     TG_CUDA_CHECK(cudaMemsetAsync(cur, 0, n * 4, st));
-    if (E > 0) near_count_kernel<<<(unsigned)((E + 255) / 256), 256, 0, st>>>(ids, E, cnt);
-    scan_i32_to_i64_kernel<<<1, 1024, 0, st>>>(cnt, n, rip);
-    if (E > 0) near_scatter_kernel<<<tg_num_sms() * 8, 128, 0, st>>>(n, ip, ids, dd, rip, cur, rids, rdd);
+    if (E > 0) near_count_kernel<<<(unsigned)((E + 255) / 256), 256, 0, st>>>(ids, E, cnt); tg_count_launch(1);
+    scan_i32_to_i64_kernel<<<1, 1024, 0, st>>>(cnt, n, rip); tg_count_launch(1);
+    if (E > 0) near_scatter_kernel<<<tg_num_sms() * 8, 128, 0, st>>>(n, ip, ids, dd, rip, cur, rids, rdd); tg_count_launch(1);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }

@@ -20,6 +20,7 @@
 #define TG_LAUNCH_CHECK() TG_CUDA_CHECK(cudaGetLastError())
 
 void tg_set_last_error(cudaError_t e, const char *file, int line);
+void tg_count_launch(int k);
 
 static inline cudaStream_t tg_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 

@@ -544,15 +544,15 @@ TG_API int tg_bubble_tree(const int32_t *clique, const int32_t *trace, int64_t n
     TG_CUDA_CHECK(cudaMemsetAsync(htab, 0xff, hs * 16, st));
     TG_CUDA_CHECK(cudaMemset2DAsync(htab, 16, 0, 8, hs, st));
     const unsigned T = 256;
-    ins_time_kernel<<<(unsigned)((n + T - 1) / T), T, 0, st>>>(n, ins_t);
-    ins_time_set_kernel<<<(unsigned)((max(nt, (int64_t)4) + T - 1) / T), T, 0, st>>>(clique, trace, nt, ins_t);
+    ins_time_kernel<<<(unsigned)((n + T - 1) / T), T, 0, st>>>(n, ins_t); tg_count_launch(1);
+    ins_time_set_kernel<<<(unsigned)((max(nt, (int64_t)4) + T - 1) / T), T, 0, st>>>(clique, trace, nt, ins_t); tg_count_launch(1);
     if (nt > 0) {
         bubble_tree_kernel<<<(unsigned)((nt + T - 1) / T), T, 0, st>>>(clique, trace, nt, n, ins_t, htab,
-                                                                     (int64_t)hs - 1, bubbles, links, link_faces, bad);
-        bubble_dup_kernel<<<(unsigned)((nt + T - 1) / T), T, 0, st>>>(trace, nt, n, htab, (int64_t)hs - 1, bad);
+                                                                     (int64_t)hs - 1, bubbles, links, link_faces, bad); tg_count_launch(1);
+        bubble_dup_kernel<<<(unsigned)((nt + T - 1) / T), T, 0, st>>>(trace, nt, n, htab, (int64_t)hs - 1, bad); tg_count_launch(1);
     } else {
         bubble_tree_kernel<<<1, 32, 0, st>>>(clique, trace, 0, n, ins_t, htab, (int64_t)hs - 1, bubbles, links,
-                                            link_faces, bad);
+                                            link_faces, bad); tg_count_launch(1);
     }
     TG_LAUNCH_CHECK();
     unsigned long long b = 0;
@@ -567,7 +567,7 @@ TG_API int tg_orient_edges(const double *S, int64_t n, const int32_t *bubbles, c
     if (!S || L < 0) return TG_ERR_ARG;
     if (L == 0) return TG_OK;
     orient_kernel<<<(unsigned)((L + 255) / 256), 256, 0, tg_stream(stream)>>>(S, n, bubbles, links, link_faces, L, src,
-                                                                             dst);
+                                                                             dst); tg_count_launch(1);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
@@ -592,15 +592,15 @@ TG_API int tg_bubble_sinks(const double *S, int64_t n, const int32_t *bubbles, i
     TG_CUDA_CHECK(cudaMemsetAsync(hops, 0xff, m * 8, st));   // -1: no outgoing link (a sink)
     const unsigned T = 256;
     if (L > 0) {
-        hop_gain_kernel<<<(unsigned)((L + T - 1) / T), T, 0, st>>>(S, n, bubbles, link_faces, src, dst, L, g, best);
+        hop_gain_kernel<<<(unsigned)((L + T - 1) / T), T, 0, st>>>(S, n, bubbles, link_faces, src, dst, L, g, best); tg_count_launch(1);
         // unsigned atomicMin: the unset value 0xff..ff is the largest
-        hop_pick_kernel<<<(unsigned)((L + T - 1) / T), T, 0, st>>>(src, dst, L, g, best, hops);
+        hop_pick_kernel<<<(unsigned)((L + T - 1) / T), T, 0, st>>>(src, dst, L, g, best, hops); tg_count_launch(1);
     }
-    sink_init_kernel<<<(unsigned)((m + T - 1) / T), T, 0, st>>>(m, hops, sinks);
+    sink_init_kernel<<<(unsigned)((m + T - 1) / T), T, 0, st>>>(m, hops, sinks); tg_count_launch(1);
     int64_t *a = sinks, *b = tmp;
     for (int it = 0; it < 64; it++) {
         TG_CUDA_CHECK(cudaMemsetAsync(changed, 0, 4, st));
-        sink_jump_kernel<<<(unsigned)((m + T - 1) / T), T, 0, st>>>(m, a, b, changed);
+        sink_jump_kernel<<<(unsigned)((m + T - 1) / T), T, 0, st>>>(m, a, b, changed); tg_count_launch(1);
         int h = 0;
         TG_CUDA_CHECK(cudaMemcpyAsync(&h, changed, 4, cudaMemcpyDeviceToHost, st));
         TG_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -630,9 +630,9 @@ TG_API int tg_assign_vertices(const tg_oracle_t *o, const int32_t *bubbles, int6
     TG_CUDA_CHECK(cudaMemsetAsync(best, 0xff, n * 8, st));
     TG_CUDA_CHECK(cudaMemsetAsync(vb, 0x7f, n * 8, st));
     const unsigned T = 256;
-    assign_mean_kernel<<<(unsigned)((4 * m + T - 1) / T), T, 0, st>>>(*o, bubbles, m, mean, best);
-    assign_pick_kernel<<<(unsigned)((4 * m + T - 1) / T), T, 0, st>>>(bubbles, m, mean, best, vb);
-    assign_conv_kernel<<<(unsigned)((n + T - 1) / T), T, 0, st>>>(n, vb, sinks, vc);
+    assign_mean_kernel<<<(unsigned)((4 * m + T - 1) / T), T, 0, st>>>(*o, bubbles, m, mean, best); tg_count_launch(1);
+    assign_pick_kernel<<<(unsigned)((4 * m + T - 1) / T), T, 0, st>>>(bubbles, m, mean, best, vb); tg_count_launch(1);
+    assign_conv_kernel<<<(unsigned)((n + T - 1) / T), T, 0, st>>>(n, vb, sinks, vc); tg_count_launch(1);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
@@ -642,7 +642,7 @@ TG_API int tg_group_blocks(const tg_oracle_t *o, const int32_t *perm, const int6
     if (!o || count < 0) return TG_ERR_ARG;
     if (count == 0) return TG_OK;
     int grid = (int)min((int64_t)tg_num_sms() * 16, count);
-    group_blocks_kernel<<<grid, 128, 0, tg_stream(stream)>>>(*o, perm, starts, count, boff, out);
+    group_blocks_kernel<<<grid, 128, 0, tg_stream(stream)>>>(*o, perm, starts, count, boff, out); tg_count_launch(1);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
@@ -662,13 +662,13 @@ TG_API int tg_group_max_batch(const tg_oracle_t *o, const int32_t *perm, const i
     TG_CUDA_CHECK(cudaMemsetAsync(out, 0, (size_t)out_len * 8, st));
     if (nsub == 0) return TG_OK;
     TG_CUDA_CHECK(cudaMemsetAsync(pos, 0xff, (size_t)n * 4, st));
-    pos_fill_kernel<<<(unsigned)min(nsub, (int64_t)65535), 256, 0, st>>>(subs, nsub, perm, pos);
+    pos_fill_kernel<<<(unsigned)min(nsub, (int64_t)65535), 256, 0, st>>>(subs, nsub, perm, pos); tg_count_launch(1);
     if (ntiles > 0) {
         int grid = (int)min((int64_t)tg_num_sms() * 8, ntiles);
         group_max_tile_kernel<<<grid, GM_T, 0, st>>>(*o, perm, gid, pos, subs, tiles, ntiles,
-                                                   reinterpret_cast<unsigned long long *>(out));
+                                                   reinterpret_cast<unsigned long long *>(out)); tg_count_launch(1);
     }
-    group_max_finalize_kernel<<<(unsigned)min(nsub, (int64_t)65535), 256, 0, st>>>(subs, nsub, o->mode, out);
+    group_max_finalize_kernel<<<(unsigned)min(nsub, (int64_t)65535), 256, 0, st>>>(subs, nsub, o->mode, out); tg_count_launch(1);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
@@ -683,7 +683,7 @@ TG_API int tg_nn_chain_batch(double *mats, const int64_t *mat_off, const int64_t
     int64_t blocks = (warps * 32 + threads - 1) / threads;
     if (blocks > (int64_t)tg_num_sms() * 32) blocks = (int64_t)tg_num_sms() * 32;
     nn_chain_kernel<<<(unsigned)blocks, threads, 0, tg_stream(stream)>>>(mats, mat_off, sizes, count, merge_off, lefts,
-                                                                       rights, heights, active, slot, chain, aux_off);
+                                                                       rights, heights, active, slot, chain, aux_off); tg_count_launch(1);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
@@ -694,7 +694,7 @@ TG_API int tg_oracle_block(const tg_oracle_t *o, const int32_t *rows, int64_t nr
     if (!o || nr < 0 || nc < 0 || !out) return TG_ERR_ARG;
     if (nr * nc == 0) return TG_OK;
     oracle_block_kernel<<<(unsigned)((nr * nc + 255) / 256), 256, 0, tg_stream(stream)>>>(*o, rows, nr, cols, nc,
-                                                                                          query_semantics, out);
+                                                                                          query_semantics, out); tg_count_launch(1);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }

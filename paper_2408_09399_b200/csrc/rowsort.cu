@@ -694,7 +694,7 @@ TG_API int tg_row_sort_f64(const double *S, int64_t n, int32_t *order, double *r
     do {                                                                                                   \
         auto kfn = row_sort_smem_kernel<EM>;                                                               \
         TG_CUDA_CHECK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem)); \
-        kfn<<<grid, RS_T, pl.smem, st>>>(S, n, order, rowsum, pl);                                         \
+        kfn<<<grid, RS_T, pl.smem, st>>>(S, n, order, rowsum, pl); tg_count_launch(1);                                         \
     } while (0)
         if (E <= 2) RS_LAUNCH(2);
         else if (E <= 4) RS_LAUNCH(4);
@@ -712,7 +712,7 @@ TG_API int tg_row_sort_f64(const double *S, int64_t n, int32_t *order, double *r
     size_t smem = (size_t)(rs_fine_cap(m) + 1) * sizeof(uint32_t);
     if (smem > 160 * 1024) return TG_ERR_ARG;
     TG_CUDA_CHECK(cudaFuncSetAttribute(row_sort_global_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    row_sort_global_kernel<<<grid, RS_T, smem, st>>>(S, n, order, rowsum, gpk);
+    row_sort_global_kernel<<<grid, RS_T, smem, st>>>(S, n, order, rowsum, gpk); tg_count_launch(1);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
@@ -724,14 +724,14 @@ TG_API int tg_row_sums_f64(const double *S, int64_t n, double *rowsum, void *, s
     if (n > 128 * (PW_MAXNODES / 2)) return TG_ERR_ARG;
     int grid = tg_num_sms() * 4;
     if (grid > n) grid = (int)n;
-    row_sums_kernel<<<grid, 256, 0, tg_stream(stream)>>>(S, n, rowsum);
+    row_sums_kernel<<<grid, 256, 0, tg_stream(stream)>>>(S, n, rowsum); tg_count_launch(1);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
 
 TG_API int tg_initial_clique(const double *rowsum, int64_t n, int32_t *clique, void *stream) {
     if (n < 4 || !rowsum || !clique) return TG_ERR_ARG;
-    clique_kernel<<<1, 1024, 0, tg_stream(stream)>>>(rowsum, n, clique);
+    clique_kernel<<<1, 1024, 0, tg_stream(stream)>>>(rowsum, n, clique); tg_count_launch(1);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }

@@ -248,7 +248,7 @@ TG_API int tg_pearson_f64(const double *X, int64_t n, int64_t L, double *S, void
     double *Xc = ar.take<double>((size_t)n * Lp);
     double *inv = ar.take<double>(n);
     cudaStream_t st = tg_stream(stream);
-    center_rows_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(X, n, L, Lp, Xc, inv);
+    center_rows_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(X, n, L, Lp, Xc, inv); tg_count_launch(1);
     TG_LAUNCH_CHECK();
     const int64_t nb = (n + PBM - 1) / PBM;
     const int64_t tiles = nb * (nb + 1) / 2;
@@ -260,7 +260,7 @@ TG_API int tg_pearson_f64(const double *X, int64_t n, int64_t L, double *S, void
         TG_CUDA_CHECK(cudaFuncSetAttribute(syrk_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    syrk_dmma_kernel<<<(unsigned)tiles, PTHREADS, smem, st>>>(Xc, inv, n, Lp, S);
+    syrk_dmma_kernel<<<(unsigned)tiles, PTHREADS, smem, st>>>(Xc, inv, n, Lp, S); tg_count_launch(1);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
@@ -270,7 +270,7 @@ TG_API int tg_validate_f64(const double *S, int64_t n, int32_t *flags, void *str
     cudaStream_t st = tg_stream(stream);
     TG_CUDA_CHECK(cudaMemsetAsync(flags, 0, sizeof(int32_t), st));
     const int64_t nb = (n + 31) / 32;
-    validate_kernel<<<(unsigned)(nb * (nb + 1) / 2), 256, 0, st>>>(S, n, flags);
+    validate_kernel<<<(unsigned)(nb * (nb + 1) / 2), 256, 0, st>>>(S, n, flags); tg_count_launch(1);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }

@@ -687,7 +687,7 @@ __global__ void edge_weights_kernel(const double *__restrict__ S, int64_t n, con
 TG_API int tg_edge_weights(const double *S, int64_t n, const int32_t *edges, int64_t m, double *w, void *stream) {
     if (!S || !edges || !w || m < 0) return TG_ERR_ARG;
     if (m == 0) return TG_OK;
-    edge_weights_kernel<<<(unsigned)((m + 255) / 256), 256, 0, tg_stream(stream)>>>(S, n, edges, m, w);
+    edge_weights_kernel<<<(unsigned)((m + 255) / 256), 256, 0, tg_stream(stream)>>>(S, n, edges, m, w); tg_count_launch(1);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
@@ -728,10 +728,10 @@ TG_API int tg_tmfg_heap(const double *S, const int32_t *order, int64_t n, const 
     size_t smem = tm_smem_bytes(n, smem_cur);
     if (smem_cur) {
         TG_CUDA_CHECK(cudaFuncSetAttribute(tmfg_heap_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        tmfg_heap_kernel<true><<<1, TM_T, smem, st>>>(A);
+        tmfg_heap_kernel<true><<<1, TM_T, smem, st>>>(A); tg_count_launch(1);
     } else {
         TG_CUDA_CHECK(cudaFuncSetAttribute(tmfg_heap_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        tmfg_heap_kernel<false><<<1, TM_T, smem, st>>>(A);
+        tmfg_heap_kernel<false><<<1, TM_T, smem, st>>>(A); tg_count_launch(1);
     }
     TG_LAUNCH_CHECK();
     return TG_OK;
