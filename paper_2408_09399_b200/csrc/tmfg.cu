@@ -34,10 +34,12 @@ namespace {
 
 constexpr int TM_T = 1024;
 constexpr int TM_WARPS = TM_T / 32;
+constexpr int TM_EPW = 1;                       // entries refreshed per warp
 constexpr int TM_NEW_WARPS = 4;                 // warps that build new-face entries
-constexpr int TM_K = 2 * (TM_WARPS - TM_NEW_WARPS);  // top-K speculated per round (56)
+constexpr int TM_K = TM_EPW * (TM_WARPS - TM_NEW_WARPS);  // top-K speculated per round (28)
 constexpr int TM_B = 1024;                      // shared-memory queue capacity
 constexpr int TM_BATCH = TM_K + 8;
+static_assert(TM_K <= 32, "replay_warp maps one queue position per lane");
 
 struct Ent {
     double g;
@@ -49,7 +51,7 @@ struct Ent {
 
 __device__ __forceinline__ bool ent_gt(const Ent &x, const Ent &y) {
     // x pops before y: heapq order of (-g, fid)
-    return x.g > y.g || (x.g == y.g && x.fid < y.fid);
+    return (x.g > y.g) | ((x.g == y.g) & (x.fid < y.fid));
 }
 
 struct Ctl {
@@ -81,6 +83,12 @@ struct Ctl {
     int hist[256];
     int done;
     int bad;
+    long long t_par, t_replay, t_merge, t_insert, t_refill, rounds, refills;
+    int it_round_max;
+    int ph[4];
+    long long phs[4];
+    long long pops_dbg;
+    long long it_total, it_maxsum;
 };
 
 struct TmArgs {
@@ -113,85 +121,132 @@ __device__ __forceinline__ void cur_set(uint16_t *sc, int32_t *gc, int w, int c)
     else gc[w] = c;
 }
 
-// One warp builds up to two entries: refresh the 3 vertices of each face
-// (first uninserted id of order[w]) and pick the best candidate.
+// One warp builds up to TM_EPW entries: refresh the 3 vertices of each face
+// (first uninserted id of order[w], tmfg.py:169-182) and pick the best of the
+// three candidates (tmfg.py:266-277).  Cursor probes: 4 x 32 ids per vertex in
+// one batch of independent loads; rare long tails continue 16 x 32 at a time.
+
 template <bool SMEM_CURSORS>
 __device__ void warp_entries(const TmArgs &A, const uint32_t *bits, uint16_t *sc, int cnt, const int (*fverts)[3],
-                             const int *fids, Ent *out) {
+                             const int *fids, Ent *out, int *iters) {
     const int lane = threadIdx.x & 31;
     const int n = A.n, m = n - 1;
-    int vv[6], cur[6], found[6];
+    constexpr int NV = 3 * TM_EPW;
+    int vv[NV], cur[NV], found[NV];
     const int nv = 3 * cnt;
 #pragma unroll
-    for (int k = 0; k < 6; k++) {
+    for (int k = 0; k < NV; k++) {
         vv[k] = k < nv ? fverts[k / 3][k % 3] : 0;
         cur[k] = k < nv ? cur_get<SMEM_CURSORS>(sc, A.gcursor, vv[k]) : 0;
         found[k] = -1;
     }
     unsigned pending = (1u << nv) - 1u;
-    while (pending) {
-        int val[6];
+    {
+        int val[NV][4];
 #pragma unroll
-        for (int k = 0; k < 6; k++) {
-            val[k] = -1;
-            if ((pending >> k) & 1u) {
-                int idx = cur[k] + lane;
-                if (idx < m) val[k] = __ldg(A.order + (int64_t)vv[k] * m + idx);
+        for (int k = 0; k < NV; k++)
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                int idx = cur[k] + q * 32 + lane;
+                val[k][q] = (k < nv && idx < m) ? __ldg(A.order + (int64_t)vv[k] * m + idx) : -1;
             }
-        }
 #pragma unroll
-        for (int k = 0; k < 6; k++) {
-            if ((pending >> k) & 1u) {
-                bool ok = val[k] >= 0 && !is_ins(bits, val[k]);
-                unsigned b = __ballot_sync(0xffffffffu, ok);
-                if (b) {
-                    int f = __ffs(b) - 1;
-                    found[k] = __shfl_sync(0xffffffffu, val[k], f);
-                    cur[k] += f;
+        for (int k = 0; k < NV; k++) {
+            if (k < nv) {
+                int firstq = 4, hitv = -1;
+#pragma unroll
+                for (int q = 3; q >= 0; q--) {
+                    bool ok = val[k][q] >= 0 && !is_ins(bits, val[k][q]);
+                    if (ok) { firstq = q; hitv = val[k][q]; }
+                }
+                const unsigned key = (unsigned)(firstq * 32 + lane);
+                const unsigned best = __reduce_min_sync(0xffffffffu, key);
+                if (best < 128u) {
+                    found[k] = __shfl_sync(0xffffffffu, hitv, best & 31);
+                    cur[k] += (int)best;
                     pending &= ~(1u << k);
                 } else {
-                    cur[k] += 32;
-                    if (cur[k] >= m) pending &= ~(1u << k);  // cannot happen while rem > 0
+                    cur[k] += 128;
                 }
             }
         }
     }
+    while (pending) {
+        (*iters)++;
+        const int k = __ffs(pending) - 1;
+        int w = 0, c = 0;
+#pragma unroll
+        for (int q = 0; q < NV; q++)
+            if (q == k) { w = vv[q]; c = cur[q]; }
+        int val[16];
+#pragma unroll
+        for (int q = 0; q < 16; q++) {
+            int idx = c + q * 32 + lane;
+            val[q] = idx < m ? __ldg(A.order + (int64_t)w * m + idx) : -1;
+        }
+        int firstq = 16, hitv = -1;
+#pragma unroll
+        for (int q = 15; q >= 0; q--) {
+            bool ok = val[q] >= 0 && !is_ins(bits, val[q]);
+            if (ok) { firstq = q; hitv = val[q]; }
+        }
+        const unsigned best = __reduce_min_sync(0xffffffffu, (unsigned)(firstq * 32 + lane));
+        const int hit = best < 512u ? __shfl_sync(0xffffffffu, hitv, best & 31) : -1;
+        const int adv = best < 512u ? (int)best : 512;
+#pragma unroll
+        for (int q = 0; q < NV; q++)
+            if (q == k) {
+                cur[q] = c + adv;
+                if (hit >= 0) found[q] = hit;
+            }
+        if (hit >= 0 || c + adv >= m) pending &= ~(1u << k);
+    }
     if (lane == 0) {
 #pragma unroll
-        for (int k = 0; k < 6; k++)
+        for (int k = 0; k < NV; k++)
             if (k < nv) cur_set<SMEM_CURSORS>(sc, A.gcursor, vv[k], cur[k]);
     }
-    // 9 similarity loads per entry: lane = e*9 + ci*3 + vi
+    // 9 similarity loads per entry: lane = e*9 + ci*3 + vi loads S[face_vi, cand_ci]
     double sv = 0.0;
-    if (lane < 9 * cnt) {
-        int e = lane / 9, r = lane % 9, ci = r / 3, vi = r % 3;
-        int u = found[e * 3 + ci];
-        int w = vv[e * 3 + vi];
-        sv = (u >= 0) ? __ldg(A.S + (int64_t)w * n + u) : 0.0;
-    }
-    double s[18];
+    int my_u = -1;
+    {
+        const int e = lane / 9, r = lane % 9, ci = r / 3, vi = r % 3;
+        int u = -1, w = 0;
 #pragma unroll
-    for (int q = 0; q < 18; q++) s[q] = __shfl_sync(0xffffffffu, sv, q);
-    if (lane == 0) {
-        for (int e = 0; e < cnt; e++) {
-            double best_g = -INFINITY;
-            int best_v = -1;
-            for (int ci = 0; ci < 3; ci++) {
-                int u = found[e * 3 + ci];
-                double g = __dadd_rn(__dadd_rn(s[e * 9 + ci * 3 + 0], s[e * 9 + ci * 3 + 1]), s[e * 9 + ci * 3 + 2]);
-                if (g > best_g || (g == best_g && u < best_v)) { best_g = g; best_v = u; }
-            }
-            Ent x;
-            x.g = best_g;
-            x.fid = fids[e];
-            x.cand = best_v;
-            x.a = fverts[e][0];
-            x.b = fverts[e][1];
-            x.c = fverts[e][2];
-            x.opt = 0;
-            out[e] = x;
+        for (int k = 0; k < NV; k++) {
+            if (k == e * 3 + ci) u = found[k];
+            if (k == e * 3 + vi) w = vv[k];
         }
+        if (e < cnt && u >= 0) sv = __ldg(A.S + (int64_t)w * n + u);
+        my_u = u;
     }
+    // lanes with vi == 0 form g = (S[a,u] + S[b,u]) + S[c,u]  (tmfg.py:273, left to right)
+    const double s1 = __shfl_down_sync(0xffffffffu, sv, 1);
+    const double s2 = __shfl_down_sync(0xffffffffu, sv, 2);
+    const double g = __dadd_rn(__dadd_rn(sv, s1), s2);
+    // entry leader (lane e*9) picks the best of its 3 candidates: g desc, u asc
+    const double g1 = __shfl_down_sync(0xffffffffu, g, 3), g2 = __shfl_down_sync(0xffffffffu, g, 6);
+    const int u1 = __shfl_down_sync(0xffffffffu, my_u, 3), u2 = __shfl_down_sync(0xffffffffu, my_u, 6);
+    if (lane % 9 == 0 && lane / 9 < cnt) {
+        const int e = lane / 9;
+        double best_g = -INFINITY;
+        int best_v = -1;
+        const double gs[3] = {g, g1, g2};
+        const int us[3] = {my_u, u1, u2};
+#pragma unroll
+        for (int ci = 0; ci < 3; ci++)
+            if (gs[ci] > best_g || (gs[ci] == best_g && us[ci] < best_v)) { best_g = gs[ci]; best_v = us[ci]; }
+        Ent x;
+        x.g = best_g;
+        x.fid = fids[e];
+        x.cand = best_v;
+        x.a = fverts[e][0];
+        x.b = fverts[e][1];
+        x.c = fverts[e][2];
+        x.opt = 0;
+        out[e] = x;
+    }
+    __syncwarp();
     if (A.check) {
         // tmfg.py:377-380 true_best_gain: brute force over every uninserted vertex
         for (int e = 0; e < cnt; e++) {
@@ -201,11 +256,10 @@ __device__ void warp_entries(const TmArgs &A, const uint32_t *bits, uint16_t *sc
             double best = -INFINITY;
             for (int u = lane; u < n; u += 32) {
                 if (is_ins(bits, u)) continue;
-                double g = __dadd_rn(__dadd_rn(Sa[u], Sb[u]), Sc[u]);
-                best = fmax(best, g);
+                double gg = __dadd_rn(__dadd_rn(Sa[u], Sb[u]), Sc[u]);
+                best = fmax(best, gg);
             }
             for (int o = 16; o; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
-            __syncwarp();
             if (lane == 0) out[e].opt = out[e].g >= __dsub_rn(best, 1e-12);
             __syncwarp();
         }
@@ -334,6 +388,162 @@ __device__ void refill(const TmArgs &A, Ctl &ctl, Ent *cur, Ent *scratch, Ent *r
     __syncthreads();
 }
 
+
+// Branch-free key compare: (g1, f1) pops before (g2, f2) -- heapq order of (-g, fid).
+__device__ __forceinline__ bool kgt(double g1, int f1, double g2, int f2) {
+    return (g1 > g2) | ((g1 == g2) & (f1 < f2));
+}
+
+// Replays the lazy heap's pops for one round (one lane per queue position,
+// TM_K <= 32).  Entries L[0..Lc) are the queue head in pop order; Lstale/Lref
+// say which are stale and their refreshed entry under the current inserted
+// set; NE are the fresh entries of the faces made by the last insertion (not
+// queued yet).  Sequentially: pop the max of (L[i], best refreshed so far, best
+// new); a stale L[i] pushes Lref[i]; the first fresh thing popped wins.  Only
+// that first fresh pop can be a refreshed or a new entry, so the round ends at
+// the first i where L[i] is fresh or is beaten by the running max of the
+// refreshed entries or by the best new entry: a prefix max + a ballot.
+__device__ void replay_warp(const TmArgs &A, Ctl &ctl, const Ent *L, const Ent *Lref, const int *Lstale,
+                            const Ent *NE, Ent *batch, Ent *tobuf, double *kg, int *kf, int *ksrc) {
+    const int lane = threadIdx.x & 31;
+    const int Lc = ctl.L_count, nec = ctl.ne_count;
+    // best new entry (<= 4, every lane)
+    double ng = 0.0;
+    int nf = 0, ni = -1;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        if (k < nec) {
+            const double g = NE[k].g;
+            const int f = NE[k].fid;
+            if ((ni < 0) | kgt(g, f, ng, nf)) { ng = g; nf = f; ni = k; }
+        }
+    }
+    const bool have_ne = ni >= 0;
+    // this lane's queue position
+    const bool v = lane < Lc;
+    const bool st = v && Lstale[lane];
+    const double hg = v ? L[lane].g : 0.0;
+    const int hf = v ? L[lane].fid : 0;
+    const double rg = st ? Lref[lane].g : 0.0;
+    const int rf = st ? Lref[lane].fid : 0;
+    // inclusive prefix max of refreshed entries, carrying their position
+    double ig = rg;
+    int ifd = rf, iix = lane;
+    bool iok = st;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double g2 = __shfl_up_sync(0xffffffffu, ig, o);
+        const int f2 = __shfl_up_sync(0xffffffffu, ifd, o);
+        const int x2 = __shfl_up_sync(0xffffffffu, iix, o);
+        const bool k2 = __shfl_up_sync(0xffffffffu, (int)iok, o) != 0;
+        const bool take = (lane >= o) & k2 & ((!iok) | kgt(g2, f2, ig, ifd));
+        ig = take ? g2 : ig;
+        ifd = take ? f2 : ifd;
+        iix = take ? x2 : iix;
+        iok = iok | take;
+    }
+    const double eg = __shfl_up_sync(0xffffffffu, ig, 1);
+    const int ef = __shfl_up_sync(0xffffffffu, ifd, 1);
+    const int eix = __shfl_up_sync(0xffffffffu, iix, 1);
+    const bool eok = (lane > 0) & (__shfl_up_sync(0xffffffffu, (int)iok, 1) != 0);
+    const bool c = v & ((!st) | (eok & kgt(eg, ef, hg, hf)) | (have_ne & kgt(ng, nf, hg, hf)));
+    const unsigned bc = __ballot_sync(0xffffffffu, c);
+    const int istar = bc ? __ffs(bc) - 1 : Lc;
+    // tmfg.py:425-431 counters over the stale pops j < istar (+ the check_invariants assertion)
+    const bool rose = st & (lane < istar) & (rg > __dadd_rn(hg, 1e-12));
+    const int ginc = __popc(__ballot_sync(0xffffffffu, rose));
+    if (A.check) {
+        const unsigned bb = __ballot_sync(0xffffffffu, rose && Lref[lane].opt);
+        if (bb) {
+            if (lane == __ffs(bb) - 1) {
+                ctl.bad = 2;
+                A.stats[4] = rf;
+                A.stats[5] = __double_as_longlong(hg);
+                A.stats[6] = __double_as_longlong(rg);
+                ctl.winner = 0;
+                ctl.exhausted = 0;
+                ctl.removed = 0;
+                ctl.nbuf_new = 0;
+            }
+            __syncwarp();
+            return;
+        }
+    }
+    // the winner: evaluated by the lane at istar (or from the full prefix max)
+    const bool more = (ctl.size > Lc) || (ctl.pool_count > 0);
+    int kind = 0, widx = -1;   // 1 = queue entry, 2 = refreshed entry, 3 = new entry
+    {
+        int k_l = 1, w_l = lane;
+        double tg = hg;
+        int tf = hf;
+        if (have_ne & kgt(ng, nf, tg, tf)) { tg = ng; tf = nf; k_l = 3; w_l = ni; }
+        if (eok & kgt(eg, ef, tg, tf)) { k_l = 2; w_l = eix; }
+        if (istar < Lc) {
+            kind = __shfl_sync(0xffffffffu, k_l, istar);
+            widx = __shfl_sync(0xffffffffu, w_l, istar);
+        } else if (!more) {
+            const double ag = __shfl_sync(0xffffffffu, ig, 31);
+            const int af = __shfl_sync(0xffffffffu, ifd, 31);
+            const int ax = __shfl_sync(0xffffffffu, iix, 31);
+            const bool aok = __shfl_sync(0xffffffffu, (int)iok, 31) != 0;
+            if (have_ne && ((!aok) | kgt(ng, nf, ag, af))) { kind = 3; widx = ni; }
+            else if (aok) { kind = 2; widx = ax; }
+        }
+    }
+    const int npop = istar < Lc ? istar : Lc;   // stale pops
+    if (lane == 0) {
+        ctl.pops += npop + (kind ? 1 : 0);
+        ctl.refreshes += npop;
+        ctl.gain_inc += ginc;
+        ctl.removed = npop + (kind == 1 ? 1 : 0);
+        ctl.winner = kind != 0;
+        ctl.exhausted = kind == 0;
+        if (kind == 0 && !more) ctl.bad = 1;
+        if (kind == 1) ctl.win = L[widx];
+        else if (kind == 2) ctl.win = Lref[widx];
+        else if (kind == 3) ctl.win = NE[widx];
+    }
+    // re-queue: refreshed entries of the stale pops (minus a refreshed winner) and
+    // new entries (minus a new winner); above the pool max -> shared buffer, else pool
+    const bool pm = ctl.pool_has_max;
+    const double pg = ctl.pool_max.g;
+    const int pf = ctl.pool_max.fid;
+    const bool br = st & (lane < npop) & !((kind == 2) & (widx == lane));
+    const bool bn = (lane < nec) & !((kind == 3) & (widx == lane));
+    const double nlg = bn ? NE[lane].g : 0.0;
+    const int nlf = bn ? NE[lane].fid : 0;
+    const bool fr = br & ((!pm) | kgt(rg, rf, pg, pf));
+    const bool fnn = bn & ((!pm) | kgt(nlg, nlf, pg, pf));
+    const bool pr = br & !fr, pn = bn & !fnn;
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned bfr = __ballot_sync(0xffffffffu, fr), bfn = __ballot_sync(0xffffffffu, fnn);
+    const unsigned bpr = __ballot_sync(0xffffffffu, pr), bpn = __ballot_sync(0xffffffffu, pn);
+    const int nfr = __popc(bfr);
+    const int nbuf = nfr + __popc(bfn);
+    // keys of the buffer-bound entries (src >= 0: Lref index, src < 0: ~NE index)
+    if (fr) { const int o = __popc(bfr & lt); kg[o] = rg; kf[o] = rf; ksrc[o] = lane; }
+    if (fnn) { const int o = nfr + __popc(bfn & lt); kg[o] = nlg; kf[o] = nlf; ksrc[o] = ~lane; }
+    Ent *pool = ctl.psel ? A.pool2 : A.pool;
+    const int pc = ctl.pool_count;
+    const int npr = __popc(bpr);
+    if (pr) pool[pc + __popc(bpr & lt)] = Lref[lane];
+    if (pn) pool[pc + npr + __popc(bpn & lt)] = NE[lane];
+    __syncwarp();
+    if (lane == 0) {
+        ctl.pool_count = pc + npr + __popc(bpn);
+        ctl.nbuf_new = nbuf;
+    }
+    for (int k = lane; k < nbuf; k += 32) {
+        const double g = kg[k];
+        const int f = kf[k];
+        int r = 0;
+        for (int j = 0; j < nbuf; j++) r += kgt(kg[j], kf[j], g, f);
+        const int sidx = ksrc[k];
+        tobuf[r] = sidx >= 0 ? Lref[sidx] : NE[~sidx];
+    }
+    __syncwarp();
+}
+
 template <bool SMEM_CURSORS>
 __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
     extern __shared__ __align__(16) unsigned char tm_smem[];
@@ -342,11 +552,14 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
     __shared__ Ctl ctl;
     __shared__ Ent L[TM_K];
     __shared__ Ent Lref[TM_K];
+    __shared__ Ent Lout[TM_WARPS - TM_NEW_WARPS][TM_EPW];
     __shared__ int Lstale[TM_K];
     __shared__ Ent NE[4];
     __shared__ Ent batch[TM_BATCH];
     __shared__ Ent tobuf[TM_BATCH];
     __shared__ Ent red_e[TM_WARPS];
+    __shared__ double rk_g[TM_BATCH];
+    __shared__ int rk_f[TM_BATCH], rk_src[TM_BATCH];
     __shared__ int red_ok[TM_WARPS];
 
     Ent *buf0 = reinterpret_cast<Ent *>(tm_smem);
@@ -390,27 +603,37 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
         ctl.psel = 0;
         ctl.done = (n <= 4);
         ctl.bad = 0;
+        ctl.t_par = ctl.t_replay = ctl.t_merge = ctl.t_insert = ctl.t_refill = ctl.rounds = ctl.refills = 0;
+        ctl.it_round_max = 0;
+        for (int q = 0; q < 4; q++) { ctl.ph[q] = 0; ctl.phs[q] = 0; }
+        ctl.pops_dbg = 0;
+        ctl.it_total = ctl.it_maxsum = 0;
     }
     __syncthreads();
 
+    long long tc0 = clock64(), tc1;
     while (!ctl.done) {
+        if (tid == 0) { tc0 = clock64(); ctl.rounds++; }
         // ================= parallel phase: new-face entries + speculative refresh of the top-K
+        int my_iters[4] = {0, 0, 0, 0};
+        long long tpw0 = clock64();
         {
             Ent *cur = ctl.sel ? buf1 : buf0;
             if (warp < TM_NEW_WARPS) {
                 if (warp < ctl.ne_count) {
                     int fids[1] = {ctl.ne_fid[warp]};
                     int fvv[1][3] = {{ctl.ne_v[warp][0], ctl.ne_v[warp][1], ctl.ne_v[warp][2]}};
-                    warp_entries<SMEM_CURSORS>(A, bits, sc, 1, fvv, fids, &NE[warp]);
+                    warp_entries<SMEM_CURSORS>(A, bits, sc, 1, fvv, fids, &NE[warp], my_iters);
                 }
             } else {
-                int base = 2 * (warp - TM_NEW_WARPS);
+                int base = TM_EPW * (warp - TM_NEW_WARPS);
                 int cntL = ctl.L_count;
-                int idx[2];
+                int idx[TM_EPW];
                 int cnt = 0;
-                int fids[2];
-                int fvv[2][3];
-                for (int q = 0; q < 2; q++) {
+                int fids[TM_EPW];
+                int fvv[TM_EPW][3];
+#pragma unroll
+                for (int q = 0; q < TM_EPW; q++) {
                     int i = base + q;
                     if (i < cntL) {
                         Ent h = cur[i];
@@ -427,106 +650,37 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
                     }
                 }
                 if (cnt) {
-                    Ent outs[2];
-                    warp_entries<SMEM_CURSORS>(A, bits, sc, cnt, fvv, fids, outs);
+                    warp_entries<SMEM_CURSORS>(A, bits, sc, cnt, fvv, fids, Lout[warp - TM_NEW_WARPS], my_iters);
                     if (lane == 0)
-                        for (int q = 0; q < cnt; q++) Lref[idx[q]] = outs[q];
+                        for (int q = 0; q < cnt; q++) Lref[idx[q]] = Lout[warp - TM_NEW_WARPS][q];
                 }
             }
         }
-        __syncthreads();
-        // ================= replay the pops (one thread)
+        if (lane == 0 && my_iters[0]) atomicMax(&ctl.it_round_max, my_iters[0]);
+        {
+            int zz = __syncthreads_or(tpw0 == 0);
+            if (tid == 0) ctl.phs[0] += clock64() + zz - tc0;   // loop top -> all warps done
+        }
+        // ================= replay the pops (warp 0, exact sequential semantics)
         if (tid == 0) {
-            int nec = ctl.ne_count;
-            // new entries sorted in pop order
-            for (int i = 1; i < nec; i++) {
-                Ent x = NE[i];
-                int j = i - 1;
-                while (j >= 0 && ent_gt(x, NE[j])) { NE[j + 1] = NE[j]; j--; }
-                NE[j + 1] = x;
-            }
-            int ne_ptr = 0;
-            bool ev = false;
-            Ent eb;
-            int eb_idx = -1;
-            int removed = 0;
-            int kind = 0;  // 1 = L entry, 2 = refreshed entry, 3 = new entry
-            int widx = -1;
-            long long pops = 0, refr = 0, ginc = 0;
-            const int Lc = ctl.L_count;
-            for (int i = 0; i < Lc; i++) {
-                Ent h = L[i];
-                int k = 1;
-                Ent top = h;
-                if (ne_ptr < nec && ent_gt(NE[ne_ptr], top)) { top = NE[ne_ptr]; k = 3; }
-                if (ev && ent_gt(eb, top)) { top = eb; k = 2; }
-                pops++;
-                if (k == 3) { kind = 3; widx = ne_ptr; break; }
-                if (k == 2) { kind = 2; widx = eb_idx; break; }
-                removed++;
-                if (!Lstale[i]) { kind = 1; widx = i; break; }
-                refr++;
-                Ent r = Lref[i];
-                if (r.g > __dadd_rn(h.g, 1e-12)) {
-                    ginc++;
-                    if (A.check && r.opt && !ctl.bad) {
-                        // tmfg.py:429 assertion: a refreshed optimal pair gained
-                        ctl.bad = 2;
-                        A.stats[4] = r.fid;
-                        A.stats[5] = __double_as_longlong(h.g);
-                        A.stats[6] = __double_as_longlong(r.g);
-                        ctl.pops += pops;
-                        ctl.refreshes += refr;
-                        ctl.gain_inc += ginc;
-                        pops = refr = ginc = 0;
-                        kind = -1;
-                        break;
-                    }
-                }
-                if (!ev || ent_gt(r, eb)) { eb = r; eb_idx = i; ev = true; }
-            }
-            bool more = (ctl.size > Lc) || (ctl.pool_count > 0);
-            if (kind == -1) kind = 0;
-            else if (kind == 0 && !more) {
-                // queue exhausted: the best of the refreshed and new entries pops
-                bool have_ne = ne_ptr < nec;
-                if (have_ne && (!ev || ent_gt(NE[ne_ptr], eb))) { kind = 3; widx = ne_ptr; }
-                else if (ev) { kind = 2; widx = eb_idx; }
-                if (kind) pops++;
-                else ctl.bad = 1;
-            }
-            ctl.pops += pops;
-            ctl.refreshes += refr;
-            ctl.gain_inc += ginc;
-            ctl.removed = removed;
-            ctl.exhausted = (kind == 0);
-            ctl.winner = (kind != 0);
-            if (kind == 1) ctl.win = L[widx];
-            else if (kind == 2) ctl.win = Lref[widx];
-            else if (kind == 3) ctl.win = NE[widx];
-            // batch of entries to (re)queue
-            int nb = 0;
-            for (int i = 0; i < removed; i++)
-                if (Lstale[i] && !(kind == 2 && i == widx)) batch[nb++] = Lref[i];
-            for (int i = 0; i < nec; i++)
-                if (!(kind == 3 && i == widx)) batch[nb++] = NE[i];
-            // split: above the pool max -> shared buffer, else -> pool
-            int nbuf = 0;
-            for (int i = 0; i < nb; i++) {
-                if (!ctl.pool_has_max || ent_gt(batch[i], ctl.pool_max)) {
-                    Ent x = batch[i];
-                    int j = nbuf - 1;
-                    while (j >= 0 && ent_gt(x, tobuf[j])) { tobuf[j + 1] = tobuf[j]; j--; }
-                    tobuf[j + 1] = x;
-                    nbuf++;
-                } else {
-                    (ctl.psel ? A.pool2 : A.pool)[ctl.pool_count++] = batch[i];
-                }
-            }
-            ctl.nbuf_new = nbuf;
-            ctl.nbatch = nb;
+            tc1 = clock64();
+            ctl.t_par += tc1 - tc0;
+            tc0 = tc1;
         }
-        __syncthreads();
+        if (warp == 0) replay_warp(A, ctl, L, Lref, Lstale, NE, batch, tobuf, rk_g, rk_f, rk_src);
+        {
+            int zz = __syncthreads_or(0);
+            if (tid == 0) ctl.phs[1] += clock64() + zz - tc0;   // loop top -> replay done
+        }
+        if (tid == 0) {
+            tc1 = clock64();
+            ctl.t_replay += tc1 - tc0;
+            tc0 = tc1;
+            ctl.it_maxsum += ctl.it_round_max;
+            ctl.it_total += ctl.it_round_max ? 1 : 0;
+            ctl.it_round_max = 0;
+            for (int q = 0; q < 4; q++) ctl.ph[q] = 0;
+        }
         // ================= merge: buffer[removed..size) + tobuf -> other half
         {
             Ent *cur = ctl.sel ? buf1 : buf0;
@@ -580,6 +734,9 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
         __syncthreads();
         // ================= insert the winner
         if (tid == 0) {
+            tc1 = clock64();
+            ctl.t_merge += tc1 - tc0;
+            tc0 = tc1;
             ctl.ne_count = 0;
             if (ctl.winner) {
                 Ent w = ctl.win;
@@ -620,10 +777,12 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
             if (ctl.bad) ctl.done = 1;
         }
         __syncthreads();
+        if (tid == 0) { tc1 = clock64(); ctl.t_insert += tc1 - tc0; tc0 = tc1; }
         if (ctl.done) break;
         // ================= refill the shared buffer from the pool when short
         if (ctl.size < TM_K && ctl.pool_count > 0) {
             refill<TM_T>(A, ctl, ctl.sel ? buf1 : buf0, ctl.sel ? buf0 : buf1, red_e, red_ok);
+            if (tid == 0) { tc1 = clock64(); ctl.t_refill += tc1 - tc0; ctl.refills++; tc0 = tc1; }
         }
         if (tid == 0) ctl.L_count = min(TM_K, ctl.size);
         __syncthreads();
@@ -666,6 +825,15 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
         A.stats[1] = ctl.refreshes;
         A.stats[2] = ctl.gain_inc;
         A.stats[3] = ctl.bad;
+        A.stats[8] = ctl.rounds;
+        A.stats[9] = ctl.refills;
+        A.stats[12] = ctl.t_merge;
+        A.stats[13] = ctl.t_insert;
+        A.stats[14] = ctl.t_refill;
+        A.stats[15] = ctl.pool_count;
+        A.stats[10] = ctl.phs[0];
+        A.stats[11] = ctl.phs[1];
+        A.stats[7] = ctl.it_total * 100000 + ctl.it_maxsum;
     }
 }
 
