@@ -202,13 +202,14 @@ typedef struct {
     int32_t len;
     int32_t m;
     int64_t out_off;
+    int64_t tile_off;   /* index of the sub-problem's first tile (row-major nt x nt, nt = ceil(len/64)) */
 } tg_gm_sub_t;
 typedef struct {
     int32_t sub;
     int32_t i0;
     int32_t j0;
 } tg_gm_tile_t;
-size_t tg_group_max_workspace_bytes(int64_t n);
+size_t tg_group_max_workspace_bytes(int64_t n, int64_t ntiles);
 int tg_group_max_batch(const tg_oracle_t *oracle, const int32_t *perm, const int32_t *gid, const void *subs,
                        int64_t nsub, const void *tiles, int64_t ntiles, double *out, int64_t out_len, void *ws,
                        size_t ws_bytes, void *stream);

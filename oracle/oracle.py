@@ -429,6 +429,8 @@ def nn_chain_raw(D: np.ndarray) -> list:
     rights = np.empty(m, dtype=np.int64)
     heights = np.empty(m)
     k = lib().orc_nn_chain(_p(D), _i(m), _p(lefts), _p(rights), _p(heights))
+    if k < 0:
+        raise RuntimeError("NN-chain does not terminate on this (non-reducible) matrix")
     return [(int(lefts[t]), int(rights[t]), float(heights[t])) for t in range(k)]
 
 

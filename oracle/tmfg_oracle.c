@@ -612,6 +612,7 @@ EXPORT int64_t orc_nn_chain(const double *D, int64_t m, int64_t *lefts, int64_t 
             slot[lo] = next_id++;
             remaining--;
         } else {
+            if (nchain >= m) { nm = -1; break; }  /* chain cycles: the reference would not terminate */
             chain[nchain++] = y;
         }
     }

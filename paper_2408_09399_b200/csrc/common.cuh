@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stddef.h>
+#include <limits.h>
 
 #include "../../include/tmfg_b200.h"
 

@@ -284,6 +284,7 @@ __global__ void group_blocks_kernel(tg_oracle_t o, const int32_t *perm, const in
 }
 
 // ------------------------------------------------------------ group max (layers 2 and 3)
+constexpr int NN_WARP_MAX = 48;  // larger matrices take the CTA-per-matrix NN-chain
 constexpr int GM_T = 256;
 constexpr int GM_TILE = 64;
 constexpr int GM_HC = 32;   // hubs staged per chunk
@@ -298,13 +299,14 @@ struct GmSub {
     int32_t len;        // vertices
     int32_t m;          // groups
     int64_t out_off;    // into out (m x m)
+    int64_t tile_off;   // first tile of this sub-problem (row-major, nt x nt tiles)
 };
 
 // out is pre-filled with 0 bits (all distances >= 0); atomicMax on raw bits.
 __global__ void __launch_bounds__(GM_T)
 group_max_tile_kernel(tg_oracle_t o, const int32_t *__restrict__ perm, const int32_t *__restrict__ gid,
                       const int32_t *__restrict__ pos, const GmSub *__restrict__ subs, const GmTile *__restrict__ tiles,
-                      int64_t ntiles, unsigned long long *__restrict__ out) {
+                      int64_t ntiles, unsigned long long *__restrict__ out, const uint64_t *__restrict__ mask) {
     // the hub panels (A, B) and the pair tile E are never live together
     __shared__ __align__(16) double gm_raw[GM_TILE * (GM_TILE + 1)];
     double (*A)[GM_TILE] = reinterpret_cast<double (*)[GM_TILE]>(gm_raw);
@@ -363,21 +365,13 @@ group_max_tile_kernel(tg_oracle_t o, const int32_t *__restrict__ perm, const int
 #pragma unroll
                 for (int c = 0; c < 4; c++) E[ty + 16 * r][tx + 16 * c] = acc[r][c];
             __syncthreads();
-            // row-vertex near tables, then column-vertex tables (they win: apsp.py:147-157)
-            for (int pass = 0; pass < 2; pass++) {
-                const int64_t *ip = pass == 0 ? o.near_indptr : o.rev_indptr;
-                const int32_t *ids = pass == 0 ? o.near_ids : o.rev_ids;
-                const double *dd = pass == 0 ? o.near_dist : o.rev_dist;
-                for (int i = tid >> 2; i < rows; i += GM_T / 4) {
-                    int u = ru[i];
-                    for (int64_t k = ip[u] + (tid & 3); k < ip[u + 1]; k += 4) {
-                        // positions are global: only vertices of this sub-problem's column range hit
-                        int p = pos[ids[k]] - (int)(sb.perm_off + tl.j0);
-                        if (p >= 0 && p < cols) E[i][p] = dd[k];
-                    }
-                }
-                __syncthreads();
+            // pairs carrying a near-table override were maxed by the override pass
+            const uint64_t *mk = mask + (size_t)t * GM_TILE;
+            for (int e = tid; e < GM_TILE * GM_TILE; e += GM_T) {
+                int i = e / GM_TILE, j = e % GM_TILE;
+                if ((mk[i] >> j) & 1ull) E[i][j] = 0.0;
             }
+            __syncthreads();
         } else {
             for (int e = tid; e < GM_TILE * GM_TILE; e += GM_T) {
                 int i = e / GM_TILE, j = e % GM_TILE;
@@ -406,6 +400,43 @@ group_max_tile_kernel(tg_oracle_t o, const int32_t *__restrict__ perm, const int
     }
 }
 
+// Near-table overrides (apsp.py:147-157): for every pair (u, v) of a sub-problem
+// with u in near(v) [column table, wins] or v in near(u) [row table], est(u, v)
+// is the recorded exact distance.  Pass 0 walks the transposed tables (column
+// overrides), pass 1 the row tables and skips pairs pass 0 already claimed.
+// Each claimed pair sets its bit in the tile mask and maxes its value into M.
+__global__ void group_max_override_kernel(tg_oracle_t o, const int32_t *__restrict__ perm,
+                                          const int32_t *__restrict__ gid, const int32_t *__restrict__ pos,
+                                          const int32_t *__restrict__ vsub, const GmSub *__restrict__ subs,
+                                          int64_t nsub, int64_t total_len, int pass, uint64_t *__restrict__ mask,
+                                          unsigned long long *__restrict__ out) {
+    const int64_t *ip = pass == 0 ? o.rev_indptr : o.near_indptr;
+    const int32_t *ids = pass == 0 ? o.rev_ids : o.near_ids;
+    const double *dd = pass == 0 ? o.rev_dist : o.near_dist;
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t g = wid; g < total_len; g += nwarps) {
+        const int u = perm[g];
+        const int p = vsub[u];
+        const GmSub sb = subs[p];
+        const int i = (int)(g - sb.perm_off);
+        const int nt = (sb.len + GM_TILE - 1) / GM_TILE;
+        const int gi = gid[g];
+        for (int64_t k = ip[u] + lane; k < ip[u + 1]; k += 32) {
+            const int v = ids[k];
+            if (vsub[v] != p) continue;
+            const int j = (int)(pos[v] - sb.perm_off);
+            const int64_t t = sb.tile_off + (int64_t)(i / GM_TILE) * nt + (j / GM_TILE);
+            uint64_t *word = mask + (size_t)t * GM_TILE + (i % GM_TILE);
+            const uint64_t bit = 1ull << (j % GM_TILE);
+            if (pass == 1 && ((*word) & bit)) continue;   // a column override already owns the pair
+            atomicOr((unsigned long long *)word, (unsigned long long)bit);
+            atomicMax(&out[sb.out_off + (int64_t)gi * sb.m + gid[pos[v]]], tg_dbits(dd[k]));
+        }
+    }
+}
+
 __global__ void group_max_finalize_kernel(const GmSub *subs, int64_t nsub, int mode, double *out) {
     for (int64_t p = blockIdx.x; p < nsub; p += gridDim.x) {
         GmSub sb = subs[p];
@@ -427,7 +458,7 @@ __global__ void nn_chain_kernel(double *mats, const int64_t *mat_off, const int6
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t b = wid; b < count; b += nwarps) {
         const int64_t m = sizes[b];
-        if (m < 2) continue;
+        if (m < 2 || m > NN_WARP_MAX) continue;
         double *W = mats + mat_off[b];
         uint8_t *active = active_all + aux_off[b];
         int64_t *slot = slot_all + aux_off[b];
@@ -498,16 +529,23 @@ __global__ void nn_chain_kernel(double *mats, const int64_t *mat_off, const int6
                 remaining--;
                 __syncwarp();
             } else {
+                if (nchain >= m) {  // a non-reducible (asymmetric) matrix made the chain cycle
+                    if (lane == 0) Hh[0] = __longlong_as_double(0x7ff8dead00000000ll);
+                    break;
+                }
                 chain[nchain++] = y;
             }
         }
     }
 }
 
-__global__ void pos_fill_kernel(const GmSub *subs, int64_t nsub, const int32_t *perm, int32_t *pos) {
+__global__ void pos_fill_kernel(const GmSub *subs, int64_t nsub, const int32_t *perm, int32_t *pos, int32_t *vsub) {
     for (int64_t p = blockIdx.x; p < nsub; p += gridDim.x)
-        for (int i = threadIdx.x; i < subs[p].len; i += blockDim.x)
-            pos[perm[subs[p].perm_off + i]] = (int32_t)(subs[p].perm_off + i);  // global position
+        for (int i = threadIdx.x; i < subs[p].len; i += blockDim.x) {
+            const int v = perm[subs[p].perm_off + i];
+            pos[v] = (int32_t)(subs[p].perm_off + i);  // global position
+            vsub[v] = (int32_t)p;
+        }
 }
 
 __global__ void oracle_block_kernel(tg_oracle_t o, const int32_t *rows, int64_t nr, const int32_t *cols, int64_t nc,
@@ -516,6 +554,119 @@ __global__ void oracle_block_kernel(tg_oracle_t o, const int32_t *rows, int64_t 
     if (e >= nr * nc) return;
     int u = rows[e / nc], v = cols[e % nc];
     out[e] = q ? oracle_query(o, u, v) : oracle_block(o, u, v);
+}
+
+// Larger matrices: one CTA per matrix, rows scanned by the whole block.
+__global__ void __launch_bounds__(512)
+nn_chain_cta_kernel(double *mats, const int64_t *mat_off, const int64_t *sizes, int64_t count,
+                    const int64_t *merge_off, int64_t *lefts, int64_t *rights, double *heights,
+                    uint8_t *active_all, int64_t *slot_all, int64_t *chain_all, const int64_t *aux_off) {
+    __shared__ double rv[16];
+    __shared__ long long ri[16];
+    __shared__ long long sh_y, sh_f;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    for (int64_t b = blockIdx.x; b < count; b += gridDim.x) {
+        const int64_t m = sizes[b];
+        if (m <= NN_WARP_MAX) continue;
+        double *W = mats + mat_off[b];
+        uint8_t *active = active_all + aux_off[b];
+        int64_t *slot = slot_all + aux_off[b];
+        int64_t *chain = chain_all + aux_off[b];
+        int64_t *L = lefts + merge_off[b], *R = rights + merge_off[b];
+        double *Hh = heights + merge_off[b];
+        for (int64_t i = tid; i < m; i += blockDim.x) {
+            active[i] = 1;
+            slot[i] = i;
+            W[i * m + i] = INFINITY;
+        }
+        __syncthreads();
+        int64_t nchain = 0, next_id = m, remaining = m, nm = 0;
+        while (remaining > 1) {
+            if (nchain == 0) {
+                long long f = LLONG_MAX;
+                for (int64_t i = tid; i < m; i += blockDim.x)
+                    if (active[i]) { f = i; break; }
+                for (int o = 16; o; o >>= 1) f = min(f, __shfl_xor_sync(0xffffffffu, f, o));
+                if (lane == 0) ri[warp] = f;
+                __syncthreads();
+                if (tid == 0) {
+                    long long g = LLONG_MAX;
+                    for (int w = 0; w < nw; w++) g = min(g, ri[w]);
+                    sh_f = g;
+                }
+                __syncthreads();
+                if (tid == 0) chain[0] = sh_f;
+                nchain = 1;
+                __syncthreads();
+            }
+            const int64_t x = chain[nchain - 1];
+            double bv = INFINITY;
+            long long bi = LLONG_MAX;
+            const double *row = W + x * m;
+            for (int64_t j = tid; j < m; j += blockDim.x) {
+                double r = (active[j] && j != x) ? row[j] : INFINITY;
+                if (r < bv || (r == bv && j < bi)) { bv = r; bi = j; }
+            }
+            for (int o = 16; o; o >>= 1) {
+                double r2 = __shfl_xor_sync(0xffffffffu, bv, o);
+                long long i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (r2 < bv || (r2 == bv && i2 < bi)) { bv = r2; bi = i2; }
+            }
+            if (lane == 0) { rv[warp] = bv; ri[warp] = bi; }
+            __syncthreads();
+            if (tid == 0) {
+                double v = INFINITY;
+                long long i = LLONG_MAX;
+                for (int w = 0; w < nw; w++)
+                    if (rv[w] < v || (rv[w] == v && ri[w] < i)) { v = rv[w]; i = ri[w]; }
+                int64_t y = (i == LLONG_MAX) ? 0 : i;  // all-inf row: np.argmin -> 0
+                if (nchain > 1) {
+                    int64_t p = chain[nchain - 2];
+                    double rp = (active[p] && p != x) ? row[p] : INFINITY;
+                    double ry = (active[y] && y != x) ? row[y] : INFINITY;
+                    if (rp == ry) y = p;
+                }
+                sh_y = y;
+            }
+            __syncthreads();
+            const int64_t y = sh_y;
+            if (nchain > 1 && y == chain[nchain - 2]) {
+                nchain -= 2;
+                const double h = row[y];
+                const int64_t lo = x < y ? x : y, hi = x < y ? y : x;
+                if (tid == 0) {
+                    L[nm] = slot[x];
+                    R[nm] = slot[y];
+                    Hh[nm] = h;
+                }
+                nm++;
+                for (int64_t j = tid; j < m; j += blockDim.x) {
+                    double p = W[lo * m + j], q = W[hi * m + j];
+                    double mg = p > q ? p : (q > p ? q : p);
+                    W[lo * m + j] = mg;
+                    W[j * m + lo] = mg;
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    W[lo * m + lo] = INFINITY;
+                    active[hi] = 0;
+                    slot[lo] = next_id;
+                }
+                next_id++;
+                remaining--;
+                __syncthreads();
+            } else {
+                if (nchain >= m) {  // a non-reducible (asymmetric) matrix made the chain cycle
+                    if (tid == 0) Hh[0] = __longlong_as_double(0x7ff8dead00000000ll);
+                    break;
+                }
+                if (tid == 0) chain[nchain] = y;
+                nchain++;
+                __syncthreads();
+            }
+        }
+        __syncthreads();
+    }
 }
 
 }  // namespace
@@ -647,26 +798,50 @@ TG_API int tg_group_blocks(const tg_oracle_t *o, const int32_t *perm, const int6
     return TG_OK;
 }
 
-TG_API size_t tg_group_max_workspace_bytes(int64_t n) { return tg_align_up((size_t)n * 4, 256) + 256; }
+TG_API size_t tg_group_max_workspace_bytes(int64_t n, int64_t ntiles) {
+    return tg_align_up((size_t)n * 4, 256) * 2 + tg_align_up((size_t)ntiles * GM_TILE * 8, 256) + 512;
+}
 
 TG_API int tg_group_max_batch(const tg_oracle_t *o, const int32_t *perm, const int32_t *gid, const void *subs_v,
                               int64_t nsub, const void *tiles_v, int64_t ntiles, double *out, int64_t out_len,
                               void *ws, size_t ws_bytes, void *stream) {
     if (!o || !perm || !gid || !subs_v || !tiles_v || !out || nsub < 0 || ntiles < 0) return TG_ERR_ARG;
     const int64_t n = o->n;
-    if (ws_bytes < tg_group_max_workspace_bytes(n)) return TG_ERR_WORKSPACE;
+    if (ws_bytes < tg_group_max_workspace_bytes(n, ntiles)) return TG_ERR_WORKSPACE;
     const GmSub *subs = reinterpret_cast<const GmSub *>(subs_v);
     const GmTile *tiles = reinterpret_cast<const GmTile *>(tiles_v);
     cudaStream_t st = tg_stream(stream);
-    int32_t *pos = reinterpret_cast<int32_t *>(ws);
+    TgArena ar(ws, ws_bytes);
+    int32_t *pos = ar.take<int32_t>(n);
+    int32_t *vsub = ar.take<int32_t>(n);
+    uint64_t *mask = ar.take<uint64_t>((size_t)ntiles * GM_TILE + 1);
     TG_CUDA_CHECK(cudaMemsetAsync(out, 0, (size_t)out_len * 8, st));
     if (nsub == 0) return TG_OK;
     TG_CUDA_CHECK(cudaMemsetAsync(pos, 0xff, (size_t)n * 4, st));
-    pos_fill_kernel<<<(unsigned)min(nsub, (int64_t)65535), 256, 0, st>>>(subs, nsub, perm, pos); tg_count_launch(1);
+    TG_CUDA_CHECK(cudaMemsetAsync(vsub, 0xff, (size_t)n * 4, st));
+    pos_fill_kernel<<<(unsigned)min(nsub, (int64_t)65535), 256, 0, st>>>(subs, nsub, perm, pos, vsub); tg_count_launch(1);
+    int64_t total_len = 0;
+    {
+        // the caller lays the sub-problems out back to back: total = last offset + length
+        GmSub last;
+        TG_CUDA_CHECK(cudaMemcpyAsync(&last, subs + nsub - 1, sizeof(GmSub), cudaMemcpyDeviceToHost, st));
+        TG_CUDA_CHECK(cudaStreamSynchronize(st));
+        total_len = last.perm_off + last.len;
+    }
+    if (o->mode == 1 && ntiles > 0) {
+        TG_CUDA_CHECK(cudaMemsetAsync(mask, 0, (size_t)ntiles * GM_TILE * 8, st));
+        const int64_t blocks = min((total_len * 32 + 255) / 256, (int64_t)tg_num_sms() * 16);
+        for (int pass = 0; pass < 2; pass++) {
+            group_max_override_kernel<<<(unsigned)blocks, 256, 0, st>>>(*o, perm, gid, pos, vsub, subs, nsub, total_len,
+                                                                        pass, mask,
+                                                                        reinterpret_cast<unsigned long long *>(out));
+            tg_count_launch(1);
+        }
+    }
     if (ntiles > 0) {
         int grid = (int)min((int64_t)tg_num_sms() * 8, ntiles);
         group_max_tile_kernel<<<grid, GM_T, 0, st>>>(*o, perm, gid, pos, subs, tiles, ntiles,
-                                                   reinterpret_cast<unsigned long long *>(out)); tg_count_launch(1);
+                                                   reinterpret_cast<unsigned long long *>(out), mask); tg_count_launch(1);
     }
     group_max_finalize_kernel<<<(unsigned)min(nsub, (int64_t)65535), 256, 0, st>>>(subs, nsub, o->mode, out); tg_count_launch(1);
     TG_LAUNCH_CHECK();
@@ -682,8 +857,12 @@ TG_API int tg_nn_chain_batch(double *mats, const int64_t *mat_off, const int64_t
     int threads = 128;
     int64_t blocks = (warps * 32 + threads - 1) / threads;
     if (blocks > (int64_t)tg_num_sms() * 32) blocks = (int64_t)tg_num_sms() * 32;
-    nn_chain_kernel<<<(unsigned)blocks, threads, 0, tg_stream(stream)>>>(mats, mat_off, sizes, count, merge_off, lefts,
-                                                                       rights, heights, active, slot, chain, aux_off); tg_count_launch(1);
+    cudaStream_t st = tg_stream(stream);
+    nn_chain_kernel<<<(unsigned)blocks, threads, 0, st>>>(mats, mat_off, sizes, count, merge_off, lefts, rights, heights,
+                                                        active, slot, chain, aux_off); tg_count_launch(1);
+    int64_t cblocks = count < (int64_t)tg_num_sms() * 2 ? count : (int64_t)tg_num_sms() * 2;
+    nn_chain_cta_kernel<<<(unsigned)cblocks, 512, 0, st>>>(mats, mat_off, sizes, count, merge_off, lefts, rights,
+                                                         heights, active, slot, chain, aux_off); tg_count_launch(1);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }

@@ -181,7 +181,7 @@ def assign_vertices(graph, dtree: DirectedBubbleTree, oracle) -> BubbleAssignmen
 
 
 # ------------------------------------------------------------------ hierarchy
-_SUB_DT = np.dtype([("perm_off", "<i8"), ("len", "<i4"), ("m", "<i4"), ("out_off", "<i8")])
+_SUB_DT = np.dtype([("perm_off", "<i8"), ("len", "<i4"), ("m", "<i4"), ("out_off", "<i8"), ("tile_off", "<i8")])
 _TILE_DT = np.dtype([("sub", "<i4"), ("i0", "<i4"), ("j0", "<i4")])
 
 
@@ -195,13 +195,14 @@ def group_max_batch(oracle, subproblems) -> list[np.ndarray]:
     perms, gids, subs, tiles = [], [], [], []
     off = 0
     out_off = 0
+    tile_base = 0
     for p, groups in enumerate(subproblems):
         sizes = np.array([len(g) for g in groups], dtype=np.int64)
         perm = np.concatenate([np.asarray(g, dtype=np.int64) for g in groups]).astype(np.int32)
         gid = np.repeat(np.arange(len(groups), dtype=np.int32), sizes)
         L = perm.shape[0]
         m = len(groups)
-        subs.append((off, L, m, out_off))
+        subs.append((off, L, m, out_off, tile_base))
         starts = np.arange(0, L, 64, dtype=np.int32)
         ii, jj = np.meshgrid(starts, starts, indexing="ij")
         tl = np.empty(ii.size, dtype=_TILE_DT)
@@ -211,6 +212,7 @@ def group_max_batch(oracle, subproblems) -> list[np.ndarray]:
         tiles.append(tl)
         perms.append(perm)
         gids.append(gid)
+        tile_base += tl.shape[0]
         off += L
         out_off += m * m
     sub_arr = np.array(subs, dtype=_SUB_DT)
@@ -221,7 +223,7 @@ def group_max_batch(oracle, subproblems) -> list[np.ndarray]:
     tile_d = D.to_device(np.frombuffer(tile_arr.tobytes(), dtype=np.uint8), t.uint8)
     out = D.empty((max(out_off, 1),), t.float64)
     s = _oracle_struct(oracle)
-    ws = D.Workspace.get(N.size("tg_group_max_workspace_bytes", oracle.n))
+    ws = D.Workspace.get(N.size("tg_group_max_workspace_bytes", oracle.n, int(tile_arr.shape[0])))
     N.call("tg_group_max_batch", s, N.ptr(perm_d), N.ptr(gid_d), N.ptr(sub_d), len(subs), N.ptr(tile_d),
            int(tile_arr.shape[0]), N.ptr(out), out_off, N.ptr(ws), ws.numel(), N.stream_ptr())
     return out, sub_arr

@@ -82,7 +82,12 @@ def nn_chain_raw_batch(blocks_dev, sizes: np.ndarray, mat_off: np.ndarray):
     chain = D.empty((naux + 1,), t.int64)
     N.call("tg_nn_chain_batch", N.ptr(blocks_dev), N.ptr(mo), N.ptr(sz), count, N.ptr(mg), N.ptr(lefts),
            N.ptr(rights), N.ptr(heights), N.ptr(ax), N.ptr(active), N.ptr(slot), N.ptr(chain), N.stream_ptr())
-    return lefts.cpu().numpy(), rights.cpu().numpy(), heights.cpu().numpy(), merge_off
+    h = heights.cpu().numpy()
+    bad = h.view(np.int64) == np.int64(0x7ff8dead00000000)
+    if bad.any():
+        raise RuntimeError("NN-chain did not terminate: the distance matrix is not reducible "
+                           "(the reference's linkage.py:50-94 loop would not terminate either)")
+    return lefts.cpu().numpy(), rights.cpu().numpy(), h, merge_off
 
 
 def canonicalize_batch(lefts, rights, heights, merge_off, sizes):
