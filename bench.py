@@ -105,14 +105,21 @@ def dist_setup():
     return world, rank, local
 
 
-def _max_over_ranks(x: float, world: int, device) -> float:
+def _max_over_ranks(x: float, world: int, device=None) -> float:
+    """Max of a per-rank timing over all ranks (works over nccl or gloo)."""
     if world == 1:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device=device)
+    t = torch.tensor([x], dtype=torch.float64, device=device if device is not None else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def replica_seed(rank: int) -> int:
+    """Replicas-only scaling: every rank clusters its own synthetic instance."""
+    from paper_2408_09399_b200 import synth
+    return synth.DEFAULT_SEED + rank
 
 
 def _barrier(world):
@@ -137,7 +144,7 @@ def run_b200(args, world, rank, local):
 
     N.load()
     cfg = args.config
-    x_host, labels = synth.generate(cfg, n=args.n, seed=synth.DEFAULT_SEED + rank)
+    x_host, labels = synth.generate(cfg, n=args.n, seed=replica_seed(rank))
     n, L = x_host.shape
     k = synth.num_clusters(cfg)
     mode = "hub" if cfg in (3, 5) else args.apsp

@@ -224,6 +224,7 @@ struct RsMisc {
     uint32_t ccnt[RS_CMAX + 1];    // coarse counts -> fine base (exclusive scan of f_c)
     uint32_t cf[RS_CMAX];          // fine buckets per coarse bin
     uint32_t wsum[32];
+    uint32_t nsamp;
 };
 
 __host__ RsPlan rs_plan(int64_t n, int nbuf) {
@@ -316,13 +317,17 @@ row_sort_smem_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restr
         }
         // ---- A: zero coarse counters, row min/max (v excluded)
         for (int c = tid; c <= C; c += RS_T) ms.ccnt[c] = 0;
+        if (tid == 0) ms.nsamp = 0;
         double mn = INFINITY, mx = -INFINITY;
+        bool nan_seen = false;
         for (int j = tid; j < n; j += RS_T) {
             if (j == v) continue;
             double x = vals[j];
             if (x < mn) mn = x;
             if (x > mx) mx = x;
+            nan_seen |= (x != x);
         }
+        const bool row_nan = __syncthreads_or(nan_seen);
         for (int o = 16; o; o >>= 1) {
             mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
             mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -343,27 +348,33 @@ row_sort_smem_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restr
             }
         }
         __syncthreads();
-        // ---- B: coarse histogram (linear bins over [min, max]), warp-aggregated
+        // ---- B: coarse histogram (linear bins over [min, max]) from a 1-in-4 sample
+        // (it only sizes the fine buckets: accuracy affects speed, never the order)
         const double rmax = ms.rmax, cscale = ms.cscale;
         uint32_t pk[EMAX];
+        int nsamp = 0;
 #pragma unroll
         for (int e = 0; e < EMAX; e++) {
             int j = tid + e * RS_T;
             bool act = j < n && j != v;
-            int c = -1;
-            if (act) {
+            if (act && (e & 3) == 0) {
                 double t;
-                c = rs_coarse_of(vals[j], rmax, cscale, C, t);
+                atomicAdd(&ms.ccnt[rs_coarse_of(vals[j], rmax, cscale, C, t)], 1u);
+                nsamp++;
             }
-            unsigned peers = __match_any_sync(0xffffffffu, c);
-            if (act && lane == __ffs(peers) - 1) atomicAdd(&ms.ccnt[c], (uint32_t)__popc(peers));
-            pk[e] = act ? (uint32_t)c : 0xffffffffu;
+            pk[e] = act ? 0u : 0xffffffffu;
         }
+        nsamp = __reduce_add_sync(0xffffffffu, nsamp);
+        if (lane == 0 && nsamp) atomicAdd(&ms.nsamp, (uint32_t)nsamp);
         __syncthreads();
         // ---- C: fine buckets per coarse bin (about two keys each), base offsets
-        for (int c = tid; c < C; c += RS_T) {
-            uint32_t h = ms.ccnt[c];
-            ms.cf[c] = h > 2 ? (h + 1) >> 1 : 1u;
+        {
+            const uint64_t den = 2ull * (ms.nsamp ? ms.nsamp : 1u);
+            for (int c = tid; c < C; c += RS_T) {
+                uint64_t h = ms.ccnt[c];
+                uint32_t f = (uint32_t)((h * (uint64_t)m + den - 1) / den);
+                ms.cf[c] = f > 1 ? f : 1u;
+            }
         }
         __syncthreads();
         if (warp == 0) {
@@ -460,9 +471,17 @@ row_sort_smem_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restr
                 int rank = 0;
                 if (s1 - s0 > 1) {
                     const double xj = vals[j];
-                    for (int k = s0; k < s1; k++) {
-                        const int o = sidx[k];
-                        rank += rs_before(vals[o], o, xj, j);
+                    if (!row_nan) {
+                        for (int k = s0; k < s1; k++) {
+                            const int o = sidx[k];
+                            const double xo = vals[o];
+                            rank += (xo > xj) | ((xo == xj) & (o < j));
+                        }
+                    } else {
+                        for (int k = s0; k < s1; k++) {
+                            const int o = sidx[k];
+                            rank += rs_before(vals[o], o, xj, j);
+                        }
                     }
                 }
                 pk[e] = (uint32_t)(s0 + rank);
@@ -523,13 +542,17 @@ row_sort_global_kernel(const double *__restrict__ S, int64_t n64, int32_t *__res
         const double *row = S + v * n64;
         int32_t *out = order + v * (int64_t)m;
         for (int c = tid; c <= C; c += RS_T) ms.ccnt[c] = 0;
+        if (tid == 0) ms.nsamp = 0;
         double mn = INFINITY, mx = -INFINITY;
+        bool nan_seen = false;
         for (int j = tid; j < n; j += RS_T) {
             if (j == v) continue;
             double x = __ldg(row + j);
             if (x < mn) mn = x;
             if (x > mx) mx = x;
+            nan_seen |= (x != x);
         }
+        const bool row_nan = __syncthreads_or(nan_seen);
         for (int o = 16; o; o >>= 1) {
             mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
             mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -551,21 +574,23 @@ row_sort_global_kernel(const double *__restrict__ S, int64_t n64, int32_t *__res
         }
         __syncthreads();
         const double rmax = ms.rmax, cscale = ms.cscale;
-        for (int j0 = 0; j0 < n; j0 += RS_T) {
-            int j = j0 + tid;
-            bool act = j < n && j != v;
-            int c = -1;
-            if (act) {
-                double t;
-                c = rs_coarse_of(__ldg(row + j), rmax, cscale, C, t);
-            }
-            unsigned peers = __match_any_sync(0xffffffffu, c);
-            if (act && lane == __ffs(peers) - 1) atomicAdd(&ms.ccnt[c], (uint32_t)__popc(peers));
+        int nsamp = 0;
+        for (int j = tid; j < n; j += 4 * RS_T) {
+            if (j == v) continue;
+            double t;
+            atomicAdd(&ms.ccnt[rs_coarse_of(__ldg(row + j), rmax, cscale, C, t)], 1u);
+            nsamp++;
         }
+        nsamp = __reduce_add_sync(0xffffffffu, nsamp);
+        if (lane == 0 && nsamp) atomicAdd(&ms.nsamp, (uint32_t)nsamp);
         __syncthreads();
-        for (int c = tid; c < C; c += RS_T) {
-            uint32_t h = ms.ccnt[c];
-            ms.cf[c] = h > 2 ? (h + 1) >> 1 : 1u;
+        {
+            const uint64_t den = 2ull * (ms.nsamp ? ms.nsamp : 1u);
+            for (int c = tid; c < C; c += RS_T) {
+                uint64_t h = ms.ccnt[c];
+                uint32_t f = (uint32_t)((h * (uint64_t)m + den - 1) / den);
+                ms.cf[c] = f > 1 ? f : 1u;
+            }
         }
         __syncthreads();
         if (warp == 0) {
@@ -651,7 +676,8 @@ row_sort_global_kernel(const double *__restrict__ S, int64_t n64, int32_t *__res
                 const double xj = __ldg(row + j);
                 for (int k = s0; k < s1; k++) {
                     const int o = out[k];
-                    rank += rs_before(__ldg(row + o), o, xj, j);
+                    const double xo = __ldg(row + o);
+                    rank += row_nan ? (int)rs_before(xo, o, xj, j) : (int)((xo > xj) | ((xo == xj) & (o < j)));
                 }
             }
             gpk[n + j] = (uint32_t)(s0 + rank);

@@ -185,47 +185,57 @@ _SUB_DT = np.dtype([("perm_off", "<i8"), ("len", "<i4"), ("m", "<i4"), ("out_off
 _TILE_DT = np.dtype([("sub", "<i4"), ("i0", "<i4"), ("j0", "<i4")])
 
 
-def group_max_batch(oracle, subproblems) -> list[np.ndarray]:
-    """dbht.py:217-230 for several vertex-disjoint sub-problems in one launch.
+def group_layout(subproblems):
+    """Host layout of a batched group-max launch (pure numpy).
 
-    subproblems: list of member lists (each a list of int arrays, one per group).
-    Returns the m x m max matrices as one flat CUDA tensor + offsets.
+    subproblems: list of member lists (each a list of int arrays, one per group),
+    vertex-disjoint.  Returns (perm int32, gid int32, subs [_SUB_DT], tiles
+    [_TILE_DT], out_len): positions of all sub-problems back to back, the group
+    index of every position, one descriptor per sub-problem (its tiles are
+    row-major, nt x nt of 64 x 64 positions, starting at tile_off) and the size
+    of the concatenated m x m outputs.
     """
-    t = D.torch()
     perms, gids, subs, tiles = [], [], [], []
-    off = 0
-    out_off = 0
-    tile_base = 0
+    off = out_off = tile_base = 0
     for p, groups in enumerate(subproblems):
         sizes = np.array([len(g) for g in groups], dtype=np.int64)
         perm = np.concatenate([np.asarray(g, dtype=np.int64) for g in groups]).astype(np.int32)
-        gid = np.repeat(np.arange(len(groups), dtype=np.int32), sizes)
-        L = perm.shape[0]
-        m = len(groups)
-        subs.append((off, L, m, out_off, tile_base))
+        L, m = perm.shape[0], len(groups)
         starts = np.arange(0, L, 64, dtype=np.int32)
         ii, jj = np.meshgrid(starts, starts, indexing="ij")
         tl = np.empty(ii.size, dtype=_TILE_DT)
         tl["sub"] = p
         tl["i0"] = ii.reshape(-1)
         tl["j0"] = jj.reshape(-1)
-        tiles.append(tl)
+        subs.append((off, L, m, out_off, tile_base))
         perms.append(perm)
-        gids.append(gid)
+        gids.append(np.repeat(np.arange(m, dtype=np.int32), sizes))
+        tiles.append(tl)
         tile_base += tl.shape[0]
         off += L
         out_off += m * m
     sub_arr = np.array(subs, dtype=_SUB_DT)
     tile_arr = np.concatenate(tiles) if tiles else np.zeros(0, dtype=_TILE_DT)
-    perm_d = D.to_device(np.concatenate(perms), t.int32)
-    gid_d = D.to_device(np.concatenate(gids), t.int32)
-    sub_d = D.to_device(np.frombuffer(sub_arr.tobytes(), dtype=np.uint8), t.uint8)
-    tile_d = D.to_device(np.frombuffer(tile_arr.tobytes(), dtype=np.uint8), t.uint8)
-    out = D.empty((max(out_off, 1),), t.float64)
+    return np.concatenate(perms), np.concatenate(gids), sub_arr, tile_arr, out_off
+
+
+def group_max_batch(oracle, subproblems):
+    """dbht.py:217-230 for several vertex-disjoint sub-problems in one launch.
+
+    Returns the concatenated m x m max matrices (flat CUDA tensor) and the
+    sub-problem descriptors (``out_off``, ``m`` ...).
+    """
+    t = D.torch()
+    perm, gid, sub_arr, tile_arr, out_len = group_layout(subproblems)
+    perm_d = D.to_device(perm, t.int32)
+    gid_d = D.to_device(gid, t.int32)
+    sub_d = D.to_device(np.frombuffer(sub_arr.tobytes(), dtype=np.uint8).copy(), t.uint8)
+    tile_d = D.to_device(np.frombuffer(tile_arr.tobytes(), dtype=np.uint8).copy(), t.uint8)
+    out = D.empty((max(out_len, 1),), t.float64)
     s = _oracle_struct(oracle)
     ws = D.Workspace.get(N.size("tg_group_max_workspace_bytes", oracle.n, int(tile_arr.shape[0])))
-    N.call("tg_group_max_batch", s, N.ptr(perm_d), N.ptr(gid_d), N.ptr(sub_d), len(subs), N.ptr(tile_d),
-           int(tile_arr.shape[0]), N.ptr(out), out_off, N.ptr(ws), ws.numel(), N.stream_ptr())
+    N.call("tg_group_max_batch", s, N.ptr(perm_d), N.ptr(gid_d), N.ptr(sub_d), int(sub_arr.shape[0]), N.ptr(tile_d),
+           int(tile_arr.shape[0]), N.ptr(out), out_len, N.ptr(ws), ws.numel(), N.stream_ptr())
     return out, sub_arr
 
 
