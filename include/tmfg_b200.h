@@ -81,10 +81,10 @@ int tg_initial_clique(const double *rowsum, int64_t n, int32_t *clique_out, void
 
 /* tmfg.py:344-436 build_tmfg_heap (+ tmfg.py:94-182 bookkeeping).
  * Outputs: trace (n-4, 4), host_fid (n-4) face id each row subdivided,
- * edges (3n-6, 2), faces (2n-4, 3) int32; stats int64[16] =
+ * edges (3n-6, 2), faces (2n-4, 3) int32; stats int64[24] =
  * {pops, refreshes, gain_increases, status, assert_fid, assert_old_gain_bits,
- *  assert_new_gain_bits, 0, rounds, refills, cycles in: parallel refresh,
- *  replay, queue merge, insertion, refill; final pool size}.  status 0 = ok, 2 = the check_invariants
+ *  assert_new_gain_bits, then kernel self-profile counters (rounds, refills,
+ *  per-phase cycles; see tools/tmfg_profile.py)}.  status 0 = ok, 2 = the check_invariants
  * assertion of tmfg.py:429 fired (check != 0 only).  Persistent single-CTA
  * kernel; check != 0 adds the brute-force optimality test of tmfg.py:377-399. */
 size_t tg_tmfg_workspace_bytes(int64_t n);

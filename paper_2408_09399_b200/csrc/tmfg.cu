@@ -34,10 +34,13 @@ namespace {
 
 constexpr int TM_T = 1024;
 constexpr int TM_WARPS = TM_T / 32;
+constexpr int TM_BG_WARPS = 4;                   // background cursor-advancing warps
+constexpr int TM_FG_WARPS = TM_WARPS - TM_BG_WARPS;
+constexpr int TM_FG_T = TM_FG_WARPS * 32;
 constexpr int TM_EPW = 1;                       // entries refreshed per warp
 constexpr int TM_NEW_WARPS = 4;                 // warps that build new-face entries
-constexpr int TM_K = TM_EPW * (TM_WARPS - TM_NEW_WARPS);  // top-K speculated per round (28)
-constexpr int TM_B = 1024;                      // shared-memory queue capacity
+constexpr int TM_K = TM_EPW * (TM_FG_WARPS - TM_NEW_WARPS);  // top-K speculated per round
+constexpr int TM_B = 512;                       // shared-memory queue capacity
 constexpr int TM_BATCH = TM_K + 8;
 static_assert(TM_K <= 32, "replay_warp maps one queue position per lane");
 
@@ -83,7 +86,8 @@ struct Ctl {
     int hist[256];
     int done;
     int bad;
-    long long t_par, t_replay, t_merge, t_insert, t_refill, rounds, refills;
+    int bg_stop;
+    long long t_par, t_replay, t_merge, t_insert, t_refill, t_tail, rounds, refills;
     int it_round_max;
     int ph[4];
     long long phs[4];
@@ -105,10 +109,20 @@ struct TmArgs {
     Ent *pool;           // global pool, capacity 3n (two arrays, swapped on compaction)
     Ent *pool2;
     int32_t *gcursor;    // global cursors when n > 65536
+    int32_t *gmc;        // global max-corr cache when it does not fit in shared memory
     int check;           // check_invariants mode (tmfg.py:375-399)
 };
 
 __device__ __forceinline__ bool is_ins(const uint32_t *bits, int v) { return (bits[v >> 5] >> (v & 31)) & 1u; }
+
+// named barrier 1 over the foreground warps only (background warps never wait on it)
+__device__ __forceinline__ void fg_sync() { asm volatile("bar.sync 1, %0;" ::"r"(TM_FG_T) : "memory"); }
+// same barrier with a reduction result: the clock read after it really follows the release
+__device__ __forceinline__ long long fg_sync_clock() {
+    unsigned r;
+    asm volatile("bar.red.popc.u32 %0, 1, %1, 1;" : "=r"(r) : "r"(TM_FG_T) : "memory");
+    return clock64() + (long long)(r & 0u);
+}
 
 template <bool SMEM_CURSORS>
 __device__ __forceinline__ int cur_get(const uint16_t *sc, const int32_t *gc, int w) {
@@ -120,15 +134,26 @@ __device__ __forceinline__ void cur_set(uint16_t *sc, int32_t *gc, int w, int c)
     if (SMEM_CURSORS) sc[w] = (uint16_t)c;
     else gc[w] = c;
 }
+// cached max_corrs[w] (tmfg.py:181): order[w][cursor[w]], 0xffff / -1 = unknown
+template <bool SMEM_MC>
+__device__ __forceinline__ int mc_get(const uint16_t *sm, const int32_t *gm, int w) {
+    if (SMEM_MC) { int x = sm[w]; return x == 0xffff ? -1 : x; }
+    return gm[w];
+}
+template <bool SMEM_MC>
+__device__ __forceinline__ void mc_set(uint16_t *sm, int32_t *gm, int w, int u) {
+    if (SMEM_MC) sm[w] = (uint16_t)u;
+    else gm[w] = u;
+}
 
 // One warp builds up to TM_EPW entries: refresh the 3 vertices of each face
 // (first uninserted id of order[w], tmfg.py:169-182) and pick the best of the
 // three candidates (tmfg.py:266-277).  Cursor probes: 4 x 32 ids per vertex in
 // one batch of independent loads; rare long tails continue 16 x 32 at a time.
 
-template <bool SMEM_CURSORS>
-__device__ void warp_entries(const TmArgs &A, const uint32_t *bits, uint16_t *sc, int cnt, const int (*fverts)[3],
-                             const int *fids, Ent *out, int *iters) {
+template <bool SMEM_CURSORS, bool SMEM_MC>
+__device__ void warp_entries(const TmArgs &A, const uint32_t *bits, uint16_t *sc, uint16_t *smc, int cnt,
+                             const int (*fverts)[3], const int *fids, Ent *out, int *iters) {
     const int lane = threadIdx.x & 31;
     const int n = A.n, m = n - 1;
     constexpr int NV = 3 * TM_EPW;
@@ -140,7 +165,18 @@ __device__ void warp_entries(const TmArgs &A, const uint32_t *bits, uint16_t *sc
         cur[k] = k < nv ? cur_get<SMEM_CURSORS>(sc, A.gcursor, vv[k]) : 0;
         found[k] = -1;
     }
-    unsigned pending = (1u << nv) - 1u;
+    // a vertex whose cached max-corr is still uninserted needs no scan at all
+    unsigned pending = 0u;
+#pragma unroll
+    for (int k = 0; k < NV; k++) {
+        if (k < nv) {
+            const int mcv = mc_get<SMEM_MC>(smc, A.gmc, vv[k]);
+            if (mcv >= 0 && !is_ins(bits, mcv)) found[k] = mcv;
+            else pending |= 1u << k;
+        }
+    }
+    const unsigned scanned = pending;
+    long long tw0 = clock64();
     {
         int val[NV][4];
 #pragma unroll
@@ -148,11 +184,11 @@ __device__ void warp_entries(const TmArgs &A, const uint32_t *bits, uint16_t *sc
 #pragma unroll
             for (int q = 0; q < 4; q++) {
                 int idx = cur[k] + q * 32 + lane;
-                val[k][q] = (k < nv && idx < m) ? __ldg(A.order + (int64_t)vv[k] * m + idx) : -1;
+                val[k][q] = (((pending >> k) & 1u) && idx < m) ? __ldg(A.order + (int64_t)vv[k] * m + idx) : -1;
             }
 #pragma unroll
         for (int k = 0; k < NV; k++) {
-            if (k < nv) {
+            if ((pending >> k) & 1u) {
                 int firstq = 4, hitv = -1;
 #pragma unroll
                 for (int q = 3; q >= 0; q--) {
@@ -171,6 +207,7 @@ __device__ void warp_entries(const TmArgs &A, const uint32_t *bits, uint16_t *sc
             }
         }
     }
+    long long tw1 = clock64() + (found[0] & 0);
     while (pending) {
         (*iters)++;
         const int k = __ffs(pending) - 1;
@@ -204,8 +241,12 @@ __device__ void warp_entries(const TmArgs &A, const uint32_t *bits, uint16_t *sc
     if (lane == 0) {
 #pragma unroll
         for (int k = 0; k < NV; k++)
-            if (k < nv) cur_set<SMEM_CURSORS>(sc, A.gcursor, vv[k], cur[k]);
+            if ((scanned >> k) & 1u) {
+                cur_set<SMEM_CURSORS>(sc, A.gcursor, vv[k], cur[k]);
+                mc_set<SMEM_MC>(smc, A.gmc, vv[k], found[k]);
+            }
     }
+    long long tw2 = clock64() + (found[0] & 0);
     // 9 similarity loads per entry: lane = e*9 + ci*3 + vi loads S[face_vi, cand_ci]
     double sv = 0.0;
     int my_u = -1;
@@ -222,6 +263,8 @@ __device__ void warp_entries(const TmArgs &A, const uint32_t *bits, uint16_t *sc
     }
     // lanes with vi == 0 form g = (S[a,u] + S[b,u]) + S[c,u]  (tmfg.py:273, left to right)
     const double s1 = __shfl_down_sync(0xffffffffu, sv, 1);
+    long long tw3 = clock64() + (long long)(s1 != s1);
+    if (lane == 0) { iters[1] = (int)(tw1 - tw0); iters[2] = (int)(tw2 - tw1); iters[3] = (int)(tw3 - tw2); }
     const double s2 = __shfl_down_sync(0xffffffffu, sv, 2);
     const double g = __dadd_rn(__dadd_rn(sv, s1), s2);
     // entry leader (lane e*9) picks the best of its 3 candidates: g desc, u asc
@@ -282,8 +325,8 @@ __device__ __forceinline__ unsigned long long ent_key_lo(const Ent &e) { return 
 // the first digit boundary whose "all keys above" set is non-empty and fits.
 // Keys are unique, the pool order is irrelevant, so the result is exact.
 template <int NT>
-__device__ void refill(const TmArgs &A, Ctl &ctl, Ent *cur, Ent *scratch, Ent *red_e, int *red_ok) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+__device__ void refill(const TmArgs &A, Ctl &ctl, Ent *cur, Ent *scratch, Ent *red_e, int *red_ok, int tid) {
+    const int lane = tid & 31, warp = tid >> 5;
     Ent *pool = ctl.psel ? A.pool2 : A.pool;
     Ent *other = ctl.psel ? A.pool : A.pool2;
     const int P = ctl.pool_count;
@@ -292,13 +335,13 @@ __device__ void refill(const TmArgs &A, Ctl &ctl, Ent *cur, Ent *scratch, Ent *r
     bool take_all = P <= room;
     if (!take_all) {
         if (tid == 0) { ctl.sel_prefix = 0ull; ctl.sel_room = room; ctl.stop = 0; }
-        __syncthreads();
+        fg_sync();
         for (int pass = 0; pass < 16; pass++) {
             const bool lo_part = pass >= 8;
             const int p = pass & 7;
             const int shift = 56 - 8 * p;
             for (int i = tid; i < 256; i += NT) ctl.hist[i] = 0;
-            __syncthreads();
+            fg_sync();
             const unsigned long long pref = ctl.sel_prefix;
             for (int i = tid; i < P; i += NT) {
                 Ent x = pool[i];
@@ -308,7 +351,7 @@ __device__ void refill(const TmArgs &A, Ctl &ctl, Ent *cur, Ent *scratch, Ent *r
                 if (p > 0) match = match && ((key >> (64 - 8 * p)) == (pref >> (64 - 8 * p)));
                 if (match) atomicAdd(&ctl.hist[(key >> shift) & 255], 1);
             }
-            __syncthreads();
+            fg_sync();
             if (tid == 0) {
                 int acc = 0, d = 255, last_fit = -1;
                 for (; d >= 0; d--) {
@@ -325,7 +368,7 @@ __device__ void refill(const TmArgs &A, Ctl &ctl, Ent *cur, Ent *scratch, Ent *r
                     ctl.sel_prefix = pref | ((unsigned long long)d << shift);
                 }
             }
-            __syncthreads();
+            fg_sync();
             if (ctl.stop) {
                 if (!lo_part) { thr_hi = ctl.sel_prefix; thr_lo = 0ull; }
                 else thr_lo = ctl.sel_prefix;
@@ -333,16 +376,16 @@ __device__ void refill(const TmArgs &A, Ctl &ctl, Ent *cur, Ent *scratch, Ent *r
             }
             if (pass == 7) {
                 thr_hi = ctl.sel_prefix;
-                __syncthreads();
+                fg_sync();
                 if (tid == 0) ctl.sel_prefix = 0ull;
-                __syncthreads();
+                fg_sync();
             }
         }
         if (!ctl.stop) thr_lo = ctl.sel_prefix;
     }
-    __syncthreads();
+    fg_sync();
     if (tid == 0) { ctl.refill_take = 0; ctl.nsurv = 0; }
-    __syncthreads();
+    fg_sync();
     Ent best;
     bool ok = false;
     for (int i = tid; i < P; i += NT) {
@@ -364,7 +407,7 @@ __device__ void refill(const TmArgs &A, Ctl &ctl, Ent *cur, Ent *scratch, Ent *r
         if (yok && (!ok || ent_gt(y, best))) { best.g = y.g; best.fid = y.fid; ok = true; }
     }
     if (lane == 0) { red_e[warp] = best; red_ok[warp] = ok; }
-    __syncthreads();
+    fg_sync();
     const int nt = ctl.refill_take;
     const int sz = ctl.size;
     for (int i = tid; i < nt; i += NT) {
@@ -373,7 +416,7 @@ __device__ void refill(const TmArgs &A, Ctl &ctl, Ent *cur, Ent *scratch, Ent *r
         for (int j = 0; j < nt; j++) rank += ent_gt(scratch[j], x);
         cur[sz + rank] = x;
     }
-    __syncthreads();
+    fg_sync();
     if (tid == 0) {
         ctl.size = sz + nt;
         ctl.pool_count = ctl.nsurv;
@@ -385,7 +428,7 @@ __device__ void refill(const TmArgs &A, Ctl &ctl, Ent *cur, Ent *scratch, Ent *r
         ctl.pool_has_max = any;
         if (any) ctl.pool_max = b;
     }
-    __syncthreads();
+    fg_sync();
 }
 
 
@@ -544,7 +587,72 @@ __device__ void replay_warp(const TmArgs &A, Ctl &ctl, const Ent *L, const Ent *
     __syncwarp();
 }
 
-template <bool SMEM_CURSORS>
+// Background warp: sweep the vertices (32 per step, lane-parallel check), and for
+// every vertex whose cached max-corr is unknown or already inserted, advance its
+// cursor to the first uninserted id of its sorted row (16 x 32 ids per load batch).
+template <bool SMEM_CURSORS, bool SMEM_MC>
+__device__ void bg_sweep(const TmArgs &A, const uint32_t *bits_, uint16_t *sc_, uint16_t *smc_, const int *stop_,
+                         int bgw) {
+    const int lane = threadIdx.x & 31;
+    const int n = A.n, m = n - 1;
+    volatile const uint32_t *bits = bits_;
+    volatile uint16_t *sc = sc_;
+    volatile uint16_t *smc = smc_;
+    volatile int32_t *gcur = A.gcursor;
+    volatile int32_t *gmc = A.gmc;
+    volatile const int *stop = stop_;
+    int w0 = bgw * 32;
+    while (!*stop) {
+        const int w = w0 + lane;
+        bool need = false;
+        if (w < n) {
+            int mcv = SMEM_MC ? (smc[w] == 0xffff ? -1 : (int)smc[w]) : gmc[w];
+            need = (mcv < 0) || ((bits[mcv >> 5] >> (mcv & 31)) & 1u);
+            // a vertex that is itself inserted may still be refreshed (face vertex)
+        }
+        unsigned todo = __ballot_sync(0xffffffffu, need);
+        while (todo && !*stop) {
+            const int l = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const int v = w0 + l;
+            int c = SMEM_CURSORS ? (int)sc[v] : gcur[v];
+            int hit = -1;
+            while (hit < 0 && c < m) {
+                int val[16];
+#pragma unroll
+                for (int q = 0; q < 16; q++) {
+                    int idx = c + q * 32 + lane;
+                    val[q] = idx < m ? __ldg(A.order + (int64_t)v * m + idx) : -1;
+                }
+                int firstq = 16, hv = -1;
+#pragma unroll
+                for (int q = 15; q >= 0; q--) {
+                    bool ok = val[q] >= 0 && !((bits[val[q] >> 5] >> (val[q] & 31)) & 1u);
+                    if (ok) { firstq = q; hv = val[q]; }
+                }
+                const unsigned best = __reduce_min_sync(0xffffffffu, (unsigned)(firstq * 32 + lane));
+                if (best < 512u) {
+                    hit = __shfl_sync(0xffffffffu, hv, best & 31);
+                    c += (int)best;
+                } else {
+                    c += 512;
+                }
+            }
+            if (lane == 0 && hit >= 0) {
+                if (SMEM_CURSORS) {
+                    if ((int)sc[v] < c) sc[v] = (uint16_t)c;
+                } else if (gcur[v] < c) gcur[v] = c;
+                if (SMEM_MC) smc[v] = (uint16_t)hit;
+                else gmc[v] = hit;
+            }
+            __syncwarp();
+        }
+        w0 += TM_BG_WARPS * 32;
+        if (w0 >= n) w0 = bgw * 32;
+    }
+}
+
+template <bool SMEM_CURSORS, bool SMEM_MC>
 __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
     extern __shared__ __align__(16) unsigned char tm_smem[];
     const int n = A.n;
@@ -567,12 +675,18 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
     uint32_t *bits = reinterpret_cast<uint32_t *>(buf1 + TM_B);
     const int nwords = (n + 31) >> 5;
     uint16_t *sc = reinterpret_cast<uint16_t *>(bits + nwords);
+    uint16_t *smc = sc + (SMEM_CURSORS ? ((n + 1) & ~1) : 0);
 
     for (int i = tid; i < nwords; i += TM_T) bits[i] = 0u;
     if (SMEM_CURSORS) {
         for (int i = tid; i < n; i += TM_T) sc[i] = 0;
     } else {
         for (int i = tid; i < n; i += TM_T) A.gcursor[i] = 0;
+    }
+    if (SMEM_MC) {
+        for (int i = tid; i < n; i += TM_T) smc[i] = 0xffff;
+    } else {
+        for (int i = tid; i < n; i += TM_T) A.gmc[i] = -1;
     }
     for (int i = tid; i < 3 * n; i += TM_T) A.fv[i] = make_int4(0, 0, 0, 0);
     __syncthreads();
@@ -603,7 +717,8 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
         ctl.psel = 0;
         ctl.done = (n <= 4);
         ctl.bad = 0;
-        ctl.t_par = ctl.t_replay = ctl.t_merge = ctl.t_insert = ctl.t_refill = ctl.rounds = ctl.refills = 0;
+        ctl.bg_stop = 0;
+        ctl.t_par = ctl.t_replay = ctl.t_merge = ctl.t_insert = ctl.t_refill = ctl.t_tail = ctl.rounds = ctl.refills = 0;
         ctl.it_round_max = 0;
         for (int q = 0; q < 4; q++) { ctl.ph[q] = 0; ctl.phs[q] = 0; }
         ctl.pops_dbg = 0;
@@ -611,6 +726,17 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
     }
     __syncthreads();
 
+    if (warp < TM_BG_WARPS) {
+        // ============ background: keep every vertex's cached max-corr fresh so the
+        // foreground refreshes rarely scan (cursor / max-corr writes are monotone
+        // facts -- "all ids before the cursor are inserted" -- valid in any order).
+        // Background warps have the LOWEST ids: the scheduler favours high warp ids,
+        // so the latency-critical foreground (replay on warp 31) keeps priority.
+        bg_sweep<SMEM_CURSORS, SMEM_MC>(A, bits, sc, smc, &ctl.bg_stop, warp);
+    } else {
+    // foreground numbering: warp 31 is foreground warp 0 (replay, insertion, leader)
+    const int warp = (TM_WARPS - 1) - (threadIdx.x >> 5);
+    const int tid = warp * 32 + lane;
     long long tc0 = clock64(), tc1;
     while (!ctl.done) {
         if (tid == 0) { tc0 = clock64(); ctl.rounds++; }
@@ -623,7 +749,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
                 if (warp < ctl.ne_count) {
                     int fids[1] = {ctl.ne_fid[warp]};
                     int fvv[1][3] = {{ctl.ne_v[warp][0], ctl.ne_v[warp][1], ctl.ne_v[warp][2]}};
-                    warp_entries<SMEM_CURSORS>(A, bits, sc, 1, fvv, fids, &NE[warp], my_iters);
+                    warp_entries<SMEM_CURSORS, SMEM_MC>(A, bits, sc, smc, 1, fvv, fids, &NE[warp], my_iters);
                 }
             } else {
                 int base = TM_EPW * (warp - TM_NEW_WARPS);
@@ -650,36 +776,34 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
                     }
                 }
                 if (cnt) {
-                    warp_entries<SMEM_CURSORS>(A, bits, sc, cnt, fvv, fids, Lout[warp - TM_NEW_WARPS], my_iters);
+                    warp_entries<SMEM_CURSORS, SMEM_MC>(A, bits, sc, smc, cnt, fvv, fids, Lout[warp - TM_NEW_WARPS], my_iters);
                     if (lane == 0)
                         for (int q = 0; q < cnt; q++) Lref[idx[q]] = Lout[warp - TM_NEW_WARPS][q];
                 }
             }
         }
         if (lane == 0 && my_iters[0]) atomicMax(&ctl.it_round_max, my_iters[0]);
-        {
-            int zz = __syncthreads_or(tpw0 == 0);
-            if (tid == 0) ctl.phs[0] += clock64() + zz - tc0;   // loop top -> all warps done
+        if (lane == 0) {
+            atomicMax(&ctl.ph[1], my_iters[1]);
+            atomicMax(&ctl.ph[2], my_iters[2]);
+            atomicMax(&ctl.ph[3], my_iters[3]);
+            atomicMax(&ctl.ph[0], (int)(clock64() - tpw0));
         }
+        tc1 = fg_sync_clock();
         // ================= replay the pops (warp 0, exact sequential semantics)
         if (tid == 0) {
-            tc1 = clock64();
             ctl.t_par += tc1 - tc0;
             tc0 = tc1;
         }
         if (warp == 0) replay_warp(A, ctl, L, Lref, Lstale, NE, batch, tobuf, rk_g, rk_f, rk_src);
-        {
-            int zz = __syncthreads_or(0);
-            if (tid == 0) ctl.phs[1] += clock64() + zz - tc0;   // loop top -> replay done
-        }
+        tc1 = fg_sync_clock();
         if (tid == 0) {
-            tc1 = clock64();
             ctl.t_replay += tc1 - tc0;
             tc0 = tc1;
             ctl.it_maxsum += ctl.it_round_max;
             ctl.it_total += ctl.it_round_max ? 1 : 0;
             ctl.it_round_max = 0;
-            for (int q = 0; q < 4; q++) ctl.ph[q] = 0;
+            for (int q = 0; q < 4; q++) { ctl.phs[q] += ctl.ph[q]; ctl.ph[q] = 0; }
         }
         // ================= merge: buffer[removed..size) + tobuf -> other half
         {
@@ -687,7 +811,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
             Ent *nxt = ctl.sel ? buf0 : buf1;
             const int r = ctl.removed, sz = ctl.size, nb = ctl.nbuf_new;
             const int old = sz - r;
-            for (int i = tid; i < old; i += TM_T) {
+            for (int i = tid; i < old; i += TM_FG_T) {
                 Ent x = cur[r + i];
                 int lo = 0, hi = nb;  // # of tobuf entries popping before x
                 while (lo < hi) {
@@ -703,7 +827,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
                     if (pos == TM_B) { ctl.pool_max = x; ctl.pool_has_max = 1; }
                 }
             }
-            for (int k = tid; k < nb; k += TM_T) {
+            for (int k = tid; k < nb; k += TM_FG_T) {
                 Ent x = tobuf[k];
                 int lo = 0, hi = old;  // # of old entries popping before x
                 while (lo < hi) {
@@ -720,7 +844,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
                 }
             }
         }
-        __syncthreads();
+        fg_sync();
         if (tid == 0) {
             int total = ctl.size - ctl.removed + ctl.nbuf_new;
             if (total > TM_B) {
@@ -731,10 +855,9 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
             ctl.size = total;
             ctl.sel ^= 1;
         }
-        __syncthreads();
+        tc1 = fg_sync_clock();
         // ================= insert the winner
         if (tid == 0) {
-            tc1 = clock64();
             ctl.t_merge += tc1 - tc0;
             tc0 = tc1;
             ctl.ne_count = 0;
@@ -776,16 +899,21 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
             }
             if (ctl.bad) ctl.done = 1;
         }
-        __syncthreads();
-        if (tid == 0) { tc1 = clock64(); ctl.t_insert += tc1 - tc0; tc0 = tc1; }
+        tc1 = fg_sync_clock();
+        if (tid == 0) { ctl.t_insert += tc1 - tc0; tc0 = tc1; }
         if (ctl.done) break;
         // ================= refill the shared buffer from the pool when short
         if (ctl.size < TM_K && ctl.pool_count > 0) {
-            refill<TM_T>(A, ctl, ctl.sel ? buf1 : buf0, ctl.sel ? buf0 : buf1, red_e, red_ok);
-            if (tid == 0) { tc1 = clock64(); ctl.t_refill += tc1 - tc0; ctl.refills++; tc0 = tc1; }
+            refill<TM_FG_T>(A, ctl, ctl.sel ? buf1 : buf0, ctl.sel ? buf0 : buf1, red_e, red_ok, tid);
+            tc1 = fg_sync_clock();
+            if (tid == 0) { ctl.t_refill += tc1 - tc0; ctl.refills++; tc0 = tc1; }
         }
         if (tid == 0) ctl.L_count = min(TM_K, ctl.size);
-        __syncthreads();
+        tc1 = fg_sync_clock();
+        if (tid == 0) ctl.t_tail += tc1 - tc0;
+    }
+    fg_sync();
+        if (tid == 0) *((volatile int *)&ctl.bg_stop) = 1;
     }
     __syncthreads();
     // ================= alive faces in creation order
@@ -825,22 +953,28 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
         A.stats[1] = ctl.refreshes;
         A.stats[2] = ctl.gain_inc;
         A.stats[3] = ctl.bad;
+        A.stats[7] = ctl.it_total * 100000 + ctl.it_maxsum;
         A.stats[8] = ctl.rounds;
         A.stats[9] = ctl.refills;
-        A.stats[12] = ctl.t_merge;
-        A.stats[13] = ctl.t_insert;
+        A.stats[10] = ctl.phs[0];   // sum over rounds of the slowest warp's refresh time
+        A.stats[11] = ctl.phs[1];   //   ... of its first cursor probe
+        A.stats[12] = ctl.phs[2];   //   ... of its long-tail scan
+        A.stats[13] = ctl.phs[3];   //   ... of its similarity loads
         A.stats[14] = ctl.t_refill;
         A.stats[15] = ctl.pool_count;
-        A.stats[10] = ctl.phs[0];
-        A.stats[11] = ctl.phs[1];
-        A.stats[7] = ctl.it_total * 100000 + ctl.it_maxsum;
+        A.stats[16] = ctl.t_par;
+        A.stats[17] = ctl.t_replay;
+        A.stats[18] = ctl.t_merge;
+        A.stats[19] = ctl.t_insert;
+        A.stats[20] = ctl.t_tail;
     }
 }
 
-size_t tm_smem_bytes(int64_t n, bool smem_cursors) {
+size_t tm_smem_bytes(int64_t n, bool smem_cursors, bool smem_mc) {
     size_t b = (size_t)2 * TM_B * sizeof(Ent);
     b += (size_t)((n + 31) / 32) * 4;
-    if (smem_cursors) b += (size_t)n * 2;
+    if (smem_cursors) b += (size_t)((n + 1) & ~1) * 2;
+    if (smem_mc) b += (size_t)n * 2;
     return tg_align_up(b, 16) + 64;
 }
 
@@ -864,7 +998,7 @@ TG_API size_t tg_tmfg_workspace_bytes(int64_t n) {
     size_t b = 0;
     b += tg_align_up((size_t)3 * n * sizeof(int4), 256);
     b += tg_align_up((size_t)(3 * n + TM_B + 64) * sizeof(Ent), 256);
-    b += tg_align_up((size_t)n * sizeof(int32_t), 256);
+    b += tg_align_up((size_t)n * sizeof(int32_t), 256) * 2;
     b += tg_align_up((size_t)(3 * n + TM_B + 64) * sizeof(Ent), 256);
     return b + 1024;
 }
@@ -890,17 +1024,23 @@ TG_API int tg_tmfg_heap(const double *S, const int32_t *order, int64_t n, const 
     A.pool = ar.take<Ent>((size_t)3 * n + TM_B + 64);
     A.pool2 = ar.take<Ent>((size_t)3 * n + TM_B + 64);
     A.gcursor = ar.take<int32_t>((size_t)n);
-    if (!A.fv || !A.pool || !A.pool2 || !A.gcursor) return TG_ERR_WORKSPACE;
+    A.gmc = ar.take<int32_t>((size_t)n);
+    if (!A.fv || !A.pool || !A.pool2 || !A.gcursor || !A.gmc) return TG_ERR_WORKSPACE;
     cudaStream_t st = tg_stream(stream);
-    bool smem_cur = n <= 65536;
-    size_t smem = tm_smem_bytes(n, smem_cur);
-    if (smem_cur) {
-        TG_CUDA_CHECK(cudaFuncSetAttribute(tmfg_heap_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        tmfg_heap_kernel<true><<<1, TM_T, smem, st>>>(A); tg_count_launch(1);
-    } else {
-        TG_CUDA_CHECK(cudaFuncSetAttribute(tmfg_heap_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        tmfg_heap_kernel<false><<<1, TM_T, smem, st>>>(A); tg_count_launch(1);
-    }
+    const bool smem_cur = n <= 65535;
+    const bool smem_mc = smem_cur && tm_smem_bytes(n, true, true) <= 200 * 1024;
+    const size_t smem = tm_smem_bytes(n, smem_cur, smem_mc);
+#define TM_LAUNCH(C, M)                                                                                   \
+    do {                                                                                                  \
+        TG_CUDA_CHECK(cudaFuncSetAttribute(tmfg_heap_kernel<C, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                           (int)smem));                                                  \
+        tmfg_heap_kernel<C, M><<<1, TM_T, smem, st>>>(A);                                                 \
+        tg_count_launch(1);                                                                               \
+    } while (0)
+    if (smem_cur && smem_mc) TM_LAUNCH(true, true);
+    else if (smem_cur) TM_LAUNCH(true, false);
+    else TM_LAUNCH(false, false);
+#undef TM_LAUNCH
     TG_LAUNCH_CHECK();
     return TG_OK;
 }

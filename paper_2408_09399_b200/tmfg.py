@@ -146,7 +146,7 @@ def build_tmfg_heap_device(Sd, order_dev, clique_dev, check_invariants: bool = F
     host_fid = D.empty((max(n - 4, 0),), t.int32)
     edges = D.empty((3 * n - 6, 2), t.int32)
     faces = D.empty((2 * n - 4, 3), t.int32)
-    stats = D.empty((16,), t.int64)
+    stats = D.empty((24,), t.int64)
     ws = D.Workspace.get(N.size("tg_tmfg_workspace_bytes", n))
     N.call("tg_tmfg_heap", N.ptr(Sd), N.ptr(order_dev), n, N.ptr(clique_dev), N.ptr(trace), N.ptr(host_fid),
            N.ptr(edges), N.ptr(faces), N.ptr(stats), 1 if check_invariants else 0, N.ptr(ws), ws.numel(),
@@ -207,7 +207,8 @@ def build_tmfg_heap(S, lists: SortedNeighborLists | None = None, config: BuildCo
     g._S_host = S
     g._raw_stats = {"pops": int(raw[0]), "refreshes": int(raw[1]), "gain_increases": int(raw[2])}
     g._kernel_profile = {k: int(raw[i]) for i, k in enumerate(
-        ["rounds", "refills", "cyc_parallel", "cyc_replay", "cyc_merge", "cyc_insert", "cyc_refill", "pool"], 8)}
+        ["rounds", "refills", "cyc_warp_max", "cyc_probe_max", "cyc_tail_max", "cyc_S_max", "cyc_refill", "pool",
+         "cyc_parallel", "cyc_replay", "cyc_merge", "cyc_insert", "cyc_round_tail"], 8)}
     return g
 
 

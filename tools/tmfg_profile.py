@@ -16,9 +16,11 @@ for rep in range(2):
     out = tmfg.build_tmfg_heap_device(S, order, clique)
     torch.cuda.synchronize(); dt = time.perf_counter() - t0
 st = out["stats"].cpu().numpy()
-names = ["pops", "refreshes", "gain_inc", "status", "a", "b", "c", "d", "rounds", "refills", "cyc_par_done", "cyc_replay_done",
-         "cyc_merge", "cyc_insert", "cyc_refill", "pool"]
+names = ["pops", "refreshes", "gain_inc", "status", "a4", "a5", "a6", "tails", "rounds", "refills", "cyc_warp_max", "cyc_probe_max", "cyc_tail_max", "cyc_S_max", "cyc_refill", "pool", "cyc_par", "cyc_replay", "cyc_merge", "cyc_insert", "cyc_tail"]
 d = {k: int(v) for k, v in zip(names, st)}
 d["ms"] = dt * 1e3
 d["us_per_insert"] = dt * 1e6 / (n - 4)
+for kk in ("cyc_warp_max", "cyc_probe_max", "cyc_tail_max", "cyc_S_max", "cyc_refill", "cyc_par", "cyc_replay", "cyc_merge", "cyc_insert", "cyc_tail"):
+    d[kk + "_per_round"] = round(d[kk] / max(d["rounds"], 1))
+d["cyc_per_round_total"] = round(dt * 1.965e9 / max(d["rounds"], 1))
 print(json.dumps(d))
