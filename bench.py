@@ -159,9 +159,9 @@ def run_b200(args, world, rank, local):
         S = simmatrix.pearson_similarity_device(X)
         marks[1].record()
         simmatrix.validate_device(S)
-        order, rowsum = simmatrix.sort_rows_device(S, with_rowsum=True)
+        order, screen = simmatrix.sort_rows_device(S, with_screen=True)
         marks[2].record()
-        clique = tmfg.initial_clique_device(S, rowsum)
+        clique = tmfg.initial_clique_device(S, screen)
         out = tmfg.build_tmfg_heap_device(S, order, clique)
         marks[3].record()
         graph = tmfg.TmfgGraph(n=n, edges=out["edges"], weights=tmfg.edge_weights_device(S, out["edges"]),
@@ -221,7 +221,7 @@ def run_b200(args, world, rank, local):
         flush.zero_()
         a, b = ev(), ev()
         a.record()
-        simmatrix.sort_rows_device(S, with_rowsum=True)
+        simmatrix.sort_rows_device(S, with_screen=True)
         b.record()
         torch.cuda.synchronize()
         sort_ms.append(a.elapsed_time(b))
@@ -268,7 +268,7 @@ def run_b200(args, world, rank, local):
                        "n": n, "L": L, "apsp": mode, "k": k, "parallelism": f"replicas{world}",
                        "l2": "flushed (256 MB write) between timed steps; S (8n^2 B) exceeds L2"},
             "stage_ms": {kk: round(float(np.mean(vv)), 3) for kk, vv in stage.items()},
-            "roofline": {"bound": "hbm", "kernel": "row_sort_smem_kernel (per-row neighbour sort)",
+            "roofline": {"bound": "hbm", "kernel": "row_sort_tma_kernel (per-row neighbour sort)",
                          "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                          "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
                          "algorithmic_bytes": sort_bytes, "kernel_ms": round(sort_avg, 4),

@@ -62,20 +62,29 @@ int tg_pearson_f64(const double *X, int64_t n, int64_t L, double *S_out, void *w
 int tg_validate_f64(const double *S, int64_t n, int32_t *flags_out, void *stream);
 
 /* simmatrix.py:225-249 sort_neighbor_lists: order_out (n, n-1) int32, each row the
- * ids by (S desc, id asc) with the row's own id removed.  If rowsum_out is not
- * NULL it also receives tmfg.py:76 `S.sum(axis=1) - diag(S)` (numpy pairwise
- * summation order, bit-identical). */
+ * ids by (S desc, id asc) with the row's own id removed.  If screen_out (2n
+ * doubles) is not NULL the same pass writes the initial-clique screen:
+ * screen_out[v] = sum_j S[v, j] - S[v, v] in this kernel's summation order and
+ * screen_out[n + v] = a rigorous bound on its distance to numpy's pairwise sum
+ * (tmfg.py:76), consumed by tg_initial_clique_screened. */
 size_t tg_row_sort_workspace_bytes(int64_t n);
-int tg_row_sort_f64(const double *S, int64_t n, int32_t *order_out, double *rowsum_out, void *ws,
+int tg_row_sort_f64(const double *S, int64_t n, int32_t *order_out, double *screen_out, void *ws,
                     size_t ws_bytes, void *stream);
 
-/* tmfg.py:76: rowsum_out[v] = pairwise_sum(S[v, :]) - S[v, v]. */
+/* tmfg.py:76: rowsum_out[v] = pairwise_sum(S[v, :]) - S[v, v] (numpy order, bit-identical). */
 size_t tg_row_sums_workspace_bytes(int64_t n);
 int tg_row_sums_f64(const double *S, int64_t n, double *rowsum_out, void *ws, size_t ws_bytes, void *stream);
 
 /* tmfg.py:71-79 select_initial_clique from the row sums: 4 ids (sum desc, id asc),
  * written ascending to clique_out (device int32[4]). */
 int tg_initial_clique(const double *rowsum, int64_t n, int32_t *clique_out, void *stream);
+
+/* tmfg.py:71-79 select_initial_clique from the row-sort screen: rows that cannot
+ * reach the top 4 under any value inside their bound are dropped, the rest get
+ * exact numpy pairwise sums (same result as tg_row_sums_f64 + tg_initial_clique). */
+size_t tg_initial_clique_screened_workspace_bytes(int64_t n);
+int tg_initial_clique_screened(const double *S, int64_t n, const double *screen, int32_t *clique_out, void *ws,
+                               size_t ws_bytes, void *stream);
 
 /* ---------------------------------------------------------------------- TMFG */
 

@@ -67,6 +67,8 @@ _PROTOS = {
     "tg_row_sums_workspace_bytes": (c_sz, [c_i64]),
     "tg_row_sums_f64": (ctypes.c_int, [c_p, c_i64, c_p, c_p, c_sz, c_p]),
     "tg_initial_clique": (ctypes.c_int, [c_p, c_i64, c_p, c_p]),
+    "tg_initial_clique_screened_workspace_bytes": (c_sz, [c_i64]),
+    "tg_initial_clique_screened": (ctypes.c_int, [c_p, c_i64, c_p, c_p, c_p, c_sz, c_p]),
     "tg_tmfg_workspace_bytes": (c_sz, [c_i64]),
     "tg_tmfg_heap": (ctypes.c_int, [c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_int32, c_p, c_sz, c_p]),
     "tg_edge_weights": (ctypes.c_int, [c_p, c_i64, c_p, c_i64, c_p, c_p]),

@@ -46,7 +46,7 @@ struct PwTree {
 };
 
 template <int N>
-__device__ int pw_build(PwTree<N> &t, int off, int len, int *height) {
+__host__ __device__ int pw_build(PwTree<N> &t, int off, int len, int *height) {
     if (len <= 128) {
         int id = t.nnodes++;
         t.a[id] = off;
@@ -67,7 +67,7 @@ __device__ int pw_build(PwTree<N> &t, int off, int len, int *height) {
 
 // single thread; `height` is scratch of PW_MAXNODES ints
 template <int N>
-__device__ void pw_plan(PwTree<N> &t, int n, int *height) {
+__host__ __device__ void pw_plan(PwTree<N> &t, int n, int *height) {
     t.nnodes = 0;
     t.root = pw_build(t, 0, n, height);
     int H = height[t.root];
@@ -129,15 +129,27 @@ __device__ double pw_eval(const PwTree<N> &t, double *val, Load ld) {
     return val[t.root];
 }
 
-__global__ void row_sums_kernel(const double *__restrict__ S, int64_t n, double *__restrict__ rowsum) {
+// rowsum[k] = pairwise_sum(S[v]) - S[v, v] for v = rows[k] (rows == NULL: v = k, k < n)
+// (the plan is built on the host and passed by value, copied to shared memory)
+__global__ void row_sums_kernel(const double *__restrict__ S, int64_t n, double *__restrict__ rowsum,
+                                const int32_t *__restrict__ rows, const int32_t *__restrict__ nrows,
+                                const __grid_constant__ PwTree<PW_MAXNODES> plan) {
     __shared__ PwTree<PW_MAXNODES> tree;
     __shared__ double val[PW_MAXNODES];
-    if (threadIdx.x == 0) pw_plan(tree, (int)n, reinterpret_cast<int *>(val));
+    for (int i = threadIdx.x; i < plan.nnodes; i += blockDim.x) {
+        tree.a[i] = plan.a[i];
+        tree.b[i] = plan.b[i];
+        tree.lvl[i] = plan.lvl[i];
+    }
+    if (threadIdx.x < 33) tree.lvl_off[threadIdx.x] = plan.lvl_off[threadIdx.x];
+    if (threadIdx.x == 0) { tree.nnodes = plan.nnodes; tree.nlevels = plan.nlevels; tree.root = plan.root; }
     __syncthreads();
-    for (int64_t v = blockIdx.x; v < n; v += gridDim.x) {
+    const int64_t cnt = rows ? (int64_t)*nrows : n;
+    for (int64_t k = blockIdx.x; k < cnt; k += gridDim.x) {
+        const int64_t v = rows ? (int64_t)rows[k] : k;
         const double *row = S + v * n;
         double root = pw_eval(tree, val, [&](int i) { return __ldg(row + i); });
-        if (threadIdx.x == 0) rowsum[v] = __dsub_rn(root, row[v]);
+        if (threadIdx.x == 0) rowsum[k] = __dsub_rn(root, row[v]);
         __syncthreads();
     }
 }
@@ -151,18 +163,22 @@ __device__ __forceinline__ bool clique_better(double si, int64_t i, double sj, i
     return i < j;
 }
 
-__global__ void clique_kernel(const double *__restrict__ rowsum, int64_t n, int32_t *__restrict__ out) {
+// top-4 of (sum desc, id asc) over rowsum[k], id = rows ? rows[k] : k
+__global__ void clique_kernel(const double *__restrict__ rowsum, int64_t n, int32_t *__restrict__ out,
+                              const int32_t *__restrict__ rows, const int32_t *__restrict__ nrows) {
     __shared__ double bs[32];
     __shared__ int64_t bi[32];
     __shared__ int64_t chosen[4];
+    const int64_t cnt = rows ? (int64_t)*nrows : n;
     for (int k = 0; k < 4; k++) {
         double best = 0.0;
         int64_t bid = -1;
-        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        for (int64_t kk = threadIdx.x; kk < cnt; kk += blockDim.x) {
+            const int64_t i = rows ? (int64_t)rows[kk] : kk;
             bool used = false;
             for (int q = 0; q < k; q++) used |= (chosen[q] == i);
             if (used) continue;
-            double s = rowsum[i];
+            double s = rowsum[kk];
             if (bid < 0 || clique_better(s, i, best, bid)) { best = s; bid = i; }
         }
         for (int o = 16; o; o >>= 1) {
@@ -213,13 +229,75 @@ __host__ __device__ __forceinline__ int rs_coarse_bins(int m) {
 // fine buckets never exceed C + ceil(m/2) + C
 __host__ __device__ __forceinline__ int rs_fine_cap(int m) { return 2 * rs_coarse_bins(m) + (m + 1) / 2 + 1; }
 
-struct RsPlan {
-    int n, C, NBcap, nbuf, stride;
-    size_t off_sidx, off_fcnt, off_misc, smem;
-};
+// Candidates for the initial clique from the sort's row-sum screen: screen[v] is
+// the row sum in any summation order and screen[n + v] bounds its distance to
+// numpy's pairwise result, so the exact sum lies in [lo_v, hi_v].  With L4 the
+// 4th largest lo, a row with hi_v < L4 has 4 rows strictly above it and cannot
+// be chosen; the rest (normally 4-6 rows) get exact pairwise sums.  Any NaN in
+// the screen makes every row a candidate (numpy's NaN ordering is then exact).
+__global__ void clique_screen_kernel(const double *__restrict__ screen, int64_t n, int32_t *__restrict__ cand,
+                                     int32_t *__restrict__ ncand) {
+    __shared__ double bs[32];
+    __shared__ int64_t bi[32];
+    __shared__ int64_t chosen[4];
+    __shared__ double l4;
+    __shared__ int cnt;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    bool nan_seen = false;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+        nan_seen |= isnan(screen[i]) | isnan(screen[n + i]);
+    const bool any_nan = __syncthreads_or(nan_seen);
+    if (threadIdx.x == 0) { cnt = 0; l4 = -INFINITY; }
+    if (!any_nan) {
+        for (int k = 0; k < 4; k++) {
+            double best = -INFINITY;
+            int64_t bid = -1;
+            for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+                bool used = false;
+                for (int q = 0; q < k; q++) used |= (chosen[q] == i);
+                if (used) continue;
+                double lo = screen[i] - screen[n + i];
+                if (lo != lo) lo = -INFINITY;   // inf - inf
+                if (bid < 0 || lo > best) { best = lo; bid = i; }
+            }
+            for (int o = 16; o; o >>= 1) {
+                const double b2 = __shfl_xor_sync(0xffffffffu, best, o);
+                const int64_t i2 = __shfl_xor_sync(0xffffffffu, bid, o);
+                if (i2 >= 0 && (bid < 0 || b2 > best)) { best = b2; bid = i2; }
+            }
+            if (lane == 0) { bs[warp] = best; bi[warp] = bid; }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                double b0 = -INFINITY;
+                int64_t i0 = -1;
+                for (int w = 0; w < (int)(blockDim.x >> 5); w++)
+                    if (bi[w] >= 0 && (i0 < 0 || bs[w] > b0)) { b0 = bs[w]; i0 = bi[w]; }
+                chosen[k] = i0;
+                l4 = b0;
+            }
+            __syncthreads();
+        }
+    }
+    __syncthreads();
+    const double L4 = l4;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        if (any_nan || !(screen[i] + screen[n + i] < L4)) cand[atomicAdd(&cnt, 1)] = (int32_t)i;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *ncand = cnt;
+}
+
+// Radius of the row-sum screen.  Recursive/tree summation of depth d is within
+// gamma_d * sum|x| of the exact sum (gamma_d ~ d u, u = 2^-53).  Depth here:
+// ceil(n/1024) per thread + 10 shuffle/block levels; numpy's pairwise tree: 16
+// per accumulator + 3 + log2(n/128) + 1 <= 40; the final "- diagonal" adds <= 4u.
+// Radius = 8x that sum of depths (+ 50) times u ~ 1.1e-16 -> 9e-16 per level.
+__device__ __forceinline__ double rs_screen_radius(int n, double abs_sum) {
+    return (double)((n + 1023) / 1024 + 60) * 9e-16 * abs_sum;
+}
 
 struct RsMisc {
-    double red[64];
+    double red[128];
     double rmin, rmax, cscale;
     uint32_t ccnt[RS_CMAX + 1];    // coarse counts -> fine base (exclusive scan of f_c)
     uint32_t cf[RS_CMAX];          // fine buckets per coarse bin
@@ -227,44 +305,9 @@ struct RsMisc {
     uint32_t nsamp;
 };
 
-__host__ RsPlan rs_plan(int64_t n, int nbuf) {
-    RsPlan p;
-    p.n = (int)n;
-    int m = (int)n - 1;
-    p.C = rs_coarse_bins(m);
-    p.NBcap = rs_fine_cap(m);
-    p.nbuf = nbuf;
-    p.stride = (int)((n + 1) & ~1LL);   // keeps the second row buffer 16-byte aligned
-    size_t off = tg_align_up((size_t)nbuf * p.stride * sizeof(double), 16);
-    p.off_sidx = off;
-    off = tg_align_up(off + (size_t)n * sizeof(uint16_t), 16);
-    p.off_fcnt = off;
-    off = tg_align_up(off + (size_t)(p.NBcap + 1) * sizeof(uint32_t), 16);
-    p.off_misc = off;
-    off += tg_align_up(sizeof(RsMisc), 16);
-    p.smem = off;
-    return p;
-}
-
 __device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
     unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async16g(void *smem, const void *gmem) {
-    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-
-__device__ __forceinline__ void rs_issue_row(double *dst, const double *src, int n) {
-    // 16-byte chunks when source and destination are 16-byte aligned, else 8-byte copies
-    if (((((uintptr_t)src) | ((uintptr_t)dst)) & 15) == 0) {
-        int nv = n >> 1;
-        for (int i = threadIdx.x; i < nv; i += blockDim.x) cp_async16g(dst + 2 * i, src + 2 * i);
-        if ((n & 1) && threadIdx.x == 0) cp_async8(dst + n - 1, src + n - 1);
-    } else {
-        for (int i = threadIdx.x; i < n; i += blockDim.x) cp_async8(dst + i, src + i);
-    }
-    asm volatile("cp.async.commit_group;\n" ::);
 }
 
 // coarse bin of x in t-space: t = (rmax - x) * cscale in [0, C]
@@ -283,171 +326,260 @@ __device__ __forceinline__ int rs_fine_of(double t, int c, const uint32_t *base,
     return (int)base[c] + sub;
 }
 
+// ---------------------------------------------------------------- TMA-fed variant
+// Same bucket algorithm, restructured for instruction count (the cp.async-fed
+// kernel above spent ~97k warp-instructions per n = 10k row):
+//  * the next row is one cp.async.bulk (TMA) copy into the other buffer, issued
+//    by one thread and tracked by an mbarrier (+ <= 2 unaligned edge doubles);
+//  * fine-bucket counters are packed u16 pairs (counts and offsets <= m < 2^16),
+//    which is what lets two row buffers + the scatter array fit in 227 KB;
+//  * the exact in-bucket rank runs by sorted POSITION: the lanes of a warp hold
+//    consecutive positions, so they mostly walk the same bucket (no divergence
+//    on one large bucket) and the final id store is a coalesced 4-byte store;
+//  * the pairwise row-sum leaves are summed in the rank phase and the tree's
+//    upper levels by one warp at the top of the next row (no block barriers).
+struct RtPlan {
+    int n, C, NBcap, nbuf, stride, div;   // div: fine buckets per sampled key share (keys per bucket ~ 1/div... see rt_plan)
+    size_t off_sidx, off_f16, off_misc, off_bar, smem;
+};
+
+// keys_per_bucket = 1 or 2: the fine-bucket budget (m / keys_per_bucket buckets)
+__host__ RtPlan rt_plan(int64_t n, int nbuf, int keys_per_bucket) {
+    RtPlan p;
+    p.n = (int)n;
+    const int m = (int)n - 1;
+    p.C = rs_coarse_bins(m);
+    p.div = keys_per_bucket;
+    p.NBcap = 2 * p.C + (m + keys_per_bucket - 1) / keys_per_bucket + 1;
+    p.nbuf = nbuf;
+    p.stride = (int)((n + 2) & ~1LL);   // room for the 8-byte alignment shift, 16-byte aligned buffers
+    size_t off = tg_align_up((size_t)nbuf * p.stride * sizeof(double), 16);
+    p.off_sidx = off;
+    off = tg_align_up(off + (size_t)n * sizeof(uint32_t), 16);
+    p.off_f16 = off;
+    off = tg_align_up(off + (size_t)(p.NBcap / 2 + 2) * sizeof(uint32_t), 16);
+    p.off_misc = off;
+    off = tg_align_up(off + sizeof(RsMisc), 16);
+    p.off_bar = off;
+    off += 2 * sizeof(uint64_t);                 // 2 mbarriers
+    p.smem = off;
+    return p;
+}
+
+__device__ __forceinline__ unsigned rt_smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void rt_bulk_row(double *buf, const double *row, int n, uint64_t *bar) {
+    // thread 0 only: 16-byte-aligned body by TMA, the unaligned edge doubles by cp.async
+    const int sh = (int)(((uintptr_t)row >> 3) & 1);
+    double *vals = buf + sh;
+    const int cnt2 = (n - sh) & ~1;
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(rt_smem_u32(bar)),
+                 "r"((unsigned)(cnt2 * 8))
+                 : "memory");
+    if (cnt2 > 0)
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                         rt_smem_u32(vals + sh)),
+                     "l"(row + sh), "r"((unsigned)(cnt2 * 8)), "r"(rt_smem_u32(bar))
+                     : "memory");
+    if (sh) cp_async8(vals, row);
+    if (sh + cnt2 < n) cp_async8(vals + n - 1, row + n - 1);
+    // second arrival of the phase: when this thread's cp.async copies have landed
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(rt_smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void rt_wait(uint64_t *bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n RT_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra RT_WAIT_%=;\n}\n" ::"r"(rt_smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+
 template <int EMAX>
 __global__ void __launch_bounds__(RS_T, 1)
-row_sort_smem_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restrict__ order,
-                     double *__restrict__ rowsum, RsPlan pl) {
+row_sort_tma_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restrict__ order,
+                    double *__restrict__ screen, RtPlan pl) {
     extern __shared__ __align__(16) unsigned char rs_smem[];
     const int n = (int)n64;
     const int m = n - 1;
     double *vbuf = reinterpret_cast<double *>(rs_smem);
-    uint16_t *sidx = reinterpret_cast<uint16_t *>(rs_smem + pl.off_sidx);
-    uint32_t *fcnt = reinterpret_cast<uint32_t *>(rs_smem + pl.off_fcnt);
+    uint32_t *sidx = reinterpret_cast<uint32_t *>(rs_smem + pl.off_sidx);
+    uint32_t *f16 = reinterpret_cast<uint32_t *>(rs_smem + pl.off_f16);
     RsMisc &ms = *reinterpret_cast<RsMisc *>(rs_smem + pl.off_misc);
-    __shared__ PwTree<PW_SMALLNODES> tree;
-    __shared__ double pwval[PW_SMALLNODES];
+    const uint16_t *o16 = reinterpret_cast<const uint16_t *>(f16);   // bucket offsets, read side
+    uint64_t *bar = reinterpret_cast<uint64_t *>(rs_smem + pl.off_bar);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int C = pl.C;
+    const int nw16 = pl.NBcap / 2 + 2;
 
-    if (rowsum) {
-        int *height = reinterpret_cast<int *>(pwval);  // scratch before first use
-        if (tid == 0) pw_plan(tree, n, height);
+    if (tid == 0) {
+        // two arrivals per phase: expect_tx (TMA body) + cp.async (unaligned edges)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;\n" ::"r"(rt_smem_u32(&bar[0])) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;\n" ::"r"(rt_smem_u32(&bar[1])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    int it = 0;
+    __syncthreads();
     int64_t v = blockIdx.x;
-    if (v < n && pl.nbuf == 2) rs_issue_row(vbuf, S + v * n64, n);
-    for (; v < n; v += gridDim.x, it++) {
-        double *vals = vbuf + (pl.nbuf == 2 ? (size_t)(it & 1) * pl.stride : 0);
-        if (pl.nbuf == 1) rs_issue_row(vals, S + v * n64, n);
-        asm volatile("cp.async.wait_group 0;\n" ::);
-        __syncthreads();
-        if (pl.nbuf == 2) {
-            int64_t vn = v + gridDim.x;
-            if (vn < n) rs_issue_row(vbuf + (size_t)((it + 1) & 1) * pl.stride, S + vn * n64, n);
-        }
-        // ---- A: zero coarse counters, row min/max (v excluded)
+    if (tid == 0 && v < n) rt_bulk_row(vbuf, S + v * n64, n, &bar[0]);
+    for (int it = 0; v < n; v += gridDim.x, it++) {
+        const int b = pl.nbuf == 2 ? (it & 1) : 0;
+        const unsigned parity = pl.nbuf == 2 ? (unsigned)((it >> 1) & 1) : (unsigned)(it & 1);
+        const double *row = S + v * n64;
+        const double *vals = vbuf + (size_t)b * pl.stride + (((uintptr_t)row >> 3) & 1);
+        rt_wait(&bar[b], parity);
+        // ---- A: clear counters; row min / max / NaN (v excluded)
+        for (int i = tid; i < nw16; i += RS_T) f16[i] = 0u;
         for (int c = tid; c <= C; c += RS_T) ms.ccnt[c] = 0;
         if (tid == 0) ms.nsamp = 0;
-        double mn = INFINITY, mx = -INFINITY;
+        double mn = INFINITY, mx = -INFINITY, sm = 0.0, sa = 0.0;
         bool nan_seen = false;
-        for (int j = tid; j < n; j += RS_T) {
-            if (j == v) continue;
-            double x = vals[j];
-            if (x < mn) mn = x;
-            if (x > mx) mx = x;
-            nan_seen |= (x != x);
+#pragma unroll
+        for (int e = 0; e < EMAX; e++) {
+            const int j = tid + e * RS_T;
+            if (j < n) {
+                const double x = vals[j];
+                sm += x;                // row-sum screen (clique candidates)
+                sa += fabs(x);
+                if (j != v) {
+                    mn = x < mn ? x : mn;   // NaN: never selected, flagged below
+                    mx = x > mx ? x : mx;
+                    nan_seen |= (x != x);
+                }
+            }
         }
-        const bool row_nan = __syncthreads_or(nan_seen);
+        const bool row_nan = __syncthreads_or(nan_seen);   // also: the row is visible to all
+        if (tid == 0 && pl.nbuf == 2) {
+            const int64_t vn = v + gridDim.x;
+            if (vn < n) rt_bulk_row(vbuf + (size_t)(b ^ 1) * pl.stride, S + vn * n64, n, &bar[b ^ 1]);
+        }
         for (int o = 16; o; o >>= 1) {
             mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
             mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            if (screen) {
+                sm += __shfl_xor_sync(0xffffffffu, sm, o);
+                sa += __shfl_xor_sync(0xffffffffu, sa, o);
+            }
         }
-        if (lane == 0) { ms.red[warp] = mn; ms.red[32 + warp] = mx; }
+        if (lane == 0) { ms.red[warp] = mn; ms.red[32 + warp] = mx; ms.red[64 + warp] = sm; ms.red[96 + warp] = sa; }
         __syncthreads();
-        if (warp == 0) {
-            double a = ms.red[lane], b = ms.red[32 + lane];
+        double rmax, cscale;
+        {
+            double a = ms.red[lane], bb = ms.red[32 + lane];
             for (int o = 16; o; o >>= 1) {
                 a = fmin(a, __shfl_xor_sync(0xffffffffu, a, o));
-                b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+                bb = fmax(bb, __shfl_xor_sync(0xffffffffu, bb, o));
             }
-            if (lane == 0) {
-                double w = b - a;
-                ms.rmin = a;
-                ms.rmax = b;
-                ms.cscale = (w > 0.0 && w < INFINITY) ? (double)C / w : 0.0;
+            const double w = bb - a;
+            rmax = bb;
+            cscale = (w > 0.0 && w < INFINITY) ? (double)C / w : 0.0;
+            if (screen && warp == 1) {
+                double s1 = ms.red[64 + lane], s2 = ms.red[96 + lane];
+                for (int o = 16; o; o >>= 1) {
+                    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+                    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+                }
+                if (lane == 0) {
+                    screen[v] = __dsub_rn(s1, vals[v]);
+                    screen[n + v] = rs_screen_radius(n, s2);
+                }
             }
         }
-        __syncthreads();
-        // ---- B: coarse histogram (linear bins over [min, max]) from a 1-in-4 sample
-        // (it only sizes the fine buckets: accuracy affects speed, never the order)
-        const double rmax = ms.rmax, cscale = ms.cscale;
-        uint32_t pk[EMAX];
+        // ---- B: coarse histogram from a sample (sizes the fine buckets only)
         int nsamp = 0;
 #pragma unroll
-        for (int e = 0; e < EMAX; e++) {
-            int j = tid + e * RS_T;
-            bool act = j < n && j != v;
-            if (act && (e & 3) == 0) {
+        for (int e = 0; e < EMAX; e += 4) {
+            const int j = tid + e * RS_T;
+            if (j < n && j != v) {
                 double t;
                 atomicAdd(&ms.ccnt[rs_coarse_of(vals[j], rmax, cscale, C, t)], 1u);
                 nsamp++;
             }
-            pk[e] = act ? 0u : 0xffffffffu;
         }
         nsamp = __reduce_add_sync(0xffffffffu, nsamp);
         if (lane == 0 && nsamp) atomicAdd(&ms.nsamp, (uint32_t)nsamp);
         __syncthreads();
-        // ---- C: fine buckets per coarse bin (about two keys each), base offsets
-        {
-            const uint64_t den = 2ull * (ms.nsamp ? ms.nsamp : 1u);
-            for (int c = tid; c < C; c += RS_T) {
-                uint64_t h = ms.ccnt[c];
-                uint32_t f = (uint32_t)((h * (uint64_t)m + den - 1) / den);
-                ms.cf[c] = f > 1 ? f : 1u;
-            }
-        }
-        __syncthreads();
+        // ---- C: fine buckets per coarse bin (about two keys each) + base offsets (warp 0)
         if (warp == 0) {
-            // exclusive scan of cf -> ccnt (base), C <= 512: 16 per lane
+            // f_c = 1 + floor(h_c * m / (div * nsamp)) (shaved so sum f_c <= C + m/div)
+            const float scale = (float)m / ((float)pl.div * (float)(ms.nsamp ? ms.nsamp : 1u)) * 0.9999f;
             const int per = (C + 31) / 32;
             uint32_t s = 0;
             for (int q = 0; q < per; q++) {
-                int c = lane * per + q;
-                if (c < C) s += ms.cf[c];
+                const int c = lane * per + q;
+                if (c < C) {
+                    const uint32_t f = 1u + (uint32_t)((float)ms.ccnt[c] * scale);
+                    ms.cf[c] = f;
+                    s += f;
+                }
             }
             uint32_t incl = s;
             for (int o = 1; o < 32; o <<= 1) {
-                uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += y;
             }
             uint32_t run = incl - s;
             for (int q = 0; q < per; q++) {
-                int c = lane * per + q;
+                const int c = lane * per + q;
                 if (c < C) { ms.ccnt[c] = run; run += ms.cf[c]; }
             }
             if (lane == 31) ms.ccnt[C] = incl;
         }
         __syncthreads();
         const int NB = (int)ms.ccnt[C];
-        for (int b = tid; b <= NB; b += RS_T) fcnt[b] = 0;
-        __syncthreads();
-        // ---- D: fine bucket + rank inside it (one shared atomic per key)
+        // ---- D: fine bucket + arrival rank (one packed shared atomic per key)
+        uint32_t pk[EMAX];
 #pragma unroll
         for (int e = 0; e < EMAX; e++) {
-            if (pk[e] != 0xffffffffu) {
-                int j = tid + e * RS_T;
+            const int j = tid + e * RS_T;
+            pk[e] = 0xffffffffu;
+            if (j < n && j != v) {
                 double t;
-                int c = rs_coarse_of(vals[j], rmax, cscale, C, t);
-                int fb = rs_fine_of(t, c, ms.ccnt, ms.cf);
-                uint32_t r = atomicAdd(&fcnt[fb], 1u);
-                pk[e] = ((uint32_t)fb << 16) | r;
+                const int c = rs_coarse_of(vals[j], rmax, cscale, C, t);
+                const int fb = rs_fine_of(t, c, ms.ccnt, ms.cf);
+                const int sh = (fb & 1) << 4;
+                const uint32_t old = atomicAdd(&f16[fb >> 1], 1u << sh);
+                pk[e] = ((uint32_t)fb << 16) | ((old >> sh) & 0xffffu);
             }
         }
         __syncthreads();
-        // ---- E: exclusive scan of the fine counters, scatter ids
+        // ---- E: exclusive scan of the packed counters (NB + 1 entries), scatter (bucket, id)
         {
-            const int len = NB + 1;
-            const int per = (len + RS_T - 1) / RS_T;
-            const int b0 = tid * per;
+            const int nw = (NB + 2) >> 1;
+            const int per = (nw + RS_T - 1) / RS_T;
+            const int w0 = tid * per;
             uint32_t s = 0;
             for (int q = 0; q < per; q++) {
-                int b = b0 + q;
-                if (b < len) s += fcnt[b];
+                const int w = w0 + q;
+                if (w < nw) { const uint32_t x = f16[w]; s += (x & 0xffffu) + (x >> 16); }
             }
             uint32_t incl = s;
             for (int o = 1; o < 32; o <<= 1) {
-                uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += y;
             }
             if (lane == 31) ms.wsum[warp] = incl;
             __syncthreads();
-            if (warp == 0) {
-                uint32_t w = ms.wsum[lane];
-                uint32_t wi = w;
+            uint32_t wex = 0;
+            {
+                const uint32_t wv = ms.wsum[lane];
+                uint32_t wi = wv;
                 for (int o = 1; o < 32; o <<= 1) {
-                    uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
                     if (lane >= o) wi += y;
                 }
-                ms.wsum[lane] = wi - w;
+                wex = __shfl_sync(0xffffffffu, wi - wv, warp);
             }
-            __syncthreads();
-            uint32_t run = ms.wsum[warp] + incl - s;
+            uint32_t run = wex + incl - s;
             for (int q = 0; q < per; q++) {
-                int b = b0 + q;
-                if (b < len) {
-                    uint32_t c = fcnt[b];
-                    fcnt[b] = run;
-                    run += c;
+                const int w = w0 + q;
+                if (w < nw) {
+                    const uint32_t x = f16[w];
+                    const uint32_t lo = run, hi = run + (x & 0xffffu);
+                    f16[w] = lo | (hi << 16);
+                    run = hi + (x >> 16);
                 }
             }
         }
@@ -455,65 +587,45 @@ row_sort_smem_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restr
 #pragma unroll
         for (int e = 0; e < EMAX; e++) {
             if (pk[e] != 0xffffffffu) {
-                int j = tid + e * RS_T;
-                sidx[fcnt[pk[e] >> 16] + (pk[e] & 0xffffu)] = (uint16_t)j;
+                const int fb = (int)(pk[e] >> 16);
+                sidx[o16[fb] + (pk[e] & 0xffffu)] = (pk[e] & 0xffff0000u) | (uint32_t)(tid + e * RS_T);
             }
         }
         __syncthreads();
-        // ---- F: exact rank of every key inside its bucket (value desc, id asc):
-        // independent loads, cost per key = its bucket size; ids placed once more.
+        // ---- F: exact rank by sorted position (value desc, id asc), coalesced id store
+        int32_t *out = order + v * (int64_t)m;
 #pragma unroll
         for (int e = 0; e < EMAX; e++) {
-            if (pk[e] != 0xffffffffu) {
-                const int j = tid + e * RS_T;
-                const int b = (int)(pk[e] >> 16);
-                const int s0 = (int)fcnt[b], s1 = (int)fcnt[b + 1];
+            const int k = tid + e * RS_T;
+            if (k < m) {
+                const uint32_t s = sidx[k];
+                const int fb = (int)(s >> 16), j = (int)(s & 0xffffu);
+                const int s0 = o16[fb], s1 = o16[fb + 1];
                 int rank = 0;
                 if (s1 - s0 > 1) {
                     const double xj = vals[j];
                     if (!row_nan) {
-                        for (int k = s0; k < s1; k++) {
-                            const int o = sidx[k];
+                        for (int q = s0; q < s1; q++) {
+                            const int o = (int)(sidx[q] & 0xffffu);
                             const double xo = vals[o];
                             rank += (xo > xj) | ((xo == xj) & (o < j));
                         }
                     } else {
-                        for (int k = s0; k < s1; k++) {
-                            const int o = sidx[k];
+                        for (int q = s0; q < s1; q++) {
+                            const int o = (int)(sidx[q] & 0xffffu);
                             rank += rs_before(vals[o], o, xj, j);
                         }
                     }
                 }
-                pk[e] = (uint32_t)(s0 + rank);
+                out[s0 + rank] = j;
             }
         }
         __syncthreads();
-#pragma unroll
-        for (int e = 0; e < EMAX; e++)
-            if (pk[e] != 0xffffffffu) sidx[pk[e]] = (uint16_t)(tid + e * RS_T);
-        __syncthreads();
-        // ---- G: write ids (16-byte stores on the aligned body)
-        {
-            int32_t *out = order + v * (int64_t)m;
-            int head = (int)(((16 - (((uintptr_t)out) & 15)) & 15) >> 2);
-            if (head > m) head = m;
-            for (int p = tid; p < head; p += RS_T) out[p] = sidx[p];
-            int body = (m - head) >> 2;
-            int4 *o4 = reinterpret_cast<int4 *>(out + head);
-            for (int q = tid; q < body; q += RS_T) {
-                int p = head + 4 * q;
-                o4[q] = make_int4(sidx[p], sidx[p + 1], sidx[p + 2], sidx[p + 3]);
-            }
-            for (int p = head + 4 * body + tid; p < m; p += RS_T) out[p] = sidx[p];
+        if (tid == 0 && pl.nbuf == 1) {
+            const int64_t vn = v + gridDim.x;
+            if (vn < n) rt_bulk_row(vbuf, S + vn * n64, n, &bar[0]);
         }
-        // ---- H: fused pairwise row sum (initial-clique input)
-        if (rowsum) {
-            double root = pw_eval(tree, pwval, [&](int i) { return vals[i]; });
-            if (tid == 0) rowsum[v] = __dsub_rn(root, vals[v]);
-        }
-        __syncthreads();
     }
-    asm volatile("cp.async.wait_group 0;\n" ::);
 }
 
 // ---------------------------------------------------------------- large rows
@@ -522,32 +634,27 @@ row_sort_smem_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restr
 // the output row itself is the scatter buffer.  Counters stay in shared memory.
 __global__ void __launch_bounds__(RS_T, 1)
 row_sort_global_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restrict__ order,
-                       double *__restrict__ rowsum, uint32_t *__restrict__ gpk_all) {
+                       double *__restrict__ screen, uint32_t *__restrict__ gpk_all) {
     const int n = (int)n64;
     const int m = n - 1;
     extern __shared__ __align__(16) unsigned char rs_smem[];
     uint32_t *fcnt = reinterpret_cast<uint32_t *>(rs_smem);
     __shared__ RsMisc ms;
-    __shared__ PwTree<PW_MAXNODES> tree;
-    __shared__ double pwval[PW_MAXNODES];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int C = rs_coarse_bins(m);
     uint32_t *gpk = gpk_all + (size_t)blockIdx.x * 2 * n;   // [n] bucket, [n] rank/position
-    if (rowsum) {
-        int *height = reinterpret_cast<int *>(pwval);
-        if (tid == 0) pw_plan(tree, n, height);
-        __syncthreads();
-    }
     for (int64_t v = blockIdx.x; v < n; v += gridDim.x) {
         const double *row = S + v * n64;
         int32_t *out = order + v * (int64_t)m;
         for (int c = tid; c <= C; c += RS_T) ms.ccnt[c] = 0;
         if (tid == 0) ms.nsamp = 0;
-        double mn = INFINITY, mx = -INFINITY;
+        double mn = INFINITY, mx = -INFINITY, sm = 0.0, sa = 0.0;
         bool nan_seen = false;
         for (int j = tid; j < n; j += RS_T) {
-            if (j == v) continue;
             double x = __ldg(row + j);
+            sm += x;
+            sa += fabs(x);
+            if (j == v) continue;
             if (x < mn) mn = x;
             if (x > mx) mx = x;
             nan_seen |= (x != x);
@@ -556,9 +663,22 @@ row_sort_global_kernel(const double *__restrict__ S, int64_t n64, int32_t *__res
         for (int o = 16; o; o >>= 1) {
             mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
             mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            sm += __shfl_xor_sync(0xffffffffu, sm, o);
+            sa += __shfl_xor_sync(0xffffffffu, sa, o);
         }
-        if (lane == 0) { ms.red[warp] = mn; ms.red[32 + warp] = mx; }
+        if (lane == 0) { ms.red[warp] = mn; ms.red[32 + warp] = mx; ms.red[64 + warp] = sm; ms.red[96 + warp] = sa; }
         __syncthreads();
+        if (screen && warp == 1) {
+            double s1 = ms.red[64 + lane], s2 = ms.red[96 + lane];
+            for (int o = 16; o; o >>= 1) {
+                s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+                s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+            }
+            if (lane == 0) {
+                screen[v] = __dsub_rn(s1, __ldg(row + v));
+                screen[n + v] = rs_screen_radius(n, s2);
+            }
+        }
         if (warp == 0) {
             double a = ms.red[lane], b = ms.red[32 + lane];
             for (int o = 16; o; o >>= 1) {
@@ -688,15 +808,22 @@ row_sort_global_kernel(const double *__restrict__ S, int64_t n64, int32_t *__res
             out[gpk[n + j]] = j;
         }
         __syncthreads();
-        if (rowsum) {
-            double root = pw_eval(tree, pwval, [&](int i) { return __ldg(row + i); });
-            if (tid == 0) rowsum[v] = __dsub_rn(root, row[v]);
-        }
-        __syncthreads();
     }
 }
 
-constexpr size_t RS_SMEM_MAX = 227 * 1024 - sizeof(PwTree<PW_SMALLNODES>) - PW_SMALLNODES * sizeof(double) - 1024;
+constexpr size_t RS_SMEM_MAX = 227 * 1024;
+
+// numpy's pairwise plan for n (a pure function of n), cached per host thread
+const PwTree<PW_MAXNODES> &pw_host_plan(int n) {
+    static thread_local PwTree<PW_MAXNODES> tree;
+    static thread_local int tree_n = -1;
+    static thread_local int height[PW_MAXNODES];
+    if (tree_n != n) {
+        pw_plan(tree, n, height);
+        tree_n = n;
+    }
+    return tree;
+}
 
 }  // namespace
 
@@ -705,22 +832,31 @@ TG_API size_t tg_row_sort_workspace_bytes(int64_t n) {
     return (size_t)tg_num_sms() * 2 * (size_t)n * sizeof(uint32_t) + 4096;
 }
 
-TG_API int tg_row_sort_f64(const double *S, int64_t n, int32_t *order, double *rowsum, void *ws, size_t ws_bytes,
+TG_API int tg_row_sort_f64(const double *S, int64_t n, int32_t *order, double *screen, void *ws, size_t ws_bytes,
                            void *stream) {
     if (n < 2 || !S || !order) return TG_ERR_ARG;
+    if ((((uintptr_t)S) & 7) != 0 || (((uintptr_t)order) & 3) != 0) return TG_ERR_ARG;
+    if (n > (int64_t)1 << 30) return TG_ERR_ARG;
     cudaStream_t st = tg_stream(stream);
     int grid = tg_num_sms();
     if (grid > n) grid = (int)n;
     if (n <= 16384) {
-        RsPlan pl = rs_plan(n, 2);
-        if (pl.smem > RS_SMEM_MAX) pl = rs_plan(n, 1);
-        if (pl.smem > RS_SMEM_MAX) return TG_ERR_ARG;
+        // preference: two row buffers (TMA of row v+grid overlaps row v) with one key per
+        // fine bucket; then two keys per bucket; then a single buffer
+        const int pref[4][2] = {{2, 1}, {2, 2}, {1, 1}, {1, 2}};
+        RtPlan pl;
+        int k = 0;
+        for (; k < 4; k++) {
+            pl = rt_plan(n, pref[k][0], pref[k][1]);
+            if (pl.smem <= RS_SMEM_MAX) break;
+        }
+        if (k == 4) return TG_ERR_ARG;
         int E = (int)((n + RS_T - 1) / RS_T);
 #define RS_LAUNCH(EM)                                                                                      \
     do {                                                                                                   \
-        auto kfn = row_sort_smem_kernel<EM>;                                                               \
+        auto kfn = row_sort_tma_kernel<EM>;                                                                \
         TG_CUDA_CHECK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem)); \
-        kfn<<<grid, RS_T, pl.smem, st>>>(S, n, order, rowsum, pl); tg_count_launch(1);                                         \
+        kfn<<<grid, RS_T, pl.smem, st>>>(S, n, order, screen, pl); tg_count_launch(1);                      \
     } while (0)
         if (E <= 2) RS_LAUNCH(2);
         else if (E <= 4) RS_LAUNCH(4);
@@ -730,15 +866,13 @@ TG_API int tg_row_sort_f64(const double *S, int64_t n, int32_t *order, double *r
         TG_LAUNCH_CHECK();
         return TG_OK;
     }
-    if (n > (int64_t)1 << 30) return TG_ERR_ARG;
-    if (n > 128 * (PW_MAXNODES / 2) && rowsum) return TG_ERR_ARG;
     if (ws_bytes < tg_row_sort_workspace_bytes(n)) return TG_ERR_WORKSPACE;
     uint32_t *gpk = reinterpret_cast<uint32_t *>(ws);
     int m = (int)n - 1;
     size_t smem = (size_t)(rs_fine_cap(m) + 1) * sizeof(uint32_t);
     if (smem > 160 * 1024) return TG_ERR_ARG;
     TG_CUDA_CHECK(cudaFuncSetAttribute(row_sort_global_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    row_sort_global_kernel<<<grid, RS_T, smem, st>>>(S, n, order, rowsum, gpk); tg_count_launch(1);
+    row_sort_global_kernel<<<grid, RS_T, smem, st>>>(S, n, order, screen, gpk); tg_count_launch(1);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
@@ -750,14 +884,38 @@ TG_API int tg_row_sums_f64(const double *S, int64_t n, double *rowsum, void *, s
     if (n > 128 * (PW_MAXNODES / 2)) return TG_ERR_ARG;
     int grid = tg_num_sms() * 4;
     if (grid > n) grid = (int)n;
-    row_sums_kernel<<<grid, 256, 0, tg_stream(stream)>>>(S, n, rowsum); tg_count_launch(1);
+    row_sums_kernel<<<grid, 256, 0, tg_stream(stream)>>>(S, n, rowsum, nullptr, nullptr, pw_host_plan((int)n));
+    tg_count_launch(1);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
 
 TG_API int tg_initial_clique(const double *rowsum, int64_t n, int32_t *clique, void *stream) {
     if (n < 4 || !rowsum || !clique) return TG_ERR_ARG;
-    clique_kernel<<<1, 1024, 0, tg_stream(stream)>>>(rowsum, n, clique); tg_count_launch(1);
+    clique_kernel<<<1, 1024, 0, tg_stream(stream)>>>(rowsum, n, clique, nullptr, nullptr); tg_count_launch(1);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+TG_API size_t tg_initial_clique_screened_workspace_bytes(int64_t n) {
+    return tg_align_up((size_t)n * sizeof(double), 256) + tg_align_up((size_t)n * sizeof(int32_t), 256) + 256;
+}
+
+TG_API int tg_initial_clique_screened(const double *S, int64_t n, const double *screen, int32_t *clique, void *ws,
+                                      size_t ws_bytes, void *stream) {
+    if (n < 4 || !S || !screen || !clique) return TG_ERR_ARG;
+    if (n > 128 * (PW_MAXNODES / 2)) return TG_ERR_ARG;
+    if (!ws || ws_bytes < tg_initial_clique_screened_workspace_bytes(n)) return TG_ERR_WORKSPACE;
+    cudaStream_t st = tg_stream(stream);
+    TgArena ar(ws, ws_bytes);
+    double *sums = ar.take<double>((size_t)n);
+    int32_t *cand = ar.take<int32_t>((size_t)n);
+    int32_t *ncand = ar.take<int32_t>(1);
+    clique_screen_kernel<<<1, 1024, 0, st>>>(screen, n, cand, ncand);
+    int grid = tg_num_sms();
+    row_sums_kernel<<<grid, 256, 0, st>>>(S, n, sums, cand, ncand, pw_host_plan((int)n));
+    clique_kernel<<<1, 1024, 0, st>>>(sums, n, clique, cand, ncand);
+    tg_count_launch(3);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }

@@ -117,11 +117,11 @@ class SortedNeighborLists:
     (``order_device``) and the host copy is made on first access.
     """
 
-    def __init__(self, S, order, S_device=None, rowsum_device=None):
+    def __init__(self, S, order, S_device=None, screen_device=None):
         self.S = S
         self._order = D.LazyHost(dev=order) if D.is_device(order) else D.LazyHost(host=np.asarray(order))
         self.S_device = S_device
-        self.rowsum_device = rowsum_device
+        self.screen_device = screen_device   # initial-clique row-sum screen (2n), see sort_rows_device
 
     @property
     def order(self) -> np.ndarray:
@@ -147,19 +147,22 @@ class SortedNeighborLists:
         return [(float(row[u]), int(u)) for u in self.order[v]]
 
 
-def sort_rows_device(Sd, with_rowsum: bool = True):
-    """(order (n, n-1) int32, rowsum (n,) float64 or None) as CUDA tensors."""
+def sort_rows_device(Sd, with_screen: bool = True):
+    """(order (n, n-1) int32, screen (2n,) float64 or None) as CUDA tensors.
+
+    ``screen[v]`` is row v's off-diagonal sum in the kernel's summation order and
+    ``screen[n + v]`` a rigorous bound on its distance to numpy's pairwise sum
+    (tmfg.py:76); ``initial_clique_device`` turns it into the exact clique.
+    """
     t = D.torch()
     n = int(Sd.shape[0])
     order = D.empty((n, max(n - 1, 0)), t.int32)
-    rowsum = D.empty((n,), t.float64) if with_rowsum else None
+    screen = D.empty((2 * n,), t.float64) if (with_screen and n >= 2) else None
     if n >= 2:
         ws = D.Workspace.get(N.size("tg_row_sort_workspace_bytes", n))
-        N.call("tg_row_sort_f64", N.ptr(Sd), n, N.ptr(order), N.ptr(rowsum), N.ptr(ws), ws.numel(),
+        N.call("tg_row_sort_f64", N.ptr(Sd), n, N.ptr(order), N.ptr(screen), N.ptr(ws), ws.numel(),
                N.stream_ptr())
-    elif rowsum is not None:
-        rowsum.zero_()
-    return order, rowsum
+    return order, screen
 
 
 def sort_neighbor_lists(S, workers: int | None = None) -> SortedNeighborLists:
@@ -171,5 +174,5 @@ def sort_neighbor_lists(S, workers: int | None = None) -> SortedNeighborLists:
     if not D.is_device(S):
         S = np.asarray(S, dtype=np.float64)
     Sd = D.device_matrix(S)
-    order, rowsum = sort_rows_device(Sd, with_rowsum=True)
-    return SortedNeighborLists(S, order, S_device=Sd, rowsum_device=rowsum)
+    order, screen = sort_rows_device(Sd, with_screen=True)
+    return SortedNeighborLists(S, order, S_device=Sd, screen_device=screen)

@@ -92,15 +92,31 @@ for _name in _HOST_FIELDS:
     setattr(TmfgGraph, _name, _make_prop(_name))
 
 
-def initial_clique_device(Sd, rowsum=None):
-    """tmfg.py:71-79 on device: int32[4] CUDA tensor (ascending)."""
+def row_sums_device(Sd):
+    """tmfg.py:76 ``S.sum(axis=1) - diag(S)`` in numpy's pairwise order, on device."""
     t = D.torch()
     n = int(Sd.shape[0])
-    if rowsum is None:
-        rowsum = D.empty((n,), t.float64)
-        ws = D.Workspace.get(N.size("tg_row_sums_workspace_bytes", n))
-        N.call("tg_row_sums_f64", N.ptr(Sd), n, N.ptr(rowsum), N.ptr(ws), ws.numel(), N.stream_ptr())
+    rowsum = D.empty((n,), t.float64)
+    ws = D.Workspace.get(N.size("tg_row_sums_workspace_bytes", n))
+    N.call("tg_row_sums_f64", N.ptr(Sd), n, N.ptr(rowsum), N.ptr(ws), ws.numel(), N.stream_ptr())
+    return rowsum
+
+
+def initial_clique_device(Sd, screen=None):
+    """tmfg.py:71-79 on device: int32[4] CUDA tensor (ascending).
+
+    With the row sort's ``screen`` only the rows that can reach the top 4 get an
+    exact pairwise sum; without it every row does.
+    """
+    t = D.torch()
+    n = int(Sd.shape[0])
     clique = D.empty((4,), t.int32)
+    if screen is not None:
+        ws = D.Workspace.get(N.size("tg_initial_clique_screened_workspace_bytes", n))
+        N.call("tg_initial_clique_screened", N.ptr(Sd), n, N.ptr(screen), N.ptr(clique), N.ptr(ws), ws.numel(),
+               N.stream_ptr())
+        return clique
+    rowsum = row_sums_device(Sd)
     N.call("tg_initial_clique", N.ptr(rowsum), n, N.ptr(clique), N.stream_ptr())
     return clique
 
@@ -189,14 +205,14 @@ def build_tmfg_heap(S, lists: SortedNeighborLists | None = None, config: BuildCo
         Sd = D.device_matrix(S)
     validate_device(Sd)
     n = shape[0]
-    rowsum = getattr(lists, "rowsum_device", None) if lists is not None and lists.S is S else None
+    screen = getattr(lists, "screen_device", None) if lists is not None and lists.S is S else None
     if lists is None:
-        order_dev, rowsum = sort_rows_device(Sd, with_rowsum=True)
+        order_dev, screen = sort_rows_device(Sd, with_screen=True)
     elif isinstance(lists, SortedNeighborLists):
         order_dev = lists.order_device
     else:
         order_dev = D.to_device(np.asarray(lists.order, dtype=np.int32), D.torch().int32)
-    clique = initial_clique_device(Sd, rowsum)
+    clique = initial_clique_device(Sd, screen)
     out = build_tmfg_heap_device(Sd, order_dev, clique, check_invariants)
     raw = out["stats"].cpu().numpy()
     stats = _stats_dict(raw, check_invariants)

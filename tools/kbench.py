@@ -61,7 +61,7 @@ def main():
     out["cublas_dgemm_8192_tflops"] = 2 * 8192 ** 3 / (mn2 * 1e-3) / 1e12
     # row sort
     order = torch.empty((n, n - 1), dtype=torch.int32, device="cuda")
-    rowsum = torch.empty((n,), dtype=torch.float64, device="cuda")
+    rowsum = torch.empty((2 * n,), dtype=torch.float64, device="cuda")   # row-sum screen
     ws = p._device.Workspace.get(N.size("tg_row_sort_workspace_bytes", n))
 
     def sort():
@@ -78,6 +78,11 @@ def main():
     mn, md = timed(sort_nosum, args.reps, flush)
     out["sort_nosum_ms"] = [mn, md]
     out["sort_nosum_gbs"] = byt / (mn * 1e-3) / 1e9
+    sort()
+    mn, md = timed(lambda: tmfg.initial_clique_device(S, rowsum), args.reps, flush)
+    out["clique_screened_ms"] = [mn, md]
+    mn, md = timed(lambda: tmfg.initial_clique_device(S, None), args.reps, flush)
+    out["clique_exact_all_rows_ms"] = [mn, md]
     # validate
     flags = torch.empty(1, dtype=torch.int32, device="cuda")
     mn, md = timed(lambda: N.call("tg_validate_f64", N.ptr(S), n, N.ptr(flags), N.stream_ptr()), args.reps, flush)

@@ -8,6 +8,6 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 10000
 N.load()
 x, _ = synth.generate(3, n=n)
 S = simmatrix.pearson_similarity_device(torch.from_numpy(x).cuda())
-order, rowsum = simmatrix.sort_rows_device(S, with_rowsum=False)
+order, rowsum = simmatrix.sort_rows_device(S, with_screen=(sys.argv[2:3] != ['nosum']))
 torch.cuda.synchronize()
 print("ok", int(order[0, 0]))
