@@ -25,6 +25,8 @@
 // variant below (same algorithm, the row and the scatter buffer live in L2).
 #include "common.cuh"
 
+#include <cmath>
+
 namespace {
 
 constexpr int RS_T = 1024;
@@ -326,43 +328,65 @@ __device__ __forceinline__ int rs_fine_of(double t, int c, const uint32_t *base,
     return (int)base[c] + sub;
 }
 
-// ---------------------------------------------------------------- TMA-fed variant
-// Same bucket algorithm, restructured for instruction count (the cp.async-fed
-// kernel above spent ~97k warp-instructions per n = 10k row):
-//  * the next row is one cp.async.bulk (TMA) copy into the other buffer, issued
-//    by one thread and tracked by an mbarrier (+ <= 2 unaligned edge doubles);
-//  * fine-bucket counters are packed u16 pairs (counts and offsets <= m < 2^16),
-//    which is what lets two row buffers + the scatter array fit in 227 KB;
-//  * the exact in-bucket rank runs by sorted POSITION: the lanes of a warp hold
-//    consecutive positions, so they mostly walk the same bucket (no divergence
-//    on one large bucket) and the final id store is a coalesced 4-byte store;
-//  * the pairwise row-sum leaves are summed in the rank phase and the tree's
-//    upper levels by one warp at the top of the next row (no block barriers).
+// ---------------------------------------------------------------- TMA-fed kernel
+// One CTA (1024 threads) per SM, persistent over rows v = blockIdx.x + k*grid.
+//  * row v+grid is one cp.async.bulk (TMA) copy into the other row buffer,
+//    issued by one thread and tracked by an mbarrier (+ <= 2 unaligned edge
+//    doubles by cp.async, which arrive on the same mbarrier);
+//  * min / max (rounded outward to float for cheap reductions) define C linear
+//    coarse bins; a sampled histogram sizes each bin's share of the fine buckets
+//    (~fs buckets per key, fs sized to fill shared memory), each bin split
+//    linearly again: bucket ids are monotone in the value, equal values share one;
+//  * one packed-u16 shared atomic per key gives its bucket and arrival rank, a
+//    block scan the bucket offsets; (bucket, id) pairs are scattered;
+//  * the exact rank inside a bucket (value desc, id asc) runs by sorted POSITION:
+//    the lanes of a warp hold consecutive positions, so bucket walks mostly
+//    coincide and the id store is coalesced;
+//  * the same pass writes the initial-clique row-sum screen (sum, bound).
 struct RtPlan {
-    int n, C, NBcap, nbuf, stride, div;   // div: fine buckets per sampled key share (keys per bucket ~ 1/div... see rt_plan)
-    size_t off_sidx, off_f16, off_misc, off_bar, smem;
+    int n, C, NBcap, nbuf, stride;
+    float fs;   // fine buckets per key
+    size_t off_sidx, off_f16, off_cinfo, off_misc, off_bar, smem;
 };
 
-// keys_per_bucket = 1 or 2: the fine-bucket budget (m / keys_per_bucket buckets)
-__host__ RtPlan rt_plan(int64_t n, int nbuf, int keys_per_bucket) {
+struct RtCoarse {   // per coarse bin after the allocation phase
+    double f;       // fine buckets in the bin (as double)
+    int base, last; // first / last fine bucket id
+};
+
+struct RtMisc {
+    float rmn[32], rmx[32];
+    double rsum[32], rabs[32];
+    uint32_t wsum[32];
+    uint32_t nsamp;
+};
+
+__host__ RtPlan rt_plan(int64_t n, int nbuf, size_t smem_max) {
     RtPlan p;
     p.n = (int)n;
     const int m = (int)n - 1;
     p.C = rs_coarse_bins(m);
-    p.div = keys_per_bucket;
-    p.NBcap = 2 * p.C + (m + keys_per_bucket - 1) / keys_per_bucket + 1;
     p.nbuf = nbuf;
     p.stride = (int)((n + 2) & ~1LL);   // room for the 8-byte alignment shift, 16-byte aligned buffers
     size_t off = tg_align_up((size_t)nbuf * p.stride * sizeof(double), 16);
     p.off_sidx = off;
     off = tg_align_up(off + (size_t)n * sizeof(uint32_t), 16);
-    p.off_f16 = off;
-    off = tg_align_up(off + (size_t)(p.NBcap / 2 + 2) * sizeof(uint32_t), 16);
+    p.off_cinfo = off;   // also the coarse histogram (u32 x C) before the allocation phase
+    off = tg_align_up(off + (size_t)p.C * sizeof(RtCoarse), 16);
     p.off_misc = off;
-    off = tg_align_up(off + sizeof(RsMisc), 16);
+    off = tg_align_up(off + sizeof(RtMisc), 16);
     p.off_bar = off;
-    off += 2 * sizeof(uint64_t);                 // 2 mbarriers
-    p.smem = off;
+    off += 2 * sizeof(uint64_t);
+    p.off_f16 = tg_align_up(off, 16);
+    // the rest: packed u16 fine-bucket counters; NB <= 2C + fs*m + 1 entries
+    const size_t fixed = p.off_f16 + 64;
+    double room = smem_max > fixed ? (double)(smem_max - fixed) / 2.0 : 0.0;   // u16 entries
+    double fs = (room - 2.0 * p.C - 8.0) / (double)(m > 0 ? m : 1);
+    if (fs > 2.0) fs = 2.0;
+    p.fs = (float)fs;
+    p.NBcap = 2 * p.C + (int)std::ceil(fs * m) + 2;
+    p.smem = p.off_f16 + (size_t)(p.NBcap / 2 + 2) * sizeof(uint32_t);
+    if (fs < 0.45 || p.NBcap >= 65535) p.smem = (size_t)-1;   // does not fit: caller tries the next layout
     return p;
 }
 
@@ -397,7 +421,6 @@ __device__ __forceinline__ void rt_wait(uint64_t *bar, unsigned parity) {
         : "memory");
 }
 
-
 template <int EMAX>
 __global__ void __launch_bounds__(RS_T, 1)
 row_sort_tma_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restrict__ order,
@@ -406,11 +429,13 @@ row_sort_tma_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restri
     const int n = (int)n64;
     const int m = n - 1;
     double *vbuf = reinterpret_cast<double *>(rs_smem);
-    uint32_t *sidx = reinterpret_cast<uint32_t *>(rs_smem + pl.off_sidx);
-    uint32_t *f16 = reinterpret_cast<uint32_t *>(rs_smem + pl.off_f16);
-    RsMisc &ms = *reinterpret_cast<RsMisc *>(rs_smem + pl.off_misc);
-    const uint16_t *o16 = reinterpret_cast<const uint16_t *>(f16);   // bucket offsets, read side
+    uint32_t *sidx = reinterpret_cast<uint32_t *>(rs_smem + pl.off_sidx);   // (bucket << 16) | id
+    RtCoarse *cinfo = reinterpret_cast<RtCoarse *>(rs_smem + pl.off_cinfo);
+    uint32_t *ccnt = reinterpret_cast<uint32_t *>(rs_smem + pl.off_cinfo);   // aliased: histogram first
+    RtMisc &ms = *reinterpret_cast<RtMisc *>(rs_smem + pl.off_misc);
     uint64_t *bar = reinterpret_cast<uint64_t *>(rs_smem + pl.off_bar);
+    uint32_t *f16 = reinterpret_cast<uint32_t *>(rs_smem + pl.off_f16);
+    const uint16_t *o16 = reinterpret_cast<const uint16_t *>(f16);   // bucket offsets, read side
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int C = pl.C;
     const int nw16 = pl.NBcap / 2 + 2;
@@ -430,9 +455,9 @@ row_sort_tma_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restri
         const double *row = S + v * n64;
         const double *vals = vbuf + (size_t)b * pl.stride + (((uintptr_t)row >> 3) & 1);
         rt_wait(&bar[b], parity);
-        // ---- A: clear counters; row min / max / NaN (v excluded)
+        // ---- A: clear counters; row min / max / NaN (v excluded); row-sum screen
         for (int i = tid; i < nw16; i += RS_T) f16[i] = 0u;
-        for (int c = tid; c <= C; c += RS_T) ms.ccnt[c] = 0;
+        for (int c = tid; c < C; c += RS_T) ccnt[c] = 0u;
         if (tid == 0) ms.nsamp = 0;
         double mn = INFINITY, mx = -INFINITY, sm = 0.0, sa = 0.0;
         bool nan_seen = false;
@@ -441,50 +466,53 @@ row_sort_tma_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restri
             const int j = tid + e * RS_T;
             if (j < n) {
                 const double x = vals[j];
-                sm += x;                // row-sum screen (clique candidates)
+                sm += x;
                 sa += fabs(x);
                 if (j != v) {
-                    mn = x < mn ? x : mn;   // NaN: never selected, flagged below
+                    mn = x < mn ? x : mn;   // NaN: never selected, flagged instead
                     mx = x > mx ? x : mx;
                     nan_seen |= (x != x);
                 }
             }
         }
-        const bool row_nan = __syncthreads_or(nan_seen);   // also: the row is visible to all
-        if (tid == 0 && pl.nbuf == 2) {
-            const int64_t vn = v + gridDim.x;
-            if (vn < n) rt_bulk_row(vbuf + (size_t)(b ^ 1) * pl.stride, S + vn * n64, n, &bar[b ^ 1]);
-        }
+        // float bounds rounded outward: the bins only need a range that contains the row
+        float fmn = __double2float_rd(mn), fmx = __double2float_ru(mx);
         for (int o = 16; o; o >>= 1) {
-            mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-            if (screen) {
+            fmn = fminf(fmn, __shfl_xor_sync(0xffffffffu, fmn, o));
+            fmx = fmaxf(fmx, __shfl_xor_sync(0xffffffffu, fmx, o));
+        }
+        if (screen) {
+            for (int o = 16; o; o >>= 1) {
                 sm += __shfl_xor_sync(0xffffffffu, sm, o);
                 sa += __shfl_xor_sync(0xffffffffu, sa, o);
             }
         }
-        if (lane == 0) { ms.red[warp] = mn; ms.red[32 + warp] = mx; ms.red[64 + warp] = sm; ms.red[96 + warp] = sa; }
-        __syncthreads();
+        if (lane == 0) { ms.rmn[warp] = fmn; ms.rmx[warp] = fmx; ms.rsum[warp] = sm; ms.rabs[warp] = sa; }
+        const bool row_nan = __syncthreads_or(nan_seen);   // also: every thread is past the row wait
+        if (tid == 0 && pl.nbuf == 2) {
+            const int64_t vn = v + gridDim.x;
+            if (vn < n) rt_bulk_row(vbuf + (size_t)(b ^ 1) * pl.stride, S + vn * n64, n, &bar[b ^ 1]);
+        }
         double rmax, cscale;
         {
-            double a = ms.red[lane], bb = ms.red[32 + lane];
+            float a = ms.rmn[lane], bb = ms.rmx[lane];
             for (int o = 16; o; o >>= 1) {
-                a = fmin(a, __shfl_xor_sync(0xffffffffu, a, o));
-                bb = fmax(bb, __shfl_xor_sync(0xffffffffu, bb, o));
+                a = fminf(a, __shfl_xor_sync(0xffffffffu, a, o));
+                bb = fmaxf(bb, __shfl_xor_sync(0xffffffffu, bb, o));
             }
-            const double w = bb - a;
-            rmax = bb;
+            const double w = (double)bb - (double)a;
+            rmax = (double)bb;
             cscale = (w > 0.0 && w < INFINITY) ? (double)C / w : 0.0;
-            if (screen && warp == 1) {
-                double s1 = ms.red[64 + lane], s2 = ms.red[96 + lane];
-                for (int o = 16; o; o >>= 1) {
-                    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-                    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-                }
-                if (lane == 0) {
-                    screen[v] = __dsub_rn(s1, vals[v]);
-                    screen[n + v] = rs_screen_radius(n, s2);
-                }
+        }
+        if (screen && warp == 1) {
+            double s1 = ms.rsum[lane], s2 = ms.rabs[lane];
+            for (int o = 16; o; o >>= 1) {
+                s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+                s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+            }
+            if (lane == 0) {
+                screen[v] = __dsub_rn(s1, vals[v]);
+                screen[n + v] = rs_screen_radius(n, s2);
             }
         }
         // ---- B: coarse histogram from a sample (sizes the fine buckets only)
@@ -494,41 +522,46 @@ row_sort_tma_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restri
             const int j = tid + e * RS_T;
             if (j < n && j != v) {
                 double t;
-                atomicAdd(&ms.ccnt[rs_coarse_of(vals[j], rmax, cscale, C, t)], 1u);
+                atomicAdd(&ccnt[rs_coarse_of(vals[j], rmax, cscale, C, t)], 1u);
                 nsamp++;
             }
         }
         nsamp = __reduce_add_sync(0xffffffffu, nsamp);
         if (lane == 0 && nsamp) atomicAdd(&ms.nsamp, (uint32_t)nsamp);
         __syncthreads();
-        // ---- C: fine buckets per coarse bin (about two keys each) + base offsets (warp 0)
+        // ---- C: fine buckets per coarse bin + base offsets (warp 0, in place over the histogram)
         if (warp == 0) {
-            // f_c = 1 + floor(h_c * m / (div * nsamp)) (shaved so sum f_c <= C + m/div)
-            const float scale = (float)m / ((float)pl.div * (float)(ms.nsamp ? ms.nsamp : 1u)) * 0.9999f;
-            const int per = (C + 31) / 32;
+            const float scale = (float)m * pl.fs / (float)(ms.nsamp ? ms.nsamp : 1u) * 0.9999f;
+            constexpr int PER = RS_CMAX / 32;
+            uint32_t f[PER];
             uint32_t s = 0;
-            for (int q = 0; q < per; q++) {
-                const int c = lane * per + q;
-                if (c < C) {
-                    const uint32_t f = 1u + (uint32_t)((float)ms.ccnt[c] * scale);
-                    ms.cf[c] = f;
-                    s += f;
-                }
+#pragma unroll
+            for (int q = 0; q < PER; q++) {
+                const int c = lane * PER + q;
+                f[q] = c < C ? 1u + (uint32_t)((float)ccnt[c] * scale) : 0u;
+                s += f[q];
             }
+            __syncwarp();
             uint32_t incl = s;
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += y;
             }
             uint32_t run = incl - s;
-            for (int q = 0; q < per; q++) {
-                const int c = lane * per + q;
-                if (c < C) { ms.ccnt[c] = run; run += ms.cf[c]; }
+#pragma unroll
+            for (int q = 0; q < PER; q++) {
+                const int c = lane * PER + q;
+                if (c < C) {
+                    RtCoarse ci;
+                    ci.f = (double)f[q];
+                    ci.base = (int)run;
+                    ci.last = (int)(run + f[q] - 1);
+                    cinfo[c] = ci;
+                    run += f[q];
+                }
             }
-            if (lane == 31) ms.ccnt[C] = incl;
         }
         __syncthreads();
-        const int NB = (int)ms.ccnt[C];
         // ---- D: fine bucket + arrival rank (one packed shared atomic per key)
         uint32_t pk[EMAX];
 #pragma unroll
@@ -536,17 +569,35 @@ row_sort_tma_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restri
             const int j = tid + e * RS_T;
             pk[e] = 0xffffffffu;
             if (j < n && j != v) {
-                double t;
-                const int c = rs_coarse_of(vals[j], rmax, cscale, C, t);
-                const int fb = rs_fine_of(t, c, ms.ccnt, ms.cf);
+                const double x = vals[j];
+                int fb;
+                if (!row_nan) {
+                    const double t = (rmax - x) * cscale;
+                    int c = __double2int_rz(t);
+                    c = c < C - 1 ? c : C - 1;
+                    c = c > 0 ? c : 0;
+                    const RtCoarse ci = cinfo[c];
+                    fb = ci.base + __double2int_rz((t - (double)c) * ci.f);
+                    fb = fb < ci.last ? fb : ci.last;
+                    fb = fb > ci.base ? fb : ci.base;
+                } else {
+                    double t;
+                    const int c = rs_coarse_of(x, rmax, cscale, C, t);
+                    const RtCoarse ci = cinfo[c];
+                    const double frac = t - (double)c;
+                    int sub = (frac >= 0.0) ? (int)(frac * ci.f) : 0;
+                    fb = ci.base + sub;
+                    fb = fb < ci.last ? fb : ci.last;
+                }
                 const int sh = (fb & 1) << 4;
                 const uint32_t old = atomicAdd(&f16[fb >> 1], 1u << sh);
                 pk[e] = ((uint32_t)fb << 16) | ((old >> sh) & 0xffffu);
             }
         }
         __syncthreads();
-        // ---- E: exclusive scan of the packed counters (NB + 1 entries), scatter (bucket, id)
+        // ---- E: exclusive scan of the packed counters, scatter ids, bucket-start bits
         {
+            const int NB = cinfo[C - 1].last + 1;
             const int nw = (NB + 2) >> 1;
             const int per = (nw + RS_T - 1) / RS_T;
             const int w0 = tid * per;
@@ -587,8 +638,7 @@ row_sort_tma_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restri
 #pragma unroll
         for (int e = 0; e < EMAX; e++) {
             if (pk[e] != 0xffffffffu) {
-                const int fb = (int)(pk[e] >> 16);
-                sidx[o16[fb] + (pk[e] & 0xffffu)] = (pk[e] & 0xffff0000u) | (uint32_t)(tid + e * RS_T);
+                sidx[o16[pk[e] >> 16] + (pk[e] & 0xffffu)] = (pk[e] & 0xffff0000u) | (uint32_t)(tid + e * RS_T);
             }
         }
         __syncthreads();
@@ -598,8 +648,8 @@ row_sort_tma_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restri
         for (int e = 0; e < EMAX; e++) {
             const int k = tid + e * RS_T;
             if (k < m) {
-                const uint32_t s = sidx[k];
-                const int fb = (int)(s >> 16), j = (int)(s & 0xffffu);
+                const uint32_t sk = sidx[k];
+                const int fb = (int)(sk >> 16), j = (int)(sk & 0xffffu);
                 const int s0 = o16[fb], s1 = o16[fb + 1];
                 int rank = 0;
                 if (s1 - s0 > 1) {
@@ -843,14 +893,11 @@ TG_API int tg_row_sort_f64(const double *S, int64_t n, int32_t *order, double *s
     if (n <= 16384) {
         // preference: two row buffers (TMA of row v+grid overlaps row v) with one key per
         // fine bucket; then two keys per bucket; then a single buffer
-        const int pref[4][2] = {{2, 1}, {2, 2}, {1, 1}, {1, 2}};
-        RtPlan pl;
-        int k = 0;
-        for (; k < 4; k++) {
-            pl = rt_plan(n, pref[k][0], pref[k][1]);
-            if (pl.smem <= RS_SMEM_MAX) break;
-        }
-        if (k == 4) return TG_ERR_ARG;
+        // two row buffers (TMA of row v+grid overlaps row v) when they leave room for
+        // >= 0.45 fine buckets per key, else one
+        RtPlan pl = rt_plan(n, 2, RS_SMEM_MAX);
+        if (pl.smem > RS_SMEM_MAX) pl = rt_plan(n, 1, RS_SMEM_MAX);
+        if (pl.smem > RS_SMEM_MAX) return TG_ERR_ARG;
         int E = (int)((n + RS_T - 1) / RS_T);
 #define RS_LAUNCH(EM)                                                                                      \
     do {                                                                                                   \
