@@ -36,6 +36,7 @@ extern "C" {
 #define TG_ERR_WORKSPACE 3   /* workspace too small */
 #define TG_ERR_CAPACITY 5    /* variable-size output larger than the given capacity */
 #define TG_ERR_TRACE 6       /* trace references a non-live face (tmfg.py:67-68 TraceError) */
+#define TG_ERR_NOT_REDUCIBLE 7 /* NN-chain cannot terminate: distances not reducible (linkage.py:50-94) */
 
 /* validation flags written by tg_validate_f64 (simmatrix.py:126-139 DataError causes) */
 #define TG_BAD_NAN 1
@@ -231,6 +232,17 @@ int tg_group_max_batch(const tg_oracle_t *oracle, const int32_t *perm, const int
 int tg_nn_chain_batch(double *mats, const int64_t *mat_offsets, const int64_t *sizes, int64_t count,
                       const int64_t *merge_offsets, int64_t *lefts_out, int64_t *rights_out, double *heights_out,
                       const int64_t *aux_offsets, uint8_t *active, int64_t *slot, int64_t *chain, void *stream);
+
+/* dbht.py:233-339 build_hierarchy (+ linkage.py:97-116 canonicalisation,
+ * linkage.py:136-148 sizes): the three complete-linkage layers over the bubble
+ * assignment, emitted with the running height floor.  vertex_bubble /
+ * vertex_converging are DEVICE arrays (n); the dendrogram rows are written to
+ * HOST arrays of n-1 entries (lefts, rights, heights, sizes) and *n_merges_out.
+ * Host-orchestrated (a few stream synchronisations); the oracle blocks, group
+ * maxima and NN-chains run on the GPU. */
+int tg_build_hierarchy(const tg_oracle_t *oracle, const int64_t *vertex_bubble, const int64_t *vertex_converging,
+                       int64_t n, int64_t *lefts_out, int64_t *rights_out, double *heights_out, int64_t *sizes_out,
+                       int64_t *n_merges_out, void *stream);
 
 #ifdef __cplusplus
 }

@@ -17,6 +17,7 @@ _LIB_DIR = Path(__file__).resolve().parent / "_lib"
 LIB_PATH = _LIB_DIR / "libtmfg_b200.so"
 
 TG_OK = 0
+TG_ERR_NOT_REDUCIBLE = 7
 TG_ERR_ARG = 1
 TG_ERR_CUDA = 2
 TG_ERR_WORKSPACE = 3
@@ -96,6 +97,7 @@ _PROTOS = {
     "tg_group_max_batch": (ctypes.c_int, [ctypes.POINTER(TgOracle), c_p, c_p, c_p, c_i64, c_p, c_i64, c_p, c_i64,
                                           c_p, c_sz, c_p]),
     "tg_nn_chain_batch": (ctypes.c_int, [c_p, c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p]),
+    "tg_build_hierarchy": (ctypes.c_int, [ctypes.POINTER(TgOracle), c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_p]),
 }
 
 EXPORTED = tuple(_PROTOS)

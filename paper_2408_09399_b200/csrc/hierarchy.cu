@@ -1,0 +1,381 @@
+// hierarchy.cu -- DBHT's three-layer complete-linkage hierarchy, native driver.
+//
+// Replaces dbht.py:233-339 build_hierarchy (+ linkage.py:97-116 canonicalisation
+// and linkage.py:136-148 sizes).  The heavy parts stay on the GPU and are the
+// kernels behind tg_group_blocks (layer-1 oracle blocks), tg_group_max_batch
+// (layer-2/3 pairwise group maxima) and tg_nn_chain_batch (every linkage of a
+// layer in one launch); this file is the host bookkeeping between them, in C++:
+// grouping vertices by bubble / converging bubble, the stable height sort and
+// renumbering of each linkage's merges, the merge records, and the emission
+// with the running height floor.  One stream synchronisation per layer.
+#include "common.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+namespace {
+
+constexpr double HEIGHT_BUMP = 1e-12;                       // dbht.py HEIGHT_BUMP
+constexpr uint64_t NN_CYCLE_SENTINEL = 0x7ff8dead00000000ull;   // tg_nn_chain_batch: chain did not terminate
+
+// stream-ordered device buffer
+struct DevBuf {
+    void *p = nullptr;
+    cudaStream_t st = nullptr;
+    DevBuf() = default;
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    ~DevBuf() {
+        if (p) cudaFreeAsync(p, st);
+    }
+    cudaError_t alloc(size_t bytes, cudaStream_t s) {
+        st = s;
+        return cudaMallocAsync(&p, bytes ? bytes : 16, s);
+    }
+    template <class T>
+    T *as() const { return reinterpret_cast<T *>(p); }
+};
+
+struct Rec {
+    int64_t l, r;
+    double h;
+};
+struct Row {
+    int64_t handle;
+    double h;
+};
+
+struct Ctx {
+    int64_t n;
+    const tg_oracle_t *oracle;
+    cudaStream_t st;
+    std::vector<Rec> records;
+};
+
+#define HC(expr)                                          \
+    do {                                                  \
+        cudaError_t _e = (expr);                          \
+        if (_e != cudaSuccess) {                          \
+            tg_set_last_error(_e, __FILE__, __LINE__);    \
+            return TG_ERR_CUDA;                           \
+        }                                                 \
+    } while (0)
+#define HR(expr)                   \
+    do {                           \
+        int _r = (expr);           \
+        if (_r != TG_OK) return _r; \
+    } while (0)
+
+// NN-chain every matrix of the batch (device, in place), canonicalise (stable
+// height sort, renumbering), append the records; per matrix: root handle + rows.
+int run_linkages(Ctx &cx, double *mats_dev, const std::vector<int64_t> &sizes, const std::vector<int64_t> &mat_off,
+                 const std::vector<std::vector<int64_t>> &handles, std::vector<int64_t> &roots,
+                 std::vector<Row> &rows_out) {
+    const size_t count = sizes.size();
+    std::vector<int64_t> merge_off(count + 1, 0), aux_off(count + 1, 0);
+    for (size_t k = 0; k < count; k++) {
+        merge_off[k + 1] = merge_off[k] + std::max<int64_t>(sizes[k] - 1, 0);
+        aux_off[k + 1] = aux_off[k] + sizes[k];
+    }
+    const int64_t total = merge_off[count], naux = aux_off[count];
+    roots.assign(count, -1);
+    if (total == 0) {
+        for (size_t k = 0; k < count; k++) roots[k] = handles[k][0];
+        return TG_OK;
+    }
+    // one device block: [mat_off | sizes | merge_off | aux_off] int64, then outputs / scratch
+    const size_t nidx = 4 * (count + 1);
+    const size_t b_idx = tg_align_up(nidx * 8, 256), b_l = tg_align_up((size_t)total * 8, 256);
+    const size_t b_h = b_l, b_slot = tg_align_up((size_t)naux * 8, 256), b_chain = tg_align_up((size_t)(naux + 1) * 8, 256);
+    const size_t b_act = tg_align_up((size_t)naux, 256);
+    DevBuf buf;
+    HC(buf.alloc(b_idx + 2 * b_l + b_h + b_slot + b_chain + b_act, cx.st));
+    char *base = buf.as<char>();
+    int64_t *d_idx = reinterpret_cast<int64_t *>(base);
+    int64_t *d_l = reinterpret_cast<int64_t *>(base + b_idx);
+    int64_t *d_r = reinterpret_cast<int64_t *>(base + b_idx + b_l);
+    double *d_h = reinterpret_cast<double *>(base + b_idx + 2 * b_l);
+    int64_t *d_slot = reinterpret_cast<int64_t *>(base + b_idx + 2 * b_l + b_h);
+    int64_t *d_chain = reinterpret_cast<int64_t *>(base + b_idx + 2 * b_l + b_h + b_slot);
+    uint8_t *d_act = reinterpret_cast<uint8_t *>(base + b_idx + 2 * b_l + b_h + b_slot + b_chain);
+    std::vector<int64_t> idx(nidx, 0);
+    std::copy(mat_off.begin(), mat_off.end(), idx.begin());
+    std::copy(sizes.begin(), sizes.end(), idx.begin() + (count + 1));
+    std::copy(merge_off.begin(), merge_off.end(), idx.begin() + 2 * (count + 1));
+    std::copy(aux_off.begin(), aux_off.end(), idx.begin() + 3 * (count + 1));
+    HC(cudaMemcpyAsync(d_idx, idx.data(), nidx * 8, cudaMemcpyHostToDevice, cx.st));
+    HR(tg_nn_chain_batch(mats_dev, d_idx, d_idx + (count + 1), (int64_t)count, d_idx + 2 * (count + 1), d_l, d_r, d_h,
+                         d_idx + 3 * (count + 1), d_act, d_slot, d_chain, cx.st));
+    std::vector<int64_t> L(total), R(total);
+    std::vector<double> Hh(total);
+    HC(cudaMemcpyAsync(L.data(), d_l, total * 8, cudaMemcpyDeviceToHost, cx.st));
+    HC(cudaMemcpyAsync(R.data(), d_r, total * 8, cudaMemcpyDeviceToHost, cx.st));
+    HC(cudaMemcpyAsync(Hh.data(), d_h, total * 8, cudaMemcpyDeviceToHost, cx.st));
+    HC(cudaStreamSynchronize(cx.st));
+    for (int64_t q = 0; q < total; q++) {
+        uint64_t bits;
+        std::memcpy(&bits, &Hh[q], 8);
+        if (bits == NN_CYCLE_SENTINEL) return TG_ERR_NOT_REDUCIBLE;
+    }
+    std::vector<int64_t> ord, rank, local;
+    for (size_t k = 0; k < count; k++) {
+        const int64_t m = sizes[k], lo = merge_off[k], nm = merge_off[k + 1] - lo;
+        // linkage.py:97-116: stable sort of the raw merges by height, id m+t -> m+rank(t)
+        ord.resize(nm);
+        for (int64_t t = 0; t < nm; t++) ord[t] = t;
+        std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return Hh[lo + a] < Hh[lo + b]; });
+        rank.resize(nm);
+        for (int64_t q = 0; q < nm; q++) rank[ord[q]] = q;
+        local.assign(handles[k].begin(), handles[k].end());
+        int64_t root = handles[k][0];
+        for (int64_t q = 0; q < nm; q++) {
+            const int64_t t = ord[q];
+            int64_t a = L[lo + t], b = R[lo + t];
+            if (a >= m) a = m + rank[a - m];
+            if (b >= m) b = m + rank[b - m];
+            const int64_t lo_id = std::min(a, b), hi_id = std::max(a, b);
+            const double h = Hh[lo + t];
+            const int64_t rec = cx.n + (int64_t)cx.records.size();
+            cx.records.push_back({local[lo_id], local[hi_id], h});
+            local.push_back(rec);
+            rows_out.push_back({rec, h});
+            root = rec;
+        }
+        roots[k] = root;
+    }
+    return TG_OK;
+}
+
+// dbht.py:217-230 group maxima for vertex-disjoint sub-problems (one launch), then the linkages
+int group_linkages(Ctx &cx, const std::vector<std::vector<const std::vector<int32_t> *>> &subproblems,
+                   const std::vector<std::vector<int64_t>> &handles, std::vector<int64_t> &roots,
+                   std::vector<Row> &rows_out) {
+    std::vector<int32_t> perm, gid;
+    std::vector<tg_gm_sub_t> subs;
+    std::vector<tg_gm_tile_t> tiles;
+    std::vector<int64_t> sizes, mat_off;
+    int64_t out_off = 0;
+    for (size_t p = 0; p < subproblems.size(); p++) {
+        const auto &groups = subproblems[p];
+        const int64_t perm_off = (int64_t)perm.size();
+        for (size_t g = 0; g < groups.size(); g++)
+            for (int32_t v : *groups[g]) {
+                perm.push_back(v);
+                gid.push_back((int32_t)g);
+            }
+        const int32_t len = (int32_t)(perm.size() - perm_off), m = (int32_t)groups.size();
+        tg_gm_sub_t sd;
+        sd.perm_off = perm_off;
+        sd.len = len;
+        sd.m = m;
+        sd.out_off = out_off;
+        sd.tile_off = (int64_t)tiles.size();
+        subs.push_back(sd);
+        for (int32_t i0 = 0; i0 < len; i0 += 64)
+            for (int32_t j0 = 0; j0 < len; j0 += 64) tiles.push_back({(int32_t)p, i0, j0});
+        sizes.push_back(m);
+        mat_off.push_back(out_off);
+        out_off += (int64_t)m * m;
+    }
+    const int64_t ntiles = (int64_t)tiles.size();
+    const size_t ws_bytes = tg_group_max_workspace_bytes(cx.n, ntiles);
+    const size_t b_perm = tg_align_up(perm.size() * 4, 256), b_sub = tg_align_up(subs.size() * sizeof(tg_gm_sub_t), 256);
+    const size_t b_tile = tg_align_up((size_t)ntiles * sizeof(tg_gm_tile_t), 256);
+    const size_t b_out = tg_align_up((size_t)std::max<int64_t>(out_off, 1) * 8, 256);
+    DevBuf buf;
+    HC(buf.alloc(2 * b_perm + b_sub + b_tile + b_out + ws_bytes, cx.st));
+    char *base = buf.as<char>();
+    int32_t *d_perm = reinterpret_cast<int32_t *>(base);
+    int32_t *d_gid = reinterpret_cast<int32_t *>(base + b_perm);
+    void *d_sub = base + 2 * b_perm;
+    void *d_tile = base + 2 * b_perm + b_sub;
+    double *d_out = reinterpret_cast<double *>(base + 2 * b_perm + b_sub + b_tile);
+    void *d_ws = base + 2 * b_perm + b_sub + b_tile + b_out;
+    HC(cudaMemcpyAsync(d_perm, perm.data(), perm.size() * 4, cudaMemcpyHostToDevice, cx.st));
+    HC(cudaMemcpyAsync(d_gid, gid.data(), gid.size() * 4, cudaMemcpyHostToDevice, cx.st));
+    HC(cudaMemcpyAsync(d_sub, subs.data(), subs.size() * sizeof(tg_gm_sub_t), cudaMemcpyHostToDevice, cx.st));
+    HC(cudaMemcpyAsync(d_tile, tiles.data(), (size_t)ntiles * sizeof(tg_gm_tile_t), cudaMemcpyHostToDevice, cx.st));
+    HR(tg_group_max_batch(cx.oracle, d_perm, d_gid, d_sub, (int64_t)subs.size(), d_tile, ntiles, d_out, out_off, d_ws,
+                          ws_bytes, cx.st));
+    return run_linkages(cx, d_out, sizes, mat_off, handles, roots, rows_out);
+}
+
+void stable_sort_rows(std::vector<Row> &rows) {
+    std::stable_sort(rows.begin(), rows.end(), [](const Row &a, const Row &b) { return a.h < b.h; });
+}
+
+int build(Ctx &cx, const int64_t *vb_dev, const int64_t *vc_dev, int64_t *lefts, int64_t *rights, double *heights,
+          int64_t *sizes_out, int64_t *n_merges) {
+    const int64_t n = cx.n;
+    std::vector<int64_t> vb(n), vc(n);
+    HC(cudaMemcpyAsync(vb.data(), vb_dev, n * 8, cudaMemcpyDeviceToHost, cx.st));
+    HC(cudaMemcpyAsync(vc.data(), vc_dev, n * 8, cudaMemcpyDeviceToHost, cx.st));
+    HC(cudaStreamSynchronize(cx.st));
+    int64_t nb = 0;
+    for (int64_t v = 0; v < n; v++) {
+        if (vb[v] < 0) return TG_ERR_ARG;
+        nb = std::max(nb, vb[v] + 1);
+    }
+    // vertices by (bubble, id): members[b] ascending
+    std::vector<std::vector<int32_t>> members(nb);
+    for (int64_t v = 0; v < n; v++) members[vb[v]].push_back((int32_t)v);
+    std::vector<int64_t> bubble_ids;
+    for (int64_t b = 0; b < nb; b++)
+        if (!members[b].empty()) bubble_ids.push_back(b);
+    std::vector<int64_t> group_root(nb, -1);
+
+    // ---- layer 1: complete linkage inside every bubble group (dbht.py:247-262)
+    std::vector<Row> rows1, rows2, rows3;
+    {
+        std::vector<int64_t> multi;
+        for (int64_t b : bubble_ids) {
+            if (members[b].size() > 1) multi.push_back(b);
+            else group_root[b] = members[b][0];
+        }
+        if (!multi.empty()) {
+            const size_t cnt = multi.size();
+            std::vector<int32_t> perm;
+            std::vector<int64_t> gst(cnt + 1, 0), boff(cnt + 1, 0), sizes(cnt), mat_off(cnt);
+            std::vector<std::vector<int64_t>> handles(cnt);
+            for (size_t k = 0; k < cnt; k++) {
+                const auto &mem = members[multi[k]];
+                const int64_t s = (int64_t)mem.size();
+                perm.insert(perm.end(), mem.begin(), mem.end());
+                gst[k + 1] = gst[k] + s;
+                boff[k + 1] = boff[k] + s * s;
+                sizes[k] = s;
+                mat_off[k] = boff[k];
+                handles[k].assign(mem.begin(), mem.end());
+            }
+            const size_t b_perm = tg_align_up(perm.size() * 4, 256), b_idx = tg_align_up((cnt + 1) * 8, 256);
+            DevBuf buf;
+            HC(buf.alloc(b_perm + 2 * b_idx + (size_t)boff[cnt] * 8, cx.st));
+            char *base = buf.as<char>();
+            int32_t *d_perm = reinterpret_cast<int32_t *>(base);
+            int64_t *d_gst = reinterpret_cast<int64_t *>(base + b_perm);
+            int64_t *d_boff = reinterpret_cast<int64_t *>(base + b_perm + b_idx);
+            double *d_blocks = reinterpret_cast<double *>(base + b_perm + 2 * b_idx);
+            HC(cudaMemcpyAsync(d_perm, perm.data(), perm.size() * 4, cudaMemcpyHostToDevice, cx.st));
+            HC(cudaMemcpyAsync(d_gst, gst.data(), (cnt + 1) * 8, cudaMemcpyHostToDevice, cx.st));
+            HC(cudaMemcpyAsync(d_boff, boff.data(), (cnt + 1) * 8, cudaMemcpyHostToDevice, cx.st));
+            HR(tg_group_blocks(cx.oracle, d_perm, d_gst, (int64_t)cnt, d_boff, d_blocks, cx.st));
+            std::vector<int64_t> roots;
+            HR(run_linkages(cx, d_blocks, sizes, mat_off, handles, roots, rows1));
+            for (size_t k = 0; k < cnt; k++) group_root[multi[k]] = roots[k];
+        }
+        stable_sort_rows(rows1);
+    }
+
+    // ---- layer 2: bubbles inside each converging group (dbht.py:264-300)
+    std::vector<int64_t> conv_ids;
+    std::vector<std::vector<int64_t>> conv_bubbles;   // parallel to conv_ids
+    std::vector<int64_t> conv_root;
+    {
+        std::vector<std::pair<int64_t, int64_t>> cb;   // (conv id, bubble) in bubble order
+        for (int64_t b : bubble_ids) cb.push_back({vc[members[b][0]], b});
+        std::stable_sort(cb.begin(), cb.end(),
+                         [](const std::pair<int64_t, int64_t> &a, const std::pair<int64_t, int64_t> &b) {
+                             return a.first < b.first;
+                         });
+        for (const auto &x : cb) {
+            if (conv_ids.empty() || conv_ids.back() != x.first) {
+                conv_ids.push_back(x.first);
+                conv_bubbles.emplace_back();
+            }
+            conv_bubbles.back().push_back(x.second);
+        }
+        conv_root.assign(conv_ids.size(), -1);
+        std::vector<std::vector<const std::vector<int32_t> *>> subproblems;
+        std::vector<std::vector<int64_t>> handles;
+        std::vector<size_t> which;
+        for (size_t c = 0; c < conv_ids.size(); c++) {
+            if (conv_bubbles[c].size() == 1) {
+                conv_root[c] = group_root[conv_bubbles[c][0]];
+                continue;
+            }
+            std::vector<const std::vector<int32_t> *> groups;
+            std::vector<int64_t> hs;
+            for (int64_t b : conv_bubbles[c]) {
+                groups.push_back(&members[b]);
+                hs.push_back(group_root[b]);
+            }
+            subproblems.push_back(std::move(groups));
+            handles.push_back(std::move(hs));
+            which.push_back(c);
+        }
+        if (!subproblems.empty()) {
+            std::vector<int64_t> roots;
+            HR(group_linkages(cx, subproblems, handles, roots, rows2));
+            for (size_t k = 0; k < which.size(); k++) conv_root[which[k]] = roots[k];
+        }
+        stable_sort_rows(rows2);
+    }
+
+    // ---- layer 3: converging groups against each other (dbht.py:302-324)
+    if (conv_ids.size() > 1) {
+        std::vector<std::vector<int32_t>> cmem(conv_ids.size());
+        std::vector<const std::vector<int32_t> *> groups;
+        std::vector<int64_t> hs;
+        for (size_t c = 0; c < conv_ids.size(); c++) {
+            for (int64_t b : conv_bubbles[c]) cmem[c].insert(cmem[c].end(), members[b].begin(), members[b].end());
+            std::sort(cmem[c].begin(), cmem[c].end());
+        }
+        for (size_t c = 0; c < conv_ids.size(); c++) {
+            groups.push_back(&cmem[c]);
+            hs.push_back(conv_root[c]);
+        }
+        std::vector<int64_t> roots;
+        HR(group_linkages(cx, {groups}, {hs}, roots, rows3));
+        stable_sort_rows(rows3);
+    }
+
+    // ---- emission with the running height floor (dbht.py:326-339) + sizes (linkage.py:136-148)
+    const int64_t nrec = (int64_t)cx.records.size();
+    std::vector<int64_t> final_id(n + nrec);
+    for (int64_t i = 0; i < n + nrec; i++) final_id[i] = i;
+    std::vector<int64_t> size_of(n + nrec, 1);
+    double floor_h = -INFINITY;
+    int64_t k = 0;
+    for (const std::vector<Row> *rows : {&rows1, &rows2, &rows3}) {
+        for (const Row &row : *rows) {
+            const Rec &rc = cx.records[row.handle - n];
+            double h = rc.h;
+            if (h < floor_h) h = floor_h + HEIGHT_BUMP;
+            floor_h = h;
+            const int64_t li = final_id[rc.l], ri = final_id[rc.r];
+            final_id[row.handle] = n + k;
+            if (k >= n - 1) return TG_ERR_ARG;   // more merges than a binary tree over n leaves has
+            lefts[k] = std::min(li, ri);
+            rights[k] = std::max(li, ri);
+            heights[k] = h;
+            const int64_t s = size_of[lefts[k]] + size_of[rights[k]];
+            size_of[n + k] = s;
+            sizes_out[k] = s;
+            k++;
+        }
+    }
+    *n_merges = k;
+    return TG_OK;
+}
+
+}  // namespace
+
+TG_API int tg_build_hierarchy(const tg_oracle_t *oracle, const int64_t *vertex_bubble, const int64_t *vertex_converging,
+                              int64_t n, int64_t *lefts_out, int64_t *rights_out, double *heights_out,
+                              int64_t *sizes_out, int64_t *n_merges_out, void *stream) {
+    if (!oracle || !vertex_bubble || !vertex_converging || !n_merges_out || n < 1) return TG_ERR_ARG;
+    if (n > 1 && (!lefts_out || !rights_out || !heights_out || !sizes_out)) return TG_ERR_ARG;
+    *n_merges_out = 0;
+    Ctx cx;
+    cx.n = n;
+    cx.oracle = oracle;
+    cx.st = tg_stream(stream);
+    try {
+        return build(cx, vertex_bubble, vertex_converging, lefts_out, rights_out, heights_out, sizes_out,
+                     n_merges_out);
+    } catch (...) {   // std::bad_alloc: no C++ exception crosses the ABI
+        return TG_ERR_ARG;
+    }
+}

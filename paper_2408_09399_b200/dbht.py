@@ -11,6 +11,8 @@ emits the merge records.
 
 from __future__ import annotations
 
+import ctypes
+
 from dataclasses import dataclass
 
 import numpy as np
@@ -177,6 +179,7 @@ def assign_vertices(graph, dtree: DirectedBubbleTree, oracle) -> BubbleAssignmen
     N.call("tg_assign_vertices", s, N.ptr(b), m, N.ptr(sinks), N.ptr(vb), N.ptr(vc), N.ptr(ws), ws.numel(),
            N.stream_ptr())
     a = BubbleAssignment(vertex_bubble=vb.cpu().numpy(), vertex_converging=vc.cpu().numpy())
+    a._vb_dev, a._vc_dev = vb, vc   # device copies for build_hierarchy
     return a
 
 
@@ -271,86 +274,35 @@ def _run_linkages(oracle, mats_dev, sizes: np.ndarray, mat_off: np.ndarray, hand
 
 def build_hierarchy(assignment: BubbleAssignment, dtree: DirectedBubbleTree, oracle,
                     workers: int | None = None) -> Dendrogram:
-    """Assemble the full dendrogram in three complete-linkage layers (dbht.py:233-339)."""
+    """Assemble the full dendrogram in three complete-linkage layers (dbht.py:233-339).
+
+    Native driver (csrc/hierarchy.cu, ``tg_build_hierarchy``): layer-1 oracle
+    blocks, layer-2/3 group maxima and every NN-chain run on the GPU; grouping,
+    canonicalisation, records and the height-floor emission are C++ host code.
+    """
     t = D.torch()
-    vb = np.asarray(assignment.vertex_bubble, dtype=np.int64)
-    vc = np.asarray(assignment.vertex_converging, dtype=np.int64)
-    n = vb.shape[0]
-    ids = np.arange(n, dtype=np.int64)
-    order = np.lexsort((ids, vb))                      # vertices by (bubble, id)
-    bubble_ids, starts, counts = np.unique(vb[order], return_index=True, return_counts=True)
-    groups = {int(b): order[s:s + c] for b, s, c in zip(bubble_ids, starts, counts)}
-    records: list = []
-
-    # ---- layer 1: complete linkage inside every bubble group (GPU blocks + NN-chain)
-    multi = [int(b) for b, c in zip(bubble_ids, counts) if c > 1]
-    group_root = {int(b): int(groups[int(b)][0]) for b, c in zip(bubble_ids, counts) if c == 1}
-    layer1_rows: list = []
-    if multi:
-        sizes = np.array([groups[b].shape[0] for b in multi], dtype=np.int64)
-        perm = np.concatenate([groups[b] for b in multi]).astype(np.int32)
-        gstarts = np.zeros(len(multi) + 1, dtype=np.int64)
-        np.cumsum(sizes, out=gstarts[1:])
-        boff = np.zeros(len(multi) + 1, dtype=np.int64)
-        np.cumsum(sizes * sizes, out=boff[1:])
-        blocks = D.empty((int(boff[-1]),), t.float64)
-        s = _oracle_struct(oracle)
-        perm_d = D.to_device(perm, t.int32)
-        gst_d = D.to_device(gstarts, t.int64)
-        boff_d = D.to_device(boff, t.int64)
-        N.call("tg_group_blocks", s, N.ptr(perm_d), N.ptr(gst_d), len(multi), N.ptr(boff_d), N.ptr(blocks),
-               N.stream_ptr())
-        roots, rows = _run_linkages(oracle, blocks, sizes, boff[:-1], [list(groups[b]) for b in multi], records, n)
-        for b, r, rr in zip(multi, roots, rows):
-            group_root[b] = r
-            layer1_rows.extend(rr)
-    layer1_rows.sort(key=lambda x: x[1])
-
-    # ---- layer 2: bubble clusters inside each converging group
-    conv_groups: dict = {}
-    for b in bubble_ids:
-        conv_groups.setdefault(int(vc[groups[int(b)][0]]), []).append(int(b))
-    conv_ids = sorted(conv_groups)
-    conv_root: dict = {}
-    layer2_rows: list = []
-    multi2 = [c for c in conv_ids if len(conv_groups[c]) > 1]
-    for c in conv_ids:
-        if len(conv_groups[c]) == 1:
-            conv_root[c] = group_root[conv_groups[c][0]]
-    if multi2:
-        out, subs = group_max_batch(oracle, [[groups[b] for b in conv_groups[c]] for c in multi2])
-        sizes = subs["m"].astype(np.int64)
-        roots, rows = _run_linkages(oracle, out, sizes, subs["out_off"].astype(np.int64),
-                                    [[group_root[b] for b in conv_groups[c]] for c in multi2], records, n)
-        for c, r, rr in zip(multi2, roots, rows):
-            conv_root[c] = r
-            layer2_rows.extend(rr)
-    layer2_rows.sort(key=lambda x: x[1])
-
-    # ---- layer 3: converging groups against each other
-    layer3_rows: list = []
-    if len(conv_ids) > 1:
-        members = [np.sort(np.concatenate([groups[b] for b in conv_groups[c]])) for c in conv_ids]
-        out, subs = group_max_batch(oracle, [members])
-        _, rows = _run_linkages(oracle, out, subs["m"].astype(np.int64), subs["out_off"].astype(np.int64),
-                                [[conv_root[c] for c in conv_ids]], records, n)
-        layer3_rows = sorted(rows[0], key=lambda x: x[1])
-
-    # ---- emit with a running height floor (dbht.py:326-339)
-    final_l, final_r, final_h = [], [], []
-    final_id: dict = {}
-    floor = -np.inf
-    for rows in (layer1_rows, layer2_rows, layer3_rows):
-        for handle, _ in rows:
-            left, right, h = records[handle - n]
-            if h < floor:
-                h = floor + HEIGHT_BUMP
-            floor = h
-            li = final_id.get(left, left)
-            ri = final_id.get(right, right)
-            final_id[handle] = n + len(final_l)
-            final_l.append(min(li, ri))
-            final_r.append(max(li, ri))
-            final_h.append(h)
-    return dendrogram_from_merges(n, (np.array(final_l, dtype=np.int64), np.array(final_r, dtype=np.int64),
-                                      np.array(final_h, dtype=np.float64)))
+    vb = getattr(assignment, "_vb_dev", None)
+    vc = getattr(assignment, "_vc_dev", None)
+    if vb is None or vc is None:
+        vb = D.to_device(np.asarray(assignment.vertex_bubble, dtype=np.int64), t.int64)
+        vc = D.to_device(np.asarray(assignment.vertex_converging, dtype=np.int64), t.int64)
+    n = int(vb.shape[0])
+    k = max(n - 1, 0)
+    lefts = np.empty(max(k, 1), dtype=np.int64)
+    rights = np.empty(max(k, 1), dtype=np.int64)
+    heights = np.empty(max(k, 1), dtype=np.float64)
+    sizes = np.empty(max(k, 1), dtype=np.int64)
+    nm = np.zeros(1, dtype=np.int64)
+    s = _oracle_struct(oracle)
+    hp = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    try:
+        N.call("tg_build_hierarchy", s, N.ptr(vb), N.ptr(vc), n, hp(lefts), hp(rights), hp(heights), hp(sizes),
+               hp(nm), N.stream_ptr())
+    except N.NativeError as e:
+        if e.code == N.TG_ERR_NOT_REDUCIBLE:
+            raise RuntimeError("NN-chain did not terminate: the distance matrix is not reducible "
+                               "(the reference's linkage.py:50-94 loop would not terminate either)") from e
+        raise
+    m = int(nm[0])
+    return Dendrogram(n_leaves=n, lefts=lefts[:m].copy(), rights=rights[:m].copy(), heights=heights[:m].copy(),
+                      sizes=sizes[:m].copy())
