@@ -58,6 +58,14 @@ size_t tg_pearson_workspace_bytes(int64_t n, int64_t L);
 int tg_pearson_f64(const double *X, int64_t n, int64_t L, double *S_out, void *ws, size_t ws_bytes,
                    void *stream);
 
+/* _kernels.py:17-37 in the reference's arithmetic order (sequential k, product
+ * and sum rounded separately, (s * inv_i) * inv_j, clamp): bit-identical to the
+ * reference's S from the same centred rows xc (n, L) and inverse norms inv (n)
+ * (its numpy prologue, simmatrix.py:113-118).  FP64-pipe bound; the DMMA path
+ * above is the fast one (within 1e-12). */
+int tg_pearson_refexact_f64(const double *xc, const double *inv, int64_t n, int64_t L, double *S_out,
+                            void *stream);
+
 /* simmatrix.py:126-139 validate_similarity: writes a TG_BAD_* bitmask to
  * *flags_out (device int32). */
 int tg_validate_f64(const double *S, int64_t n, int32_t *flags_out, void *stream);

@@ -62,6 +62,7 @@ _PROTOS = {
     "tg_launch_count": (ctypes.c_longlong, []),
     "tg_pearson_workspace_bytes": (c_sz, [c_i64, c_i64]),
     "tg_pearson_f64": (ctypes.c_int, [c_p, c_i64, c_i64, c_p, c_p, c_sz, c_p]),
+    "tg_pearson_refexact_f64": (ctypes.c_int, [c_p, c_p, c_i64, c_i64, c_p, c_p]),
     "tg_validate_f64": (ctypes.c_int, [c_p, c_i64, c_p, c_p]),
     "tg_row_sort_workspace_bytes": (c_sz, [c_i64]),
     "tg_row_sort_f64": (ctypes.c_int, [c_p, c_i64, c_p, c_p, c_p, c_sz, c_p]),

@@ -232,6 +232,79 @@ __global__ void validate_kernel(const double *__restrict__ S, int64_t n, int32_t
     if (tx == 0 && f) atomicOr(flags, f);
 }
 
+
+// ---------------------------------------------------------------- reference-order variant
+// _kernels.py:17-37 evaluated in the reference's own arithmetic order: for each
+// pair a sequential k loop s += xc_ik * xc_jk (separate rounding of the product
+// and the sum, no FMA), r = (s * inv_i) * inv_j, clamp.  Bit-identical to the
+// reference's S given the same xc / inv (its numpy prologue).  CTA tile 64 x 64
+// pairs (upper triangle), 16 x 16 threads with 4 x 4 pairs each, k staged in
+// shared memory 16 at a time; FP64 pipe bound (2 ops per pair per k).
+constexpr int RX_T = 64;
+constexpr int RX_K = 16;
+
+__global__ void __launch_bounds__(256) pearson_refexact_kernel(const double *__restrict__ xc,
+                                                                const double *__restrict__ inv, int64_t n,
+                                                                int64_t L, double *__restrict__ S) {
+    // upper-triangular tile (I <= J) from the linear block id
+    const int64_t nt = (n + RX_T - 1) / RX_T;
+    int64_t b = blockIdx.x, I = 0;
+    while (b >= nt - I) { b -= nt - I; I++; }
+    const int64_t J = I + b;
+    __shared__ double As[RX_K][RX_T + 1];
+    __shared__ double Bs[RX_K][RX_T + 1];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int64_t i0 = I * RX_T, j0 = J * RX_T;
+    double acc[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; r++)
+#pragma unroll
+        for (int c = 0; c < 4; c++) acc[r][c] = 0.0;
+    for (int64_t k0 = 0; k0 < L; k0 += RX_K) {
+        for (int e = threadIdx.x; e < RX_T * RX_K; e += 256) {
+            const int rr = e / RX_K, kk = e % RX_K;
+            const int64_t gi = i0 + rr, gj = j0 + rr, gk = k0 + kk;
+            As[kk][rr] = (gi < n && gk < L) ? xc[gi * L + gk] : 0.0;
+            Bs[kk][rr] = (gj < n && gk < L) ? xc[gj * L + gk] : 0.0;
+        }
+        __syncthreads();
+        const int kend = (int)(L - k0 < RX_K ? L - k0 : RX_K);
+        for (int kk = 0; kk < kend; kk++) {
+            double a[4], bv[4];
+#pragma unroll
+            for (int r = 0; r < 4; r++) a[r] = As[kk][ty * 4 + r];
+#pragma unroll
+            for (int c = 0; c < 4; c++) bv[c] = Bs[kk][tx * 4 + c];
+#pragma unroll
+            for (int r = 0; r < 4; r++)
+#pragma unroll
+                for (int c = 0; c < 4; c++) acc[r][c] = __dadd_rn(acc[r][c], __dmul_rn(a[r], bv[c]));
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < 4; r++) {
+        const int64_t i = i0 + ty * 4 + r;
+        if (i >= n) continue;
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            const int64_t j = j0 + tx * 4 + c;
+            if (j >= n || j < i) continue;
+            if (j == i) { S[i * n + i] = 1.0; continue; }
+            double v;
+            if (inv[i] == 0.0 || inv[j] == 0.0) {
+                v = 0.0;
+            } else {
+                v = __dmul_rn(__dmul_rn(acc[r][c], inv[i]), inv[j]);
+                if (v > 1.0) v = 1.0;
+                else if (v < -1.0) v = -1.0;
+            }
+            S[i * n + j] = v;
+            S[j * n + i] = v;
+        }
+    }
+}
+
 }  // namespace
 
 TG_API size_t tg_pearson_workspace_bytes(int64_t n, int64_t L) {
@@ -271,6 +344,17 @@ TG_API int tg_validate_f64(const double *S, int64_t n, int32_t *flags, void *str
     TG_CUDA_CHECK(cudaMemsetAsync(flags, 0, sizeof(int32_t), st));
     const int64_t nb = (n + 31) / 32;
     validate_kernel<<<(unsigned)(nb * (nb + 1) / 2), 256, 0, st>>>(S, n, flags); tg_count_launch(1);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
+TG_API int tg_pearson_refexact_f64(const double *xc, const double *inv, int64_t n, int64_t L, double *S, void *stream) {
+    if (n < 1 || L < 0 || !xc || !inv || !S) return TG_ERR_ARG;
+    const int64_t nt = (n + RX_T - 1) / RX_T;
+    const int64_t tiles = nt * (nt + 1) / 2;
+    if (tiles > 0x7fffffffLL) return TG_ERR_ARG;
+    pearson_refexact_kernel<<<(unsigned)tiles, 256, 0, tg_stream(stream)>>>(xc, inv, n, L, S);
+    tg_count_launch(1);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }

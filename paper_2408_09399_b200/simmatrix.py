@@ -66,6 +66,31 @@ def pearson_similarity_device(X):
     return S
 
 
+def pearson_similarity_refexact_device(x):
+    """(n, L) host series -> the reference's exact S as a CUDA tensor.
+
+    The numpy prologue is the reference's own (simmatrix.py:113-118: mean,
+    einsum norm, guarded reciprocal), the O(n^2 L) kernel runs on the GPU in the
+    reference's arithmetic order (``tg_pearson_refexact_f64``), so S is
+    bit-identical to ``tmfgclust.simmatrix.pearson_similarity`` -- the input the
+    bit-exactness contract is stated on.  ``pearson_similarity_device`` (DMMA)
+    is the fast path, within 1e-12.
+    """
+    t = D.torch()
+    x = np.asarray(x, dtype=np.float64)
+    xc = x - x.mean(axis=1, keepdims=True)
+    norm = np.sqrt(np.einsum("ij,ij->i", xc, xc))
+    inv = np.zeros_like(norm)
+    nz = norm > 0.0
+    inv[nz] = 1.0 / norm[nz]
+    n, L = xc.shape
+    xcd = D.to_device(np.ascontiguousarray(xc), t.float64)
+    invd = D.to_device(inv, t.float64)
+    S = D.empty((n, n), t.float64)
+    N.call("tg_pearson_refexact_f64", N.ptr(xcd), N.ptr(invd), n, L, N.ptr(S), N.stream_ptr())
+    return S
+
+
 def pearson_similarity(data: Dataset, workers: int | None = None):
     """Dense Pearson correlation matrix of the dataset's rows (simmatrix.py:105-123).
 

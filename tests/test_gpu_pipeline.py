@@ -107,3 +107,30 @@ def test_corrupt_trace_raises(small_cases, pkg):
                        faces=g.faces)
     with pytest.raises(pkg.TraceError):
         pkg.build_bubble_tree(g2)
+
+
+def test_pipeline_config5_50k(pkg):
+    """BASELINE config 5 (n = 50,000, 20 GB S resident in HBM): the reference's own S
+    (reference-order Pearson on the GPU), then the whole pipeline; golden record
+    from the pinned C oracle (tests/golden/make_config5.py)."""
+    import json
+    from pathlib import Path
+
+    from oracle import oracle as orc
+    from paper_2408_09399_b200 import simmatrix, synth
+    path = Path(__file__).parent / "golden" / "config5.json"
+    if not path.exists():
+        pytest.skip("tests/golden/config5.json not generated")
+    rec = json.loads(path.read_text())
+    x, labels = synth.generate(5)
+    Sd = simmatrix.pearson_similarity_refexact_device(x)
+    assert orc.sha(Sd[:64].cpu().numpy()) == rec["S_rows"]
+    n = rec["n"]
+    band = Sd.reshape(-1)[pkg._device.torch().arange(n, device=Sd.device) * n
+                          + (pkg._device.torch().arange(n, device=Sd.device) * 7919) % n]
+    assert orc.sha(band.cpu().numpy()) == rec["S_diag_band"]
+    report, graph, dend, flat = pkg.run_stages(pkg.PipelineConfig(apsp_mode="hub", k=rec["k"]), Sd, labels)
+    assert orc.sha(np.asarray(graph.edges, dtype=np.int32)) == rec["tmfg_edges"]
+    assert report.digest == rec["hub_digest"]
+    assert orc.sha(np.asarray(flat, dtype=np.int64)) == rec["hub_labels"]
+    assert report.num_converging == rec["hub_num_converging"]

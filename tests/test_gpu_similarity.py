@@ -62,6 +62,26 @@ def test_pearson_within_tolerance(n, L, oracle, pkg):
     pkg.validate_similarity(got)
 
 
+@pytest.mark.parametrize("n,L", [(5, 3), (70, 17), (257, 64), (1000, 128)])
+def test_pearson_refexact_bit_identical(n, L, oracle, pkg):
+    """The reference-order kernel reproduces the reference's S bit for bit."""
+    from paper_2408_09399_b200 import simmatrix
+    rng = np.random.default_rng(7 * n + L)
+    x = rng.standard_normal((n, L)) * rng.uniform(0.1, 10, size=(n, 1))
+    x[min(2, n - 1)] = -1.5  # constant row
+    got = simmatrix.pearson_similarity_refexact_device(x).cpu().numpy()
+    assert np.array_equal(got, oracle.pearson_similarity(x))
+
+
+def test_pearson_refexact_matches_golden_configs(digests, pkg):
+    from oracle import oracle as orc
+    from paper_2408_09399_b200 import simmatrix, synth
+    for cfg in (1, 2, 4):
+        x, _ = synth.generate(cfg)
+        S = simmatrix.pearson_similarity_refexact_device(x).cpu().numpy()
+        assert orc.sha(S) == digests[f"config{cfg}"]["S"]
+
+
 def test_pearson_config4_integer_series(oracle, pkg):
     from paper_2408_09399_b200 import synth
     x, lab = synth.generate(4, n=1500)
