@@ -75,10 +75,10 @@ struct Ctl {
     Ent win;
     long long pops, refreshes, gain_inc;
     int pool_count;
+    unsigned long long pool_minkey;   // <= the smallest pool key (order key of the gain)
     int pool_has_max;
     Ent pool_max;
     int refill_take;
-    int psel;        // which pool array is current
     int nsurv;
     int stop;
     unsigned long long sel_prefix;
@@ -106,8 +106,9 @@ struct TmArgs {
     int32_t *faces;
     int64_t *stats;
     int4 *fv;            // face vertices (a, b, c) + alive flag, 3n entries
-    Ent *pool;           // global pool, capacity 3n (two arrays, swapped on compaction)
-    Ent *pool2;
+    double *pool_g;      // global pool (struct of arrays): gain
+    int2 *pool_fc;       //   (fid, cand); capacity 3n + B
+
     int32_t *gcursor;    // global cursors when n > 65536
     int32_t *gmc;        // global max-corr cache when it does not fit in shared memory
     int check;           // check_invariants mode (tmfg.py:375-399)
@@ -316,115 +317,244 @@ __device__ __forceinline__ void sort3(int &x, int &y, int &z) {
     if (y < x) { t = x; x = y; y = t; }
 }
 
-__device__ __forceinline__ unsigned long long ent_key_hi(const Ent &e) { return tg_order_key(e.g); }
-__device__ __forceinline__ unsigned long long ent_key_lo(const Ent &e) { return ~(unsigned long long)(unsigned)e.fid; }
+__device__ __forceinline__ void pool_put(const TmArgs &A, unsigned long long *minkey, int idx, const Ent &x) {
+    A.pool_g[idx] = x.g;
+    A.pool_fc[idx] = make_int2(x.fid, x.cand);
+    atomicMin(minkey, tg_order_key(x.g));
+}
 
-
-// Move the largest pool entries into the (short) shared buffer.  Threshold by
-// a most-significant-digit radix walk over the 96-bit key (gain, ~fid): stop at
+// Move the largest pool entries into the (short) shared buffer.  The pool is
+// struct-of-arrays (gain | fid, cand; face vertices come back from fv[fid]) so
+// the selection passes stream 8 bytes per entry.  Threshold by a most-
+// significant-digit radix walk over the 96-bit key (gain, ~fid) that starts at
+// the first byte where the pool's smallest and largest gain keys differ; stop at
 // the first digit boundary whose "all keys above" set is non-empty and fits.
-// Keys are unique, the pool order is irrelevant, so the result is exact.
+// Keys are unique and the pool order is irrelevant, so the result is exact.
+// Taken entries leave holes that are refilled from the pool's tail (O(taken)).
+constexpr int RF_U = 8;   // pool loads in flight per thread in the selection passes
+constexpr int RF_LOG = 11, RF_BINS = 1 << RF_LOG;   // selection histogram bins
+static_assert(RF_BINS * 4 + TM_B / 2 * 20 <= TM_B * (int)sizeof(Ent), "refill scratch overflows the spare buffer");
+
 template <int NT>
 __device__ void refill(const TmArgs &A, Ctl &ctl, Ent *cur, Ent *scratch, Ent *red_e, int *red_ok, int tid) {
     const int lane = tid & 31, warp = tid >> 5;
-    Ent *pool = ctl.psel ? A.pool2 : A.pool;
-    Ent *other = ctl.psel ? A.pool : A.pool2;
     const int P = ctl.pool_count;
     const int room = min(TM_B - ctl.size, TM_B / 2);
+    int *takeidx = reinterpret_cast<int *>(scratch) + RF_BINS;   // room entries (after the histogram)
+    int *holes = takeidx + TM_B / 2;                         // room entries
+    double *tgv = reinterpret_cast<double *>(holes + TM_B / 2);
+    int *tfv = reinterpret_cast<int *>(tgv + TM_B / 2);
     unsigned long long thr_hi = 0ull, thr_lo = 0ull;
-    bool take_all = P <= room;
+    const bool take_all = P <= room;
     if (!take_all) {
-        if (tid == 0) { ctl.sel_prefix = 0ull; ctl.sel_room = room; ctl.stop = 0; }
-        fg_sync();
-        for (int pass = 0; pass < 16; pass++) {
-            const bool lo_part = pass >= 8;
-            const int p = pass & 7;
-            const int shift = 56 - 8 * p;
-            for (int i = tid; i < 256; i += NT) ctl.hist[i] = 0;
+        // Threshold key: linear 2048-bin histograms over the pool's key window
+        // [pool min, pool max] (kept incrementally), refined inside the top bin
+        // only when that bin alone is larger than the room; exact gain ties that
+        // straddle the room fall through to a byte-radix walk over ~fid.
+        int *hist = reinterpret_cast<int *>(scratch);
+        if (tid == 0) { ctl.sel_room = room; ctl.stop = 0; }
+        unsigned long long lo = ctl.pool_minkey, hi = tg_order_key(ctl.pool_max.g);
+        bool need_fid = false, done = false;
+        for (int it = 0; it < 8 && !done; it++) {
+            if (lo >= hi) { thr_hi = hi; need_fid = true; break; }
+            const int nb = 64 - __clzll(hi - lo);
+            const int shift = nb > RF_LOG ? nb - RF_LOG : 0;
+            for (int i = tid; i < RF_BINS; i += NT) hist[i] = 0;
             fg_sync();
-            const unsigned long long pref = ctl.sel_prefix;
-            for (int i = tid; i < P; i += NT) {
-                Ent x = pool[i];
-                unsigned long long kh = ent_key_hi(x), kl = ent_key_lo(x);
-                unsigned long long key = lo_part ? kl : kh;
-                bool match = lo_part ? (kh == thr_hi) : true;
-                if (p > 0) match = match && ((key >> (64 - 8 * p)) == (pref >> (64 - 8 * p)));
-                if (match) atomicAdd(&ctl.hist[(key >> shift) & 255], 1);
+            for (int i0 = tid; i0 < P; i0 += RF_U * NT) {
+                double gv[RF_U];
+#pragma unroll
+                for (int u = 0; u < RF_U; u++) gv[u] = i0 + u * NT < P ? A.pool_g[i0 + u * NT] : -INFINITY;
+#pragma unroll
+                for (int u = 0; u < RF_U; u++) {
+                    const unsigned long long key = tg_order_key(gv[u]);
+                    if (i0 + u * NT < P && key >= lo && key <= hi) atomicAdd(&hist[(int)((key - lo) >> shift)], 1);
+                }
             }
             fg_sync();
-            if (tid == 0) {
-                int acc = 0, d = 255, last_fit = -1;
-                for (; d >= 0; d--) {
-                    if (acc + ctl.hist[d] > ctl.sel_room) break;
-                    acc += ctl.hist[d];
-                    if (ctl.hist[d]) last_fit = d;
+            if (warp == 0) {
+                // lane l owns bins [RF_BINS - (l+1)*PB, RF_BINS - l*PB): suffix sums from the top
+                constexpr int PB = RF_BINS / 32;
+                const int b0 = RF_BINS - (lane + 1) * PB;
+                int s = 0, topnz = -1;
+                for (int q = PB - 1; q >= 0; q--) {
+                    s += hist[b0 + q];
+                    if (topnz < 0 && hist[b0 + q]) topnz = b0 + q;
                 }
-                if (acc > 0) {
-                    // take every key whose digit here is >= last_fit (within the prefix group)
-                    ctl.sel_prefix = pref | ((unsigned long long)last_fit << shift);
-                    ctl.stop = 1;
-                } else {
-                    // the top non-empty bin alone is too large: refine inside it
-                    ctl.sel_prefix = pref | ((unsigned long long)d << shift);
+                int incl = s;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                const int excl = incl - s;   // keys in bins above this lane's chunk
+                const int room_now = ctl.sel_room;
+                // lowest bin whose suffix still fits: inside the first lane whose total exceeds the room
+                const unsigned over = __ballot_sync(0xffffffffu, incl > room_now);
+                const int fl = over ? __ffs(over) - 1 : 31;
+                int best = -1;
+                if (lane == fl) {
+                    int acc = excl;
+                    best = acc > 0 ? b0 + PB : -1;   // everything above this chunk fits
+                    for (int q = PB - 1; q >= 0; q--) {
+                        if (acc + hist[b0 + q] > room_now) break;
+                        acc += hist[b0 + q];
+                        if (acc > 0) best = b0 + q;
+                    }
+                }
+                best = __shfl_sync(0xffffffffu, best, fl);
+                const unsigned nzb = __ballot_sync(0xffffffffu, topnz >= 0);
+                const int top = nzb ? __shfl_sync(0xffffffffu, topnz, __ffs(nzb) - 1) : -1;
+                if (lane == 0) {
+                    if (best >= 0) {
+                        ctl.sel_prefix = lo + ((unsigned long long)best << shift);
+                        ctl.stop = 1;
+                    } else {
+                        ctl.sel_prefix = lo + ((unsigned long long)top << shift);   // refine inside the top bin
+                        ctl.stop = 0;
+                    }
                 }
             }
             fg_sync();
             if (ctl.stop) {
-                if (!lo_part) { thr_hi = ctl.sel_prefix; thr_lo = 0ull; }
-                else thr_lo = ctl.sel_prefix;
-                break;
-            }
-            if (pass == 7) {
                 thr_hi = ctl.sel_prefix;
-                fg_sync();
-                if (tid == 0) ctl.sel_prefix = 0ull;
-                fg_sync();
+                thr_lo = 0ull;
+                done = true;
+            } else {
+                const unsigned long long nlo = ctl.sel_prefix;
+                const unsigned long long nhi = nlo + ((1ull << shift) - 1ull);
+                lo = nlo;
+                hi = nhi < hi ? nhi : hi;
             }
+            fg_sync();
         }
-        if (!ctl.stop) thr_lo = ctl.sel_prefix;
+        if (need_fid) {
+            // all remaining candidates share one gain: select on ~fid bytes
+            if (tid == 0) { ctl.sel_prefix = 0ull; ctl.stop = 0; }
+            fg_sync();
+            for (int pass = 8; pass < 16; pass++) {
+                const int p = pass & 7;
+                const int shift = 56 - 8 * p;
+                for (int i = tid; i < 256; i += NT) ctl.hist[i] = 0;
+                fg_sync();
+                const unsigned long long pref = ctl.sel_prefix;
+                for (int i = tid; i < P; i += NT) {
+                    if (tg_order_key(A.pool_g[i]) != thr_hi) continue;
+                    const unsigned long long key = ~(unsigned long long)(unsigned)A.pool_fc[i].x;
+                    if (p > 0 && (key >> (64 - 8 * p)) != (pref >> (64 - 8 * p))) continue;
+                    atomicAdd(&ctl.hist[(key >> shift) & 255], 1);
+                }
+                fg_sync();
+                if (tid == 0) {
+                    int acc = 0, d = 255, last_fit = -1;
+                    for (; d >= 0; d--) {
+                        if (acc + ctl.hist[d] > ctl.sel_room) break;
+                        acc += ctl.hist[d];
+                        if (ctl.hist[d]) last_fit = d;
+                    }
+                    if (acc > 0) {
+                        ctl.sel_prefix = pref | ((unsigned long long)last_fit << shift);
+                        ctl.stop = 1;
+                    } else {
+                        ctl.sel_prefix = pref | ((unsigned long long)d << shift);
+                    }
+                }
+                fg_sync();
+                if (ctl.stop) break;
+            }
+            thr_lo = ctl.sel_prefix;
+        }
     }
     fg_sync();
     if (tid == 0) { ctl.refill_take = 0; ctl.nsurv = 0; }
     fg_sync();
-    Ent best;
+    // take pass: indices of the selected entries; best (max) of the rest
+    double bg = 0.0;
+    int bf = 0;
     bool ok = false;
-    for (int i = tid; i < P; i += NT) {
-        Ent x = pool[i];
-        unsigned long long kh = ent_key_hi(x), kl = ent_key_lo(x);
-        bool take = take_all || kh > thr_hi || (kh == thr_hi && kl >= thr_lo);
-        if (take) {
-            scratch[atomicAdd(&ctl.refill_take, 1)] = x;
-        } else {
-            other[atomicAdd(&ctl.nsurv, 1)] = x;
-            if (!ok || ent_gt(x, best)) { best = x; ok = true; }
+    for (int i0 = tid; i0 < P; i0 += RF_U * NT) {
+        double gv[RF_U];
+        int fv[RF_U];
+#pragma unroll
+        for (int u = 0; u < RF_U; u++) {
+            const int i = i0 + u * NT;
+            gv[u] = i < P ? A.pool_g[i] : 0.0;
+            fv[u] = i < P ? A.pool_fc[i].x : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < RF_U; u++) {
+            const int i = i0 + u * NT;
+            if (i >= P) continue;
+            const double g = gv[u];
+            const int f = fv[u];
+            const unsigned long long kh = tg_order_key(g), kl = ~(unsigned long long)(unsigned)f;
+            const bool take = take_all || kh > thr_hi || (kh == thr_hi && kl >= thr_lo);
+            if (take) {
+                const int s = atomicAdd(&ctl.refill_take, 1);
+                takeidx[s] = i;
+                tgv[s] = g;
+                tfv[s] = f;
+            } else if (!ok || (g > bg) || (g == bg && f < bf)) {
+                bg = g; bf = f; ok = true;
+            }
         }
     }
     for (int o = 16; o; o >>= 1) {
-        Ent y;
-        y.g = __shfl_xor_sync(0xffffffffu, best.g, o);
-        y.fid = __shfl_xor_sync(0xffffffffu, best.fid, o);
-        int yok = __shfl_xor_sync(0xffffffffu, (int)ok, o);
-        if (yok && (!ok || ent_gt(y, best))) { best.g = y.g; best.fid = y.fid; ok = true; }
+        const double g2 = __shfl_xor_sync(0xffffffffu, bg, o);
+        const int f2 = __shfl_xor_sync(0xffffffffu, bf, o);
+        const int ok2 = __shfl_xor_sync(0xffffffffu, (int)ok, o);
+        if (ok2 && (!ok || g2 > bg || (g2 == bg && f2 < bf))) { bg = g2; bf = f2; ok = true; }
     }
-    if (lane == 0) { red_e[warp] = best; red_ok[warp] = ok; }
+    if (lane == 0) { red_e[warp].g = bg; red_e[warp].fid = bf; red_ok[warp] = ok; }
     fg_sync();
     const int nt = ctl.refill_take;
     const int sz = ctl.size;
-    for (int i = tid; i < nt; i += NT) {
-        Ent x = scratch[i];
+    const int keep = P - nt;
+    // selected entries -> sorted tail of the buffer; holes below `keep` listed
+    for (int s = tid; s < nt; s += NT) {
+        const double g = tgv[s];
+        const int f = tfv[s];
         int rank = 0;
-        for (int j = 0; j < nt; j++) rank += ent_gt(scratch[j], x);
+        for (int j = 0; j < nt; j++) rank += (tgv[j] > g) | ((tgv[j] == g) & (tfv[j] < f));
+        const int i = takeidx[s];
+        const int2 fc = A.pool_fc[i];
+        const int4 fvv = A.fv[fc.x];
+        Ent x;
+        x.g = g;
+        x.fid = fc.x;
+        x.cand = fc.y;
+        x.a = fvv.x;
+        x.b = fvv.y;
+        x.c = fvv.z;
+        x.opt = 0;
         cur[sz + rank] = x;
+        if (i < keep) holes[atomicAdd(&ctl.nsurv, 1)] = i;
+    }
+    fg_sync();
+    // fill the holes with the surviving entries of the tail [keep, P) (any pairing)
+    if (tid == 0) ctl.nsurv = 0;
+    fg_sync();
+    for (int i = keep + tid; i < P; i += NT) {
+        const double g = A.pool_g[i];
+        const int2 fc = A.pool_fc[i];
+        const unsigned long long kh = tg_order_key(g), kl = ~(unsigned long long)(unsigned)fc.x;
+        if (!(take_all || kh > thr_hi || (kh == thr_hi && kl >= thr_lo))) {
+            const int h = holes[atomicAdd(&ctl.nsurv, 1)];
+            A.pool_g[h] = g;
+            A.pool_fc[h] = fc;
+        }
     }
     fg_sync();
     if (tid == 0) {
         ctl.size = sz + nt;
-        ctl.pool_count = ctl.nsurv;
-        ctl.psel ^= 1;
+        ctl.pool_count = keep;
+        if (keep == 0) ctl.pool_minkey = ~0ull;
         bool any = false;
         Ent b;
         for (int w = 0; w < NT / 32; w++)
-            if (red_ok[w] && (!any || ent_gt(red_e[w], b))) { b = red_e[w]; any = true; }
+            if (red_ok[w] && (!any || red_e[w].g > b.g || (red_e[w].g == b.g && red_e[w].fid < b.fid))) {
+                b = red_e[w];
+                any = true;
+            }
         ctl.pool_has_max = any;
         if (any) ctl.pool_max = b;
     }
@@ -566,11 +696,10 @@ __device__ void replay_warp(const TmArgs &A, Ctl &ctl, const Ent *L, const Ent *
     // keys of the buffer-bound entries (src >= 0: Lref index, src < 0: ~NE index)
     if (fr) { const int o = __popc(bfr & lt); kg[o] = rg; kf[o] = rf; ksrc[o] = lane; }
     if (fnn) { const int o = nfr + __popc(bfn & lt); kg[o] = nlg; kf[o] = nlf; ksrc[o] = ~lane; }
-    Ent *pool = ctl.psel ? A.pool2 : A.pool;
     const int pc = ctl.pool_count;
     const int npr = __popc(bpr);
-    if (pr) pool[pc + __popc(bpr & lt)] = Lref[lane];
-    if (pn) pool[pc + npr + __popc(bpn & lt)] = NE[lane];
+    if (pr) pool_put(A, &ctl.pool_minkey, pc + __popc(bpr & lt), Lref[lane]);
+    if (pn) pool_put(A, &ctl.pool_minkey, pc + npr + __popc(bpn & lt), NE[lane]);
     __syncwarp();
     if (lane == 0) {
         ctl.pool_count = pc + npr + __popc(bpn);
@@ -713,8 +842,8 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
         ctl.L_count = 0;
         ctl.pops = ctl.refreshes = ctl.gain_inc = 0;
         ctl.pool_count = 0;
+        ctl.pool_minkey = ~0ull;
         ctl.pool_has_max = 0;
-        ctl.psel = 0;
         ctl.done = (n <= 4);
         ctl.bad = 0;
         ctl.bg_stop = 0;
@@ -822,8 +951,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
                 int pos = i + lo;
                 if (pos < TM_B) nxt[pos] = x;
                 else {
-                    Ent *pool = ctl.psel ? A.pool2 : A.pool;
-                    pool[atomicAdd(&ctl.pool_count, 1)] = x;
+                    pool_put(A, &ctl.pool_minkey, atomicAdd(&ctl.pool_count, 1), x);
                     if (pos == TM_B) { ctl.pool_max = x; ctl.pool_has_max = 1; }
                 }
             }
@@ -838,8 +966,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
                 int pos = k + lo;
                 if (pos < TM_B) nxt[pos] = x;
                 else {
-                    Ent *pool = ctl.psel ? A.pool2 : A.pool;
-                    pool[atomicAdd(&ctl.pool_count, 1)] = x;
+                    pool_put(A, &ctl.pool_minkey, atomicAdd(&ctl.pool_count, 1), x);
                     if (pos == TM_B) { ctl.pool_max = x; ctl.pool_has_max = 1; }
                 }
             }
@@ -997,9 +1124,9 @@ TG_API int tg_edge_weights(const double *S, int64_t n, const int32_t *edges, int
 TG_API size_t tg_tmfg_workspace_bytes(int64_t n) {
     size_t b = 0;
     b += tg_align_up((size_t)3 * n * sizeof(int4), 256);
-    b += tg_align_up((size_t)(3 * n + TM_B + 64) * sizeof(Ent), 256);
+    b += tg_align_up((size_t)(3 * n + TM_B + 64) * sizeof(double), 256);
+    b += tg_align_up((size_t)(3 * n + TM_B + 64) * sizeof(int2), 256);
     b += tg_align_up((size_t)n * sizeof(int32_t), 256) * 2;
-    b += tg_align_up((size_t)(3 * n + TM_B + 64) * sizeof(Ent), 256);
     return b + 1024;
 }
 
@@ -1021,11 +1148,11 @@ TG_API int tg_tmfg_heap(const double *S, const int32_t *order, int64_t n, const 
     A.stats = stats;
     A.check = check;
     A.fv = ar.take<int4>((size_t)3 * n);
-    A.pool = ar.take<Ent>((size_t)3 * n + TM_B + 64);
-    A.pool2 = ar.take<Ent>((size_t)3 * n + TM_B + 64);
+    A.pool_g = ar.take<double>((size_t)3 * n + TM_B + 64);
+    A.pool_fc = ar.take<int2>((size_t)3 * n + TM_B + 64);
     A.gcursor = ar.take<int32_t>((size_t)n);
     A.gmc = ar.take<int32_t>((size_t)n);
-    if (!A.fv || !A.pool || !A.pool2 || !A.gcursor || !A.gmc) return TG_ERR_WORKSPACE;
+    if (!A.fv || !A.pool_g || !A.pool_fc || !A.gcursor || !A.gmc) return TG_ERR_WORKSPACE;
     cudaStream_t st = tg_stream(stream);
     const bool smem_cur = n <= 65535;
     const bool smem_mc = smem_cur && tm_smem_bytes(n, true, true) <= 200 * 1024;
