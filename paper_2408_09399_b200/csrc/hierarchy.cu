@@ -32,7 +32,21 @@ struct DevBuf {
     }
     cudaError_t alloc(size_t bytes, cudaStream_t s) {
         st = s;
+        keep_pool_memory();
         return cudaMallocAsync(&p, bytes ? bytes : 16, s);
+    }
+    // the default pool returns freed memory to the OS at every synchronisation
+    // (release threshold 0): keep it, so per-layer buffers are recycled cheaply
+    static void keep_pool_memory() {
+        static thread_local int dev_done = -1;
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || dev == dev_done) return;
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = 1ull << 30;   // keep up to 1 GiB cached
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        dev_done = dev;
     }
     template <class T>
     T *as() const { return reinterpret_cast<T *>(p); }
