@@ -79,6 +79,7 @@ struct Ctl {
     int pool_has_max;
     Ent pool_max;
     int refill_take;
+    int need_refill;
     int nsurv;
     int stop;
     unsigned long long sel_prefix;
@@ -867,13 +868,14 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
     const int warp = (TM_WARPS - 1) - (threadIdx.x >> 5);
     const int tid = warp * 32 + lane;
     long long tc0 = clock64(), tc1;
+    int sel = 0;   // which half of the queue buffer is current (tracked by every foreground thread)
     while (!ctl.done) {
         if (tid == 0) { tc0 = clock64(); ctl.rounds++; }
         // ================= parallel phase: new-face entries + speculative refresh of the top-K
         int my_iters[4] = {0, 0, 0, 0};
         long long tpw0 = clock64();
         {
-            Ent *cur = ctl.sel ? buf1 : buf0;
+            Ent *cur = sel ? buf1 : buf0;
             if (warp < TM_NEW_WARPS) {
                 if (warp < ctl.ne_count) {
                     int fids[1] = {ctl.ne_fid[warp]};
@@ -934,110 +936,106 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
             ctl.it_round_max = 0;
             for (int q = 0; q < 4; q++) { ctl.phs[q] += ctl.ph[q]; ctl.ph[q] = 0; }
         }
-        // ================= merge: buffer[removed..size) + tobuf -> other half
+        // ================= merge buffer[removed..size) + tobuf -> other half (warps 1..),
+        // while thread 0 inserts the winner and settles the queue size: both only
+        // depend on the replay's results, so one barrier closes the round
         {
-            Ent *cur = ctl.sel ? buf1 : buf0;
-            Ent *nxt = ctl.sel ? buf0 : buf1;
             const int r = ctl.removed, sz = ctl.size, nb = ctl.nbuf_new;
-            const int old = sz - r;
-            for (int i = tid; i < old; i += TM_FG_T) {
-                Ent x = cur[r + i];
-                int lo = 0, hi = nb;  // # of tobuf entries popping before x
-                while (lo < hi) {
-                    int mid = (lo + hi) >> 1;
-                    if (ent_gt(tobuf[mid], x)) lo = mid + 1;
-                    else hi = mid;
+            if (warp > 0) {
+                Ent *cur = sel ? buf1 : buf0;
+                Ent *nxt = sel ? buf0 : buf1;
+                const int old = sz - r;
+                const int mt = tid - 32;
+                constexpr int MT = TM_FG_T - 32;
+                for (int i = mt; i < old; i += MT) {
+                    Ent x = cur[r + i];
+                    int lo = 0, hi = nb;  // # of tobuf entries popping before x
+                    while (lo < hi) {
+                        int mid = (lo + hi) >> 1;
+                        if (ent_gt(tobuf[mid], x)) lo = mid + 1;
+                        else hi = mid;
+                    }
+                    int pos = i + lo;
+                    if (pos < TM_B) nxt[pos] = x;
+                    else {
+                        pool_put(A, &ctl.pool_minkey, atomicAdd(&ctl.pool_count, 1), x);
+                        if (pos == TM_B) { ctl.pool_max = x; ctl.pool_has_max = 1; }
+                    }
                 }
-                int pos = i + lo;
-                if (pos < TM_B) nxt[pos] = x;
-                else {
-                    pool_put(A, &ctl.pool_minkey, atomicAdd(&ctl.pool_count, 1), x);
-                    if (pos == TM_B) { ctl.pool_max = x; ctl.pool_has_max = 1; }
+                for (int k = mt; k < nb; k += MT) {
+                    Ent x = tobuf[k];
+                    int lo = 0, hi = old;  // # of old entries popping before x
+                    while (lo < hi) {
+                        int mid = (lo + hi) >> 1;
+                        if (ent_gt(cur[r + mid], x)) lo = mid + 1;
+                        else hi = mid;
+                    }
+                    int pos = k + lo;
+                    if (pos < TM_B) nxt[pos] = x;
+                    else {
+                        pool_put(A, &ctl.pool_minkey, atomicAdd(&ctl.pool_count, 1), x);
+                        if (pos == TM_B) { ctl.pool_max = x; ctl.pool_has_max = 1; }
+                    }
                 }
-            }
-            for (int k = tid; k < nb; k += TM_FG_T) {
-                Ent x = tobuf[k];
-                int lo = 0, hi = old;  // # of old entries popping before x
-                while (lo < hi) {
-                    int mid = (lo + hi) >> 1;
-                    if (ent_gt(cur[r + mid], x)) lo = mid + 1;
-                    else hi = mid;
+            } else if (lane == 0) {
+                // spilled entries (total > B) are the smallest of the buffer; then no refill
+                const int total = min(sz - r + nb, TM_B);
+                ctl.size = total;
+                ctl.sel = sel ^ 1;
+                ctl.need_refill = total < TM_K && ctl.pool_count > 0;
+                ctl.L_count = min(TM_K, total);
+                // ================= insert the winner (tmfg.py:94-143 bookkeeping)
+                ctl.ne_count = 0;
+                if (ctl.winner) {
+                    Ent w = ctl.win;
+                    int v = w.cand, fid = w.fid;
+                    int a = w.a, b = w.b, c = w.c;
+                    int t = ctl.nt;
+                    A.trace[4 * t] = v;
+                    A.trace[4 * t + 1] = a;
+                    A.trace[4 * t + 2] = b;
+                    A.trace[4 * t + 3] = c;
+                    A.host_fid[t] = fid;
+                    int e = 6 + 3 * t;
+                    int wv[3] = {a, b, c};
+                    for (int q = 0; q < 3; q++) {
+                        A.edges[2 * (e + q)] = min(wv[q], v);
+                        A.edges[2 * (e + q) + 1] = max(wv[q], v);
+                    }
+                    int4 old = A.fv[fid];
+                    A.fv[fid] = make_int4(old.x, old.y, old.z, 0);
+                    int f0 = ctl.nf;
+                    int ch[3][3] = {{v, a, b}, {v, a, c}, {v, b, c}};
+                    for (int q = 0; q < 3; q++) {
+                        int x = ch[q][0], y = ch[q][1], z = ch[q][2];
+                        sort3(x, y, z);
+                        A.fv[f0 + q] = make_int4(x, y, z, 1);
+                        ctl.ne_fid[q] = f0 + q;
+                        ctl.ne_v[q][0] = x;
+                        ctl.ne_v[q][1] = y;
+                        ctl.ne_v[q][2] = z;
+                    }
+                    ctl.nf = f0 + 3;
+                    bits[v >> 5] |= 1u << (v & 31);
+                    ctl.nt = t + 1;
+                    ctl.rem -= 1;
+                    if (ctl.rem == 0) ctl.done = 1;
+                    else ctl.ne_count = 3;
                 }
-                int pos = k + lo;
-                if (pos < TM_B) nxt[pos] = x;
-                else {
-                    pool_put(A, &ctl.pool_minkey, atomicAdd(&ctl.pool_count, 1), x);
-                    if (pos == TM_B) { ctl.pool_max = x; ctl.pool_has_max = 1; }
-                }
+                if (ctl.bad) ctl.done = 1;
             }
         }
-        fg_sync();
-        if (tid == 0) {
-            int total = ctl.size - ctl.removed + ctl.nbuf_new;
-            if (total > TM_B) {
-                // spilled entries are the smallest of the buffer: the pool max is
-                // the largest spilled one, i.e. the entry right after the kept tail
-                total = TM_B;
-            }
-            ctl.size = total;
-            ctl.sel ^= 1;
-        }
+        sel ^= 1;
         tc1 = fg_sync_clock();
-        // ================= insert the winner
-        if (tid == 0) {
-            ctl.t_merge += tc1 - tc0;
-            tc0 = tc1;
-            ctl.ne_count = 0;
-            if (ctl.winner) {
-                Ent w = ctl.win;
-                int v = w.cand, fid = w.fid;
-                int a = w.a, b = w.b, c = w.c;
-                int t = ctl.nt;
-                A.trace[4 * t] = v;
-                A.trace[4 * t + 1] = a;
-                A.trace[4 * t + 2] = b;
-                A.trace[4 * t + 3] = c;
-                A.host_fid[t] = fid;
-                int e = 6 + 3 * t;
-                int wv[3] = {a, b, c};
-                for (int q = 0; q < 3; q++) {
-                    A.edges[2 * (e + q)] = min(wv[q], v);
-                    A.edges[2 * (e + q) + 1] = max(wv[q], v);
-                }
-                int4 old = A.fv[fid];
-                A.fv[fid] = make_int4(old.x, old.y, old.z, 0);
-                int f0 = ctl.nf;
-                int ch[3][3] = {{v, a, b}, {v, a, c}, {v, b, c}};
-                for (int q = 0; q < 3; q++) {
-                    int x = ch[q][0], y = ch[q][1], z = ch[q][2];
-                    sort3(x, y, z);
-                    A.fv[f0 + q] = make_int4(x, y, z, 1);
-                    ctl.ne_fid[q] = f0 + q;
-                    ctl.ne_v[q][0] = x;
-                    ctl.ne_v[q][1] = y;
-                    ctl.ne_v[q][2] = z;
-                }
-                ctl.nf = f0 + 3;
-                bits[v >> 5] |= 1u << (v & 31);
-                ctl.nt = t + 1;
-                ctl.rem -= 1;
-                if (ctl.rem == 0) ctl.done = 1;
-                else ctl.ne_count = 3;
-            }
-            if (ctl.bad) ctl.done = 1;
-        }
-        tc1 = fg_sync_clock();
-        if (tid == 0) { ctl.t_insert += tc1 - tc0; tc0 = tc1; }
+        if (tid == 0) { ctl.t_merge += tc1 - tc0; tc0 = tc1; }
         if (ctl.done) break;
         // ================= refill the shared buffer from the pool when short
-        if (ctl.size < TM_K && ctl.pool_count > 0) {
-            refill<TM_FG_T>(A, ctl, ctl.sel ? buf1 : buf0, ctl.sel ? buf0 : buf1, red_e, red_ok, tid);
+        if (ctl.need_refill) {
+            refill<TM_FG_T>(A, ctl, sel ? buf1 : buf0, sel ? buf0 : buf1, red_e, red_ok, tid);
+            if (tid == 0) ctl.L_count = min(TM_K, ctl.size);
             tc1 = fg_sync_clock();
             if (tid == 0) { ctl.t_refill += tc1 - tc0; ctl.refills++; tc0 = tc1; }
         }
-        if (tid == 0) ctl.L_count = min(TM_K, ctl.size);
-        tc1 = fg_sync_clock();
-        if (tid == 0) ctl.t_tail += tc1 - tc0;
     }
     fg_sync();
         if (tid == 0) *((volatile int *)&ctl.bg_stop) = 1;
