@@ -32,6 +32,12 @@
 
 namespace {
 
+// TM_PROFILE=1 (make PROFILE=1): per-warp phase clocks of the parallel phase
+// (tools/tmfg_profile.py); the round-level phase clocks are always on.
+#ifndef TM_PROFILE
+#define TM_PROFILE 0
+#endif
+
 constexpr int TM_T = 1024;
 constexpr int TM_WARPS = TM_T / 32;
 constexpr int TM_BG_WARPS = 4;                   // background cursor-advancing warps
@@ -178,7 +184,9 @@ __device__ void warp_entries(const TmArgs &A, const uint32_t *bits, uint16_t *sc
         }
     }
     const unsigned scanned = pending;
+#if TM_PROFILE
     long long tw0 = clock64();
+#endif
     {
         int val[NV][4];
 #pragma unroll
@@ -209,7 +217,9 @@ __device__ void warp_entries(const TmArgs &A, const uint32_t *bits, uint16_t *sc
             }
         }
     }
+#if TM_PROFILE
     long long tw1 = clock64() + (found[0] & 0);
+#endif
     while (pending) {
         (*iters)++;
         const int k = __ffs(pending) - 1;
@@ -248,7 +258,9 @@ __device__ void warp_entries(const TmArgs &A, const uint32_t *bits, uint16_t *sc
                 mc_set<SMEM_MC>(smc, A.gmc, vv[k], found[k]);
             }
     }
+#if TM_PROFILE
     long long tw2 = clock64() + (found[0] & 0);
+#endif
     // 9 similarity loads per entry: lane = e*9 + ci*3 + vi loads S[face_vi, cand_ci]
     double sv = 0.0;
     int my_u = -1;
@@ -265,8 +277,10 @@ __device__ void warp_entries(const TmArgs &A, const uint32_t *bits, uint16_t *sc
     }
     // lanes with vi == 0 form g = (S[a,u] + S[b,u]) + S[c,u]  (tmfg.py:273, left to right)
     const double s1 = __shfl_down_sync(0xffffffffu, sv, 1);
+#if TM_PROFILE
     long long tw3 = clock64() + (long long)(s1 != s1);
     if (lane == 0) { iters[1] = (int)(tw1 - tw0); iters[2] = (int)(tw2 - tw1); iters[3] = (int)(tw3 - tw2); }
+#endif
     const double s2 = __shfl_down_sync(0xffffffffu, sv, 2);
     const double g = __dadd_rn(__dadd_rn(sv, s1), s2);
     // entry leader (lane e*9) picks the best of its 3 candidates: g desc, u asc
@@ -873,7 +887,9 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
         if (tid == 0) { tc0 = clock64(); ctl.rounds++; }
         // ================= parallel phase: new-face entries + speculative refresh of the top-K
         int my_iters[4] = {0, 0, 0, 0};
+#if TM_PROFILE
         long long tpw0 = clock64();
+#endif
         {
             Ent *cur = sel ? buf1 : buf0;
             if (warp < TM_NEW_WARPS) {
@@ -913,6 +929,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
                 }
             }
         }
+#if TM_PROFILE
         if (lane == 0 && my_iters[0]) atomicMax(&ctl.it_round_max, my_iters[0]);
         if (lane == 0) {
             atomicMax(&ctl.ph[1], my_iters[1]);
@@ -920,6 +937,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
             atomicMax(&ctl.ph[3], my_iters[3]);
             atomicMax(&ctl.ph[0], (int)(clock64() - tpw0));
         }
+#endif
         tc1 = fg_sync_clock();
         // ================= replay the pops (warp 0, exact sequential semantics)
         if (tid == 0) {
