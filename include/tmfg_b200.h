@@ -99,7 +99,7 @@ int tg_initial_clique_screened(const double *S, int64_t n, const double *screen,
 
 /* tmfg.py:344-436 build_tmfg_heap (+ tmfg.py:94-182 bookkeeping).
  * Outputs: trace (n-4, 4), host_fid (n-4) face id each row subdivided,
- * edges (3n-6, 2), faces (2n-4, 3) int32; stats int64[24] =
+ * edges (3n-6, 2), faces (2n-4, 3) int32; stats int64[32] =
  * {pops, refreshes, gain_increases, status, assert_fid, assert_old_gain_bits,
  *  assert_new_gain_bits, then kernel self-profile counters (rounds, refills,
  *  per-phase cycles; see tools/tmfg_profile.py)}.  status 0 = ok, 2 = the check_invariants

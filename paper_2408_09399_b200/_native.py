@@ -15,6 +15,8 @@ import numpy as np
 
 _LIB_DIR = Path(__file__).resolve().parent / "_lib"
 LIB_PATH = _LIB_DIR / "libtmfg_b200.so"
+if os.environ.get("TG_LIB"):   # developer override (e.g. the TM_PROFILE build used by tools/tmfg_profile.py)
+    LIB_PATH = Path(os.environ["TG_LIB"])
 
 TG_OK = 0
 TG_ERR_NOT_REDUCIBLE = 7

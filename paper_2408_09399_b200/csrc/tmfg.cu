@@ -99,6 +99,7 @@ struct Ctl {
     int ph[4];
     long long phs[4];
     long long pops_dbg;
+    long long rf_t[4];   // refill phases: select, take, place, hole fill (TM_PROFILE)
     long long it_total, it_maxsum;
 };
 
@@ -355,6 +356,9 @@ __device__ void refill(const TmArgs &A, Ctl &ctl, Ent *cur, Ent *scratch, Ent *r
     const int lane = tid & 31, warp = tid >> 5;
     const int P = ctl.pool_count;
     const int room = min(TM_B - ctl.size, TM_B / 2);
+#if TM_PROFILE
+    long long rc0 = fg_sync_clock(), rc1;
+#endif
     int *takeidx = reinterpret_cast<int *>(scratch) + RF_BINS;   // room entries (after the histogram)
     int *holes = takeidx + TM_B / 2;                         // room entries
     double *tgv = reinterpret_cast<double *>(holes + TM_B / 2);
@@ -479,6 +483,10 @@ __device__ void refill(const TmArgs &A, Ctl &ctl, Ent *cur, Ent *scratch, Ent *r
             thr_lo = ctl.sel_prefix;
         }
     }
+#if TM_PROFILE
+    rc1 = fg_sync_clock();
+    if (tid == 0) { ctl.rf_t[0] += rc1 - rc0; rc0 = rc1; }
+#endif
     fg_sync();
     if (tid == 0) { ctl.refill_take = 0; ctl.nsurv = 0; }
     fg_sync();
@@ -521,6 +529,10 @@ __device__ void refill(const TmArgs &A, Ctl &ctl, Ent *cur, Ent *scratch, Ent *r
     }
     if (lane == 0) { red_e[warp].g = bg; red_e[warp].fid = bf; red_ok[warp] = ok; }
     fg_sync();
+#if TM_PROFILE
+    rc1 = fg_sync_clock();
+    if (tid == 0) { ctl.rf_t[1] += rc1 - rc0; rc0 = rc1; }
+#endif
     const int nt = ctl.refill_take;
     const int sz = ctl.size;
     const int keep = P - nt;
@@ -546,6 +558,10 @@ __device__ void refill(const TmArgs &A, Ctl &ctl, Ent *cur, Ent *scratch, Ent *r
     }
     fg_sync();
     // fill the holes with the surviving entries of the tail [keep, P) (any pairing)
+#if TM_PROFILE
+    rc1 = fg_sync_clock();
+    if (tid == 0) { ctl.rf_t[2] += rc1 - rc0; rc0 = rc1; }
+#endif
     if (tid == 0) ctl.nsurv = 0;
     fg_sync();
     for (int i = keep + tid; i < P; i += NT) {
@@ -559,6 +575,10 @@ __device__ void refill(const TmArgs &A, Ctl &ctl, Ent *cur, Ent *scratch, Ent *r
         }
     }
     fg_sync();
+#if TM_PROFILE
+    rc1 = fg_sync_clock();
+    if (tid == 0) { ctl.rf_t[3] += rc1 - rc0; rc0 = rc1; }
+#endif
     if (tid == 0) {
         ctl.size = sz + nt;
         ctl.pool_count = keep;
@@ -866,6 +886,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
         ctl.it_round_max = 0;
         for (int q = 0; q < 4; q++) { ctl.ph[q] = 0; ctl.phs[q] = 0; }
         ctl.pops_dbg = 0;
+        ctl.rf_t[0] = ctl.rf_t[1] = ctl.rf_t[2] = ctl.rf_t[3] = 0;
         ctl.it_total = ctl.it_maxsum = 0;
     }
     __syncthreads();
@@ -1110,6 +1131,10 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
         A.stats[18] = ctl.t_merge;
         A.stats[19] = ctl.t_insert;
         A.stats[20] = ctl.t_tail;
+        A.stats[24] = ctl.rf_t[0];
+        A.stats[25] = ctl.rf_t[1];
+        A.stats[26] = ctl.rf_t[2];
+        A.stats[27] = ctl.rf_t[3];
     }
 }
 

@@ -162,7 +162,7 @@ def build_tmfg_heap_device(Sd, order_dev, clique_dev, check_invariants: bool = F
     host_fid = D.empty((max(n - 4, 0),), t.int32)
     edges = D.empty((3 * n - 6, 2), t.int32)
     faces = D.empty((2 * n - 4, 3), t.int32)
-    stats = D.empty((24,), t.int64)
+    stats = D.empty((32,), t.int64)
     ws = D.Workspace.get(N.size("tg_tmfg_workspace_bytes", n))
     N.call("tg_tmfg_heap", N.ptr(Sd), N.ptr(order_dev), n, N.ptr(clique_dev), N.ptr(trace), N.ptr(host_fid),
            N.ptr(edges), N.ptr(faces), N.ptr(stats), 1 if check_invariants else 0, N.ptr(ws), ws.numel(),

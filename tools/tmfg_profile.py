@@ -1,7 +1,10 @@
 """Time the TMFG kernel at config-3 size and print its internal phase profile."""
-import sys, time, json
+import os, sys, time, json
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+_prof = Path(__file__).resolve().parent.parent / "paper_2408_09399_b200" / "_lib" / "libtmfg_b200_prof.so"
+if _prof.exists():   # built by `make -C paper_2408_09399_b200/csrc PROFILE=1`
+    os.environ.setdefault("TG_LIB", str(_prof))
 import torch
 from paper_2408_09399_b200 import simmatrix, synth, tmfg, _native as N
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 10000
@@ -16,7 +19,7 @@ for rep in range(2):
     out = tmfg.build_tmfg_heap_device(S, order, clique)
     torch.cuda.synchronize(); dt = time.perf_counter() - t0
 st = out["stats"].cpu().numpy()
-names = ["pops", "refreshes", "gain_inc", "status", "a4", "a5", "a6", "tails", "rounds", "refills", "cyc_warp_max", "cyc_probe_max", "cyc_tail_max", "cyc_S_max", "cyc_refill", "pool", "cyc_par", "cyc_replay", "cyc_merge", "cyc_insert", "cyc_tail", "tail_iters_ne", "tail_iters_ref"]
+names = ["pops", "refreshes", "gain_inc", "status", "a4", "a5", "a6", "tails", "rounds", "refills", "cyc_warp_max", "cyc_probe_max", "cyc_tail_max", "cyc_S_max", "cyc_refill", "pool", "cyc_par", "cyc_replay", "cyc_merge", "cyc_insert", "cyc_tail", "s21", "s22", "s23", "rf_select", "rf_take", "rf_place", "rf_fill"]
 d = {k: int(v) for k, v in zip(names, st)}
 d["ms"] = dt * 1e3
 d["us_per_insert"] = dt * 1e6 / (n - 4)
