@@ -252,6 +252,12 @@ int tg_build_hierarchy(const tg_oracle_t *oracle, const int64_t *vertex_bubble, 
                        int64_t n, int64_t *lefts_out, int64_t *rights_out, double *heights_out, int64_t *sizes_out,
                        int64_t *n_merges_out, void *stream);
 
+/* linkage.py:181-187 serialize_dendrogram (HOST arrays): "left right height size\n"
+ * per merge, height as %.17g (== Python "{:.17g}").  Needed length in *len_out;
+ * TG_ERR_CAPACITY when it exceeds cap. */
+int tg_serialize_dendrogram(const int64_t *lefts, const int64_t *rights, const double *heights, const int64_t *sizes,
+                            int64_t k, char *out, size_t cap, size_t *len_out);
+
 #ifdef __cplusplus
 }
 #endif

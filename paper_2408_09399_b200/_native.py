@@ -100,6 +100,7 @@ _PROTOS = {
     "tg_group_max_batch": (ctypes.c_int, [ctypes.POINTER(TgOracle), c_p, c_p, c_p, c_i64, c_p, c_i64, c_p, c_i64,
                                           c_p, c_sz, c_p]),
     "tg_nn_chain_batch": (ctypes.c_int, [c_p, c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p]),
+    "tg_serialize_dendrogram": (ctypes.c_int, [c_p, c_p, c_p, c_p, c_i64, c_p, c_sz, ctypes.POINTER(c_sz)]),
     "tg_build_hierarchy": (ctypes.c_int, [ctypes.POINTER(TgOracle), c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_p]),
 }
 

@@ -11,7 +11,9 @@
 #include "common.cuh"
 
 #include <algorithm>
+#include <charconv>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <vector>
 
@@ -392,4 +394,32 @@ TG_API int tg_build_hierarchy(const tg_oracle_t *oracle, const int64_t *vertex_b
     } catch (...) {   // std::bad_alloc: no C++ exception crosses the ABI
         return TG_ERR_ARG;
     }
+}
+
+// linkage.py:181-187 serialize_dendrogram: "left right height size\n" per merge,
+// height with 17 significant digits (Python's "{:.17g}" == C's "%.17g": both
+// correctly rounded, same exponent style).  Host arrays; writes at most `cap`
+// bytes to out and the needed length to *len_out (TG_ERR_CAPACITY if larger).
+TG_API int tg_serialize_dendrogram(const int64_t *lefts, const int64_t *rights, const double *heights,
+                                   const int64_t *sizes, int64_t k, char *out, size_t cap, size_t *len_out) {
+    if (k < 0 || !len_out || (k > 0 && (!lefts || !rights || !heights || !sizes))) return TG_ERR_ARG;
+    size_t used = 0;
+    char line[128];
+    for (int64_t t = 0; t < k; t++) {
+        // std::to_chars(general, 17) is printf's "%.17g" (correctly rounded), much faster
+        char *p = line, *end = line + sizeof(line);
+        p = std::to_chars(p, end, (long long)lefts[t]).ptr;
+        *p++ = ' ';
+        p = std::to_chars(p, end, (long long)rights[t]).ptr;
+        *p++ = ' ';
+        p = std::to_chars(p, end, heights[t], std::chars_format::general, 17).ptr;
+        *p++ = ' ';
+        p = std::to_chars(p, end, (long long)sizes[t]).ptr;
+        *p++ = '\n';
+        const int w = (int)(p - line);
+        if (out && used + (size_t)w <= cap) std::memcpy(out + used, line, (size_t)w);
+        used += (size_t)w;
+    }
+    *len_out = used;
+    return (out && used > cap) ? TG_ERR_CAPACITY : TG_OK;
 }

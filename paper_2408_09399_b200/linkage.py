@@ -182,6 +182,26 @@ def cut(dendrogram: Dendrogram, k: int) -> np.ndarray:
 
 
 def serialize_dendrogram(d: Dendrogram) -> str:
-    """Text rows "left right height size", one merge per line (linkage.py:181-187)."""
-    lines = [f"{int(a)} {int(b)} {h:.17g} {int(s)}" for a, b, h, s in zip(d.lefts, d.rights, d.heights, d.sizes)]
-    return "\n".join(lines) + ("\n" if lines else "")
+    """Text rows "left right height size", one merge per line (linkage.py:181-187).
+
+    Formatted by the library's C++ side (``tg_serialize_dendrogram``: %.17g is
+    Python's "{:.17g}"); the dendrogram digest of the pipeline hashes this text.
+    """
+    import ctypes
+
+    k = int(d.lefts.shape[0])
+    if k == 0:
+        return ""
+    cols = [np.ascontiguousarray(d.lefts, dtype=np.int64), np.ascontiguousarray(d.rights, dtype=np.int64),
+            np.ascontiguousarray(d.heights, dtype=np.float64), np.ascontiguousarray(d.sizes, dtype=np.int64)]
+    ptrs = [c.ctypes.data_as(ctypes.c_void_p) for c in cols]
+    cap = 80 * k
+    buf = ctypes.create_string_buffer(cap)
+    need = ctypes.c_size_t(0)
+    lib = N.load(require_cuda=False)
+    rc = lib.tg_serialize_dendrogram(*ptrs, k, buf, cap, ctypes.byref(need))
+    if rc == N.TG_ERR_CAPACITY:
+        buf = ctypes.create_string_buffer(need.value)
+        rc = lib.tg_serialize_dendrogram(*ptrs, k, buf, need.value, ctypes.byref(need))
+    N.check("tg_serialize_dendrogram", rc)
+    return buf.raw[: need.value].decode()

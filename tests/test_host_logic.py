@@ -91,3 +91,21 @@ def test_synth_configs_are_deterministic():
         assert a.shape == (120, synth.CONFIGS[cfg].length)
     x, lab = synth.generate(4, n=100)
     assert set(np.unique(x).tolist()) <= {-3.0, -2.0, -1.0, 0.0, 1.0, 2.0, 3.0}
+
+
+def test_serialize_dendrogram_matches_python_format():
+    """The C++ serializer is byte-identical to linkage.py:181-187's f"{h:.17g}" rows."""
+    from paper_2408_09399_b200 import linkage
+    rng = np.random.default_rng(5)
+    k = 4000
+    h = rng.standard_normal(k) * 10.0 ** rng.integers(-300, 300, k)
+    h[:20] = [0.0, -0.0, 1e-12, 9.999999999999999e-13, 1.0, 0.1, 1e300, 5e-324, 2.5, 100.0, 1e16,
+              123456789012345678.0, np.inf, -np.inf, 1e17, 1e-5, 1e-4, 123456.7, 1.7976931348623157e308,
+              2.2250738585072014e-308]
+    d = linkage.Dendrogram(n_leaves=k + 1, lefts=rng.integers(0, 10**6, k), rights=rng.integers(0, 10**6, k),
+                           heights=h, sizes=rng.integers(2, 10**5, k))
+    ref = "\n".join(f"{int(a)} {int(b)} {x:.17g} {int(s)}" for a, b, x, s in zip(d.lefts, d.rights, d.heights, d.sizes))
+    assert linkage.serialize_dendrogram(d) == ref + "\n"
+    empty = linkage.Dendrogram(n_leaves=1, lefts=np.zeros(0, np.int64), rights=np.zeros(0, np.int64),
+                               heights=np.zeros(0), sizes=np.zeros(0, np.int64))
+    assert linkage.serialize_dendrogram(empty) == ""
