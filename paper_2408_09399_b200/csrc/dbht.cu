@@ -556,101 +556,150 @@ __global__ void oracle_block_kernel(tg_oracle_t o, const int32_t *rows, int64_t 
     out[e] = q ? oracle_query(o, u, v) : oracle_block(o, u, v);
 }
 
-// Larger matrices: one CTA per matrix, rows scanned by the whole block.
-__global__ void __launch_bounds__(512)
+// Larger matrices: one CTA per matrix, rows scanned by the whole block.  Chain,
+// activity flags and slot ids live in shared memory (m <= NN_SMEM_MAX); each
+// step is one coalesced row read (L2), a two-level argmin (shuffles, then warp 0)
+// and two barriers.  The value at the chain's second-to-last entry -- needed by
+// the tie rule -- is captured during the scan instead of re-read.
+constexpr int NN_SMEM_MAX = 7168;
+constexpr int NN_CTA_T = 512;
+
+__global__ void __launch_bounds__(NN_CTA_T)
 nn_chain_cta_kernel(double *mats, const int64_t *mat_off, const int64_t *sizes, int64_t count,
                     const int64_t *merge_off, int64_t *lefts, int64_t *rights, double *heights,
                     uint8_t *active_all, int64_t *slot_all, int64_t *chain_all, const int64_t *aux_off) {
-    __shared__ double rv[16];
-    __shared__ long long ri[16];
-    __shared__ long long sh_y, sh_f;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    extern __shared__ __align__(16) unsigned char nn_smem[];
+    __shared__ double rv[NN_CTA_T / 32];
+    __shared__ int ri[NN_CTA_T / 32];
+    __shared__ int sh_y, sh_first;
+    __shared__ double sh_rp;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = NN_CTA_T / 32;
+    int32_t *s_chain = reinterpret_cast<int32_t *>(nn_smem);
+    int32_t *s_slot = s_chain + NN_SMEM_MAX;
+    uint8_t *s_act = reinterpret_cast<uint8_t *>(s_slot + NN_SMEM_MAX);
     for (int64_t b = blockIdx.x; b < count; b += gridDim.x) {
-        const int64_t m = sizes[b];
-        if (m <= NN_WARP_MAX) continue;
+        const int64_t m64 = sizes[b];
+        if (m64 <= NN_WARP_MAX) continue;
+        const int m = (int)m64;
         double *W = mats + mat_off[b];
-        uint8_t *active = active_all + aux_off[b];
-        int64_t *slot = slot_all + aux_off[b];
-        int64_t *chain = chain_all + aux_off[b];
         int64_t *L = lefts + merge_off[b], *R = rights + merge_off[b];
         double *Hh = heights + merge_off[b];
-        for (int64_t i = tid; i < m; i += blockDim.x) {
-            active[i] = 1;
-            slot[i] = i;
-            W[i * m + i] = INFINITY;
+        const bool in_smem = m <= NN_SMEM_MAX;
+        // state: shared memory when it fits, else the caller's scratch (int64 slot/chain)
+        uint8_t *act = in_smem ? s_act : active_all + aux_off[b];
+        int64_t *gslot = slot_all + aux_off[b];
+        int64_t *gchain = chain_all + aux_off[b];
+        auto slot_get = [&](int i) -> int64_t { return in_smem ? (int64_t)s_slot[i] : gslot[i]; };
+        auto slot_set = [&](int i, int64_t v) { if (in_smem) s_slot[i] = (int32_t)v; else gslot[i] = v; };
+        auto chain_get = [&](int i) -> int { return in_smem ? s_chain[i] : (int)gchain[i]; };
+        auto chain_set = [&](int i, int v) { if (in_smem) s_chain[i] = v; else gchain[i] = v; };
+        for (int i = tid; i < m; i += NN_CTA_T) {
+            act[i] = 1;
+            slot_set(i, i);
+            W[(int64_t)i * m + i] = INFINITY;
         }
         __syncthreads();
-        int64_t nchain = 0, next_id = m, remaining = m, nm = 0;
+        int nchain = 0, remaining = m, nm = 0;
+        int64_t next_id = m;
         while (remaining > 1) {
             if (nchain == 0) {
-                long long f = LLONG_MAX;
-                for (int64_t i = tid; i < m; i += blockDim.x)
-                    if (active[i]) { f = i; break; }
-                for (int o = 16; o; o >>= 1) f = min(f, __shfl_xor_sync(0xffffffffu, f, o));
+                // chain start: the first active cluster
+                int f = INT_MAX;
+                for (int i = tid; i < m; i += NN_CTA_T)
+                    if (act[i]) { f = i; break; }
+                f = __reduce_min_sync(0xffffffffu, (unsigned)f);
                 if (lane == 0) ri[warp] = f;
                 __syncthreads();
-                if (tid == 0) {
-                    long long g = LLONG_MAX;
-                    for (int w = 0; w < nw; w++) g = min(g, ri[w]);
-                    sh_f = g;
+                if (warp == 0) {
+                    int g = lane < NW ? ri[lane] : INT_MAX;
+                    g = (int)__reduce_min_sync(0xffffffffu, (unsigned)g);
+                    if (lane == 0) { chain_set(0, g); sh_first = g; }
                 }
                 __syncthreads();
-                if (tid == 0) chain[0] = sh_f;
                 nchain = 1;
-                __syncthreads();
             }
-            const int64_t x = chain[nchain - 1];
+            const int x = nchain > 0 ? (in_smem ? s_chain[nchain - 1] : chain_get(nchain - 1)) : 0;
+            const int p = nchain > 1 ? chain_get(nchain - 2) : -1;
+            const double *row = W + (int64_t)x * m;
             double bv = INFINITY;
-            long long bi = LLONG_MAX;
-            const double *row = W + x * m;
-            for (int64_t j = tid; j < m; j += blockDim.x) {
-                double r = (active[j] && j != x) ? row[j] : INFINITY;
-                if (r < bv || (r == bv && j < bi)) { bv = r; bi = j; }
+            int bi = INT_MAX;
+            for (int j0 = tid; j0 < m; j0 += 4 * NN_CTA_T) {
+                double rr[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {   // all loads in flight before any use
+                    const int j = j0 + u * NN_CTA_T;
+                    rr[u] = j < m ? row[j] : INFINITY;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int j = j0 + u * NN_CTA_T;
+                    if (j < m) {
+                        const double r = (act[j] && j != x) ? rr[u] : INFINITY;
+                        if (r < bv || (r == bv && j < bi)) { bv = r; bi = j; }
+                        if (j == p) sh_rp = r;
+                    }
+                }
             }
             for (int o = 16; o; o >>= 1) {
-                double r2 = __shfl_xor_sync(0xffffffffu, bv, o);
-                long long i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+                const double r2 = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
                 if (r2 < bv || (r2 == bv && i2 < bi)) { bv = r2; bi = i2; }
             }
             if (lane == 0) { rv[warp] = bv; ri[warp] = bi; }
             __syncthreads();
-            if (tid == 0) {
-                double v = INFINITY;
-                long long i = LLONG_MAX;
-                for (int w = 0; w < nw; w++)
-                    if (rv[w] < v || (rv[w] == v && ri[w] < i)) { v = rv[w]; i = ri[w]; }
-                int64_t y = (i == LLONG_MAX) ? 0 : i;  // all-inf row: np.argmin -> 0
-                if (nchain > 1) {
-                    int64_t p = chain[nchain - 2];
-                    double rp = (active[p] && p != x) ? row[p] : INFINITY;
-                    double ry = (active[y] && y != x) ? row[y] : INFINITY;
-                    if (rp == ry) y = p;
+            if (warp == 0) {
+                double v = lane < NW ? rv[lane] : INFINITY;
+                int i = lane < NW ? ri[lane] : INT_MAX;
+                for (int o = 16; o; o >>= 1) {
+                    const double r2 = __shfl_xor_sync(0xffffffffu, v, o);
+                    const int i2 = __shfl_xor_sync(0xffffffffu, i, o);
+                    if (r2 < v || (r2 == v && i2 < i)) { v = r2; i = i2; }
                 }
-                sh_y = y;
+                if (lane == 0) {
+                    int y = (i == INT_MAX) ? 0 : i;  // all-inf row: np.argmin -> 0
+                    // linkage.py: prefer the previous chain element on ties (row[y] is the minimum v)
+                    if (p >= 0 && sh_rp == v) y = p;
+                    sh_y = y;
+                }
             }
             __syncthreads();
-            const int64_t y = sh_y;
-            if (nchain > 1 && y == chain[nchain - 2]) {
+            const int y = sh_y;
+            if (p >= 0 && y == p) {
                 nchain -= 2;
-                const double h = row[y];
-                const int64_t lo = x < y ? x : y, hi = x < y ? y : x;
+                const double h = sh_rp;
+                const int lo = x < y ? x : y, hi = x < y ? y : x;
                 if (tid == 0) {
-                    L[nm] = slot[x];
-                    R[nm] = slot[y];
+                    L[nm] = slot_get(x);
+                    R[nm] = slot_get(y);
                     Hh[nm] = h;
                 }
                 nm++;
-                for (int64_t j = tid; j < m; j += blockDim.x) {
-                    double p = W[lo * m + j], q = W[hi * m + j];
-                    double mg = p > q ? p : (q > p ? q : p);
-                    W[lo * m + j] = mg;
-                    W[j * m + lo] = mg;
+                double *Wlo = W + (int64_t)lo * m;
+                const double *Whi = W + (int64_t)hi * m;
+                for (int j0 = tid; j0 < m; j0 += 4 * NN_CTA_T) {
+                    double pv[4], qv[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const int j = j0 + u * NN_CTA_T;
+                        pv[u] = j < m ? Wlo[j] : 0.0;
+                        qv[u] = j < m ? Whi[j] : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const int j = j0 + u * NN_CTA_T;
+                        if (j < m) {
+                            const double mg = pv[u] > qv[u] ? pv[u] : (qv[u] > pv[u] ? qv[u] : pv[u]);
+                            Wlo[j] = mg;
+                            W[(int64_t)j * m + lo] = mg;
+                        }
+                    }
                 }
                 __syncthreads();
                 if (tid == 0) {
-                    W[lo * m + lo] = INFINITY;
-                    active[hi] = 0;
-                    slot[lo] = next_id;
+                    Wlo[lo] = INFINITY;
+                    act[hi] = 0;
+                    slot_set(lo, next_id);
                 }
                 next_id++;
                 remaining--;
@@ -660,7 +709,7 @@ nn_chain_cta_kernel(double *mats, const int64_t *mat_off, const int64_t *sizes, 
                     if (tid == 0) Hh[0] = __longlong_as_double(0x7ff8dead00000000ll);
                     break;
                 }
-                if (tid == 0) chain[nchain] = y;
+                if (tid == 0) chain_set(nchain, y);
                 nchain++;
                 __syncthreads();
             }
@@ -861,8 +910,11 @@ TG_API int tg_nn_chain_batch(double *mats, const int64_t *mat_off, const int64_t
     nn_chain_kernel<<<(unsigned)blocks, threads, 0, st>>>(mats, mat_off, sizes, count, merge_off, lefts, rights, heights,
                                                         active, slot, chain, aux_off); tg_count_launch(1);
     int64_t cblocks = count < (int64_t)tg_num_sms() * 2 ? count : (int64_t)tg_num_sms() * 2;
-    nn_chain_cta_kernel<<<(unsigned)cblocks, 512, 0, st>>>(mats, mat_off, sizes, count, merge_off, lefts, rights,
-                                                         heights, active, slot, chain, aux_off); tg_count_launch(1);
+    const size_t nn_smem = (size_t)NN_SMEM_MAX * 9;
+    TG_CUDA_CHECK(cudaFuncSetAttribute(nn_chain_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nn_smem));
+    nn_chain_cta_kernel<<<(unsigned)cblocks, NN_CTA_T, nn_smem, st>>>(mats, mat_off, sizes, count, merge_off, lefts,
+                                                                      rights, heights, active, slot, chain, aux_off);
+    tg_count_launch(1);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
