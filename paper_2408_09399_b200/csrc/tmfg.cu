@@ -63,6 +63,15 @@ __device__ __forceinline__ bool ent_gt(const Ent &x, const Ent &y) {
     return (x.g > y.g) | ((x.g == y.g) & (x.fid < y.fid));
 }
 
+// refresh cache slot (direct-mapped by face id)
+struct RcEnt {
+    double g;
+    int fid, cand;
+    int m[3];
+    int pad;
+};
+constexpr int TM_RC = 1024;
+
 struct Ctl {
     int size;        // entries in the shared buffer
     int sel;         // which half of the double buffer is current
@@ -100,6 +109,7 @@ struct Ctl {
     long long phs[4];
     long long pops_dbg;
     long long rf_t[4];   // refill phases: select, take, place, hole fill (TM_PROFILE)
+    unsigned rc_hit;     // refresh-cache hits (TM_PROFILE)
     long long it_total, it_maxsum;
 };
 
@@ -162,7 +172,7 @@ __device__ __forceinline__ void mc_set(uint16_t *sm, int32_t *gm, int w, int u) 
 
 template <bool SMEM_CURSORS, bool SMEM_MC>
 __device__ void warp_entries(const TmArgs &A, const uint32_t *bits, uint16_t *sc, uint16_t *smc, int cnt,
-                             const int (*fverts)[3], const int *fids, Ent *out, int *iters) {
+                             const int (*fverts)[3], const int *fids, Ent *out, int *iters, int *mc_out) {
     const int lane = threadIdx.x & 31;
     const int n = A.n, m = n - 1;
     constexpr int NV = 3 * TM_EPW;
@@ -252,6 +262,11 @@ __device__ void warp_entries(const TmArgs &A, const uint32_t *bits, uint16_t *sc
         if (hit >= 0 || c + adv >= m) pending &= ~(1u << k);
     }
     if (lane == 0) {
+        if (mc_out) {
+#pragma unroll
+            for (int k = 0; k < NV; k++)
+                if (k < nv) mc_out[k] = found[k];
+        }
 #pragma unroll
         for (int k = 0; k < NV; k++)
             if ((scanned >> k) & 1u) {
@@ -833,6 +848,9 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
     __shared__ double rk_g[TM_BATCH];
     __shared__ int rk_f[TM_BATCH], rk_src[TM_BATCH];
     __shared__ int red_ok[TM_WARPS];
+    __shared__ RcEnt rcache[TM_RC];
+    __shared__ int Lmc[TM_K][3];
+    __shared__ int Lcomp[TM_K];
 
     Ent *buf0 = reinterpret_cast<Ent *>(tm_smem);
     Ent *buf1 = buf0 + TM_B;
@@ -853,6 +871,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
         for (int i = tid; i < n; i += TM_T) A.gmc[i] = -1;
     }
     for (int i = tid; i < 3 * n; i += TM_T) A.fv[i] = make_int4(0, 0, 0, 0);
+    for (int i = tid; i < TM_RC; i += TM_T) rcache[i].fid = -1;
     __syncthreads();
     if (tid == 0) {
         int a = A.clique[0], b = A.clique[1], c = A.clique[2], d = A.clique[3];
@@ -887,6 +906,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
         for (int q = 0; q < 4; q++) { ctl.ph[q] = 0; ctl.phs[q] = 0; }
         ctl.pops_dbg = 0;
         ctl.rf_t[0] = ctl.rf_t[1] = ctl.rf_t[2] = ctl.rf_t[3] = 0;
+        ctl.rc_hit = 0;
         ctl.it_total = ctl.it_maxsum = 0;
     }
     __syncthreads();
@@ -917,7 +937,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
                 if (warp < ctl.ne_count) {
                     int fids[1] = {ctl.ne_fid[warp]};
                     int fvv[1][3] = {{ctl.ne_v[warp][0], ctl.ne_v[warp][1], ctl.ne_v[warp][2]}};
-                    warp_entries<SMEM_CURSORS, SMEM_MC>(A, bits, sc, smc, 1, fvv, fids, &NE[warp], my_iters);
+                    warp_entries<SMEM_CURSORS, SMEM_MC>(A, bits, sc, smc, 1, fvv, fids, &NE[warp], my_iters, nullptr);
                 }
             } else {
                 int base = TM_EPW * (warp - TM_NEW_WARPS);
@@ -932,8 +952,32 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
                     if (i < cntL) {
                         Ent h = cur[i];
                         bool stale = is_ins(bits, h.cand);
-                        if (lane == 0) { L[i] = h; Lstale[i] = stale; }
-                        if (stale) {
+                        // refresh cache (written only between rounds, so this read is stable):
+                        // a refreshed entry stays exact while its three max-corr candidates
+                        // are still uninserted (each is a monotone fact).  Decided on lane 0.
+                        int hit = 0;
+                        if (lane == 0) {
+                            L[i] = h;
+                            Lstale[i] = stale;
+                            Lcomp[i] = 0;
+                            if (stale && !A.check) {
+                                const RcEnt &rc = rcache[h.fid & (TM_RC - 1)];
+                                if (rc.fid == h.fid && rc.m[0] >= 0 && rc.m[1] >= 0 && rc.m[2] >= 0 &&
+                                    !is_ins(bits, rc.m[0]) && !is_ins(bits, rc.m[1]) && !is_ins(bits, rc.m[2])) {
+                                    Ent x = h;
+                                    x.g = rc.g;
+                                    x.cand = rc.cand;
+                                    x.opt = 0;
+                                    Lref[i] = x;
+                                    hit = 1;
+#if TM_PROFILE
+                                    atomicAdd(&ctl.rc_hit, 1u);
+#endif
+                                }
+                            }
+                        }
+                        hit = __shfl_sync(0xffffffffu, hit, 0);
+                        if (stale && !hit) {
                             idx[cnt] = i;
                             fids[cnt] = h.fid;
                             fvv[cnt][0] = h.a;
@@ -944,9 +988,17 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
                     }
                 }
                 if (cnt) {
-                    warp_entries<SMEM_CURSORS, SMEM_MC>(A, bits, sc, smc, cnt, fvv, fids, Lout[warp - TM_NEW_WARPS], my_iters);
+                    int mcs[3 * TM_EPW];
+                    warp_entries<SMEM_CURSORS, SMEM_MC>(A, bits, sc, smc, cnt, fvv, fids, Lout[warp - TM_NEW_WARPS], my_iters,
+                                                        mcs);
                     if (lane == 0)
-                        for (int q = 0; q < cnt; q++) Lref[idx[q]] = Lout[warp - TM_NEW_WARPS][q];
+                        for (int q = 0; q < cnt; q++) {
+                            Lref[idx[q]] = Lout[warp - TM_NEW_WARPS][q];
+                            Lmc[idx[q]][0] = mcs[3 * q];
+                            Lmc[idx[q]][1] = mcs[3 * q + 1];
+                            Lmc[idx[q]][2] = mcs[3 * q + 2];
+                            Lcomp[idx[q]] = 1;
+                        }
                 }
             }
         }
@@ -966,6 +1018,20 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
             tc0 = tc1;
         }
         if (warp == 0) replay_warp(A, ctl, L, Lref, Lstale, NE, batch, tobuf, rk_g, rk_f, rk_src);
+        else if (warp == 1 && !A.check) {
+            // publish this round's computed refreshes (nobody reads the cache now)
+            for (int i = lane; i < ctl.L_count; i += 32)
+                if (Lcomp[i]) {
+                    const Ent &x = Lref[i];
+                    RcEnt &rc = rcache[x.fid & (TM_RC - 1)];
+                    rc.g = x.g;
+                    rc.fid = x.fid;
+                    rc.cand = x.cand;
+                    rc.m[0] = Lmc[i][0];
+                    rc.m[1] = Lmc[i][1];
+                    rc.m[2] = Lmc[i][2];
+                }
+        }
         tc1 = fg_sync_clock();
         if (tid == 0) {
             ctl.t_replay += tc1 - tc0;
@@ -1135,6 +1201,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
         A.stats[25] = ctl.rf_t[1];
         A.stats[26] = ctl.rf_t[2];
         A.stats[27] = ctl.rf_t[3];
+        A.stats[28] = ctl.rc_hit;
     }
 }
 

@@ -19,7 +19,7 @@ for rep in range(2):
     out = tmfg.build_tmfg_heap_device(S, order, clique)
     torch.cuda.synchronize(); dt = time.perf_counter() - t0
 st = out["stats"].cpu().numpy()
-names = ["pops", "refreshes", "gain_inc", "status", "a4", "a5", "a6", "tails", "rounds", "refills", "cyc_warp_max", "cyc_probe_max", "cyc_tail_max", "cyc_S_max", "cyc_refill", "pool", "cyc_par", "cyc_replay", "cyc_merge", "cyc_insert", "cyc_tail", "s21", "s22", "s23", "rf_select", "rf_take", "rf_place", "rf_fill"]
+names = ["pops", "refreshes", "gain_inc", "status", "a4", "a5", "a6", "tails", "rounds", "refills", "cyc_warp_max", "cyc_probe_max", "cyc_tail_max", "cyc_S_max", "cyc_refill", "pool", "cyc_par", "cyc_replay", "cyc_merge", "cyc_insert", "cyc_tail", "s21", "s22", "s23", "rf_select", "rf_take", "rf_place", "rf_fill", "rc_hit"]
 d = {k: int(v) for k, v in zip(names, st)}
 d["ms"] = dt * 1e3
 d["us_per_insert"] = dt * 1e6 / (n - 4)
