@@ -1019,8 +1019,11 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
         }
         if (warp == 0) replay_warp(A, ctl, L, Lref, Lstale, NE, batch, tobuf, rk_g, rk_f, rk_src);
         else if (warp == 1 && !A.check) {
-            // publish this round's computed refreshes (nobody reads the cache now)
-            for (int i = lane; i < ctl.L_count; i += 32)
+            // publish this round's computed refreshes (nobody reads the cache now).  One
+            // lane writes them all: two faces of the window may share a slot, and two
+            // lanes writing one slot at once would interleave their fields.
+            if (lane == 0)
+            for (int i = 0; i < ctl.L_count; i++)
                 if (Lcomp[i]) {
                     const Ent &x = Lref[i];
                     RcEnt &rc = rcache[x.fid & (TM_RC - 1)];

@@ -88,3 +88,26 @@ def test_tmfg_nan_raises(pkg):
     lists = pkg.sort_neighbor_lists(S)
     with pytest.raises(pkg.DataError, match="NaN"):
         pkg.build_tmfg_heap(S, lists)
+
+
+@pytest.mark.parametrize("config,n", [(3, 10000), (4, 4000), (2, 2000), (1, 500), (5, 3000), (3, 6001)])
+def test_tmfg_matches_oracle_larger(config, n, oracle, pkg):
+    """Full-size heap TMFG vs the oracle on the reference's own S (reference-order Pearson on
+    the GPU): trace, edges, faces and the debug counters, bit for bit.  Sizes where the
+    speculation window, queue refills and refresh-cache collisions all occur."""
+    from paper_2408_09399_b200 import simmatrix, synth
+    x, _ = synth.generate(config, n=n)
+    Sd = simmatrix.pearson_similarity_refexact_device(x)
+    S = Sd.cpu().numpy()
+    ref_order = oracle.sort_neighbor_lists(S)
+    ref = oracle.build_tmfg_heap(S, ref_order)
+    lists = pkg.sort_neighbor_lists(Sd)
+    assert np.array_equal(lists.order, ref_order)
+    g = pkg.build_tmfg_heap(Sd, lists)
+    assert list(g.initial_clique) == list(ref["initial_clique"])
+    assert np.array_equal(np.asarray(g.trace), ref["trace"])
+    assert np.array_equal(np.asarray(g.edges), ref["edges"])
+    assert np.array_equal(np.asarray(g.faces), ref["faces"])
+    raw = g._raw_stats
+    assert (int(raw[0]), int(raw[1]), int(raw[2])) == (ref["stats"]["pops"], ref["stats"]["refreshes"],
+                                                       ref["stats"]["gain_increases"])
