@@ -1019,14 +1019,17 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
         }
         if (warp == 0) replay_warp(A, ctl, L, Lref, Lstale, NE, batch, tobuf, rk_g, rk_f, rk_src);
         else if (warp == 1 && !A.check) {
-            // publish this round's computed refreshes (nobody reads the cache now).  One
-            // lane writes them all: two faces of the window may share a slot, and two
-            // lanes writing one slot at once would interleave their fields.
-            if (lane == 0)
-            for (int i = 0; i < ctl.L_count; i++)
-                if (Lcomp[i]) {
+            // publish this round's computed refreshes (nobody reads the cache now).  Two
+            // window faces may share a slot: of the lanes writing one slot only the last
+            // writes (interleaved stores of two entries would tear the slot).
+            for (int i0 = 0; i0 < ctl.L_count; i0 += 32) {
+                const int i = i0 + lane;
+                const bool pub = i < ctl.L_count && Lcomp[i];
+                const int slot = pub ? (Lref[i].fid & (TM_RC - 1)) : -1 - lane;
+                const unsigned same = __match_any_sync(0xffffffffu, slot);
+                if (pub && (31 - __clz(same)) == lane) {
                     const Ent &x = Lref[i];
-                    RcEnt &rc = rcache[x.fid & (TM_RC - 1)];
+                    RcEnt &rc = rcache[slot];
                     rc.g = x.g;
                     rc.fid = x.fid;
                     rc.cand = x.cand;
@@ -1034,6 +1037,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
                     rc.m[1] = Lmc[i][1];
                     rc.m[2] = Lmc[i][2];
                 }
+            }
         }
         tc1 = fg_sync_clock();
         if (tid == 0) {
