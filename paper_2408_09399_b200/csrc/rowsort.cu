@@ -349,6 +349,13 @@ struct RtPlan {
     size_t off_sidx, off_f16, off_cinfo, off_misc, off_bar, smem;
 };
 
+#ifndef RS_DEBUG_PHASES
+#define RS_DEBUG_PHASES 0
+#endif
+#if RS_DEBUG_PHASES
+__device__ long long g_rs_phase[8];
+#endif
+
 struct RtCoarse {   // per coarse bin after the allocation phase
     double f;       // fine buckets in the bin (as double)
     int base, last; // first / last fine bucket id
@@ -449,12 +456,20 @@ row_sort_tma_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restri
     __syncthreads();
     int64_t v = blockIdx.x;
     if (tid == 0 && v < n) rt_bulk_row(vbuf, S + v * n64, n, &bar[0]);
+#if RS_DEBUG_PHASES
+    long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long pt = clock64();
+#define RS_PH(k) do { if (tid == 0) { const long long now = clock64(); ph[k] += now - pt; pt = now; } } while (0)
+#else
+#define RS_PH(k) do {} while (0)
+#endif
     for (int it = 0; v < n; v += gridDim.x, it++) {
         const int b = pl.nbuf == 2 ? (it & 1) : 0;
         const unsigned parity = pl.nbuf == 2 ? (unsigned)((it >> 1) & 1) : (unsigned)(it & 1);
         const double *row = S + v * n64;
         const double *vals = vbuf + (size_t)b * pl.stride + (((uintptr_t)row >> 3) & 1);
         rt_wait(&bar[b], parity);
+        RS_PH(0);
         // ---- A: clear counters; row min / max / NaN (v excluded); row-sum screen
         for (int i = tid; i < nw16; i += RS_T) f16[i] = 0u;
         for (int c = tid; c < C; c += RS_T) ccnt[c] = 0u;
@@ -515,6 +530,7 @@ row_sort_tma_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restri
                 screen[n + v] = rs_screen_radius(n, s2);
             }
         }
+        RS_PH(1);
         // ---- B: coarse histogram from a sample (sizes the fine buckets only)
         int nsamp = 0;
 #pragma unroll
@@ -529,39 +545,33 @@ row_sort_tma_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restri
         nsamp = __reduce_add_sync(0xffffffffu, nsamp);
         if (lane == 0 && nsamp) atomicAdd(&ms.nsamp, (uint32_t)nsamp);
         __syncthreads();
-        // ---- C: fine buckets per coarse bin + base offsets (warp 0, in place over the histogram)
-        if (warp == 0) {
+        RS_PH(2);
+        // ---- C: fine buckets per coarse bin + base offsets: one thread per bin (C <= 512),
+        // warp scans + a 16-entry scan of warp totals; written in place over the histogram
+        // (every read happens before the first barrier below)
+        {
             const float scale = (float)m * pl.fs / (float)(ms.nsamp ? ms.nsamp : 1u) * 0.9999f;
-            constexpr int PER = RS_CMAX / 32;
-            uint32_t f[PER];
-            uint32_t s = 0;
-#pragma unroll
-            for (int q = 0; q < PER; q++) {
-                const int c = lane * PER + q;
-                f[q] = c < C ? 1u + (uint32_t)((float)ccnt[c] * scale) : 0u;
-                s += f[q];
-            }
-            __syncwarp();
-            uint32_t incl = s;
+            const uint32_t f = tid < C ? 1u + (uint32_t)((float)ccnt[tid] * scale) : 0u;
+            uint32_t incl = f;
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += y;
             }
-            uint32_t run = incl - s;
-#pragma unroll
-            for (int q = 0; q < PER; q++) {
-                const int c = lane * PER + q;
-                if (c < C) {
-                    RtCoarse ci;
-                    ci.f = (double)f[q];
-                    ci.base = (int)run;
-                    ci.last = (int)(run + f[q] - 1);
-                    cinfo[c] = ci;
-                    run += f[q];
-                }
+            if (lane == 31 && warp < RS_CMAX / 32) ms.wsum[warp] = incl;
+            __syncthreads();
+            if (tid < C) {
+                uint32_t off = 0;
+                for (int w = 0; w < warp; w++) off += ms.wsum[w];
+                const uint32_t base = off + incl - f;
+                RtCoarse ci;
+                ci.f = (double)f;
+                ci.base = (int)base;
+                ci.last = (int)(base + f - 1);
+                cinfo[tid] = ci;
             }
         }
         __syncthreads();
+        RS_PH(3);
         // ---- D: fine bucket + arrival rank (one packed shared atomic per key)
         uint32_t pk[EMAX];
 #pragma unroll
@@ -595,6 +605,7 @@ row_sort_tma_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restri
             }
         }
         __syncthreads();
+        RS_PH(4);
         // ---- E: exclusive scan of the packed counters, scatter ids, bucket-start bits
         {
             const int NB = cinfo[C - 1].last + 1;
@@ -642,6 +653,7 @@ row_sort_tma_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restri
             }
         }
         __syncthreads();
+        RS_PH(5);
         // ---- F: exact rank by sorted position (value desc, id asc), coalesced id store
         int32_t *out = order + v * (int64_t)m;
 #pragma unroll
@@ -671,11 +683,17 @@ row_sort_tma_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restri
             }
         }
         __syncthreads();
+        RS_PH(6);
         if (tid == 0 && pl.nbuf == 1) {
             const int64_t vn = v + gridDim.x;
             if (vn < n) rt_bulk_row(vbuf, S + vn * n64, n, &bar[0]);
         }
     }
+#if RS_DEBUG_PHASES
+    if (tid == 0)
+        for (int k = 0; k < 7; k++) atomicAdd((unsigned long long *)&g_rs_phase[k], (unsigned long long)ph[k]);
+#endif
+#undef RS_PH
 }
 
 // ---------------------------------------------------------------- large rows
@@ -966,3 +984,12 @@ TG_API int tg_initial_clique_screened(const double *S, int64_t n, const double *
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
+
+#if RS_DEBUG_PHASES
+// debug build only: per-phase cycle sums (thread 0 of every CTA) since the last call
+TG_API void tg_row_sort_debug_phases(long long *out) {
+    cudaMemcpyFromSymbol(out, g_rs_phase, 8 * sizeof(long long));
+    long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_rs_phase, z, sizeof(z));
+}
+#endif
