@@ -29,6 +29,8 @@
 // keys are all below the buffer's; the buffer is refilled by a radix select
 // over the pool when it runs short.
 #include "common.cuh"
+#include <cooperative_groups.h>
+#include <cstdlib>
 
 namespace {
 
@@ -46,6 +48,10 @@ constexpr int TM_FG_T = TM_FG_WARPS * 32;
 constexpr int TM_EPW = 1;                       // entries refreshed per warp
 constexpr int TM_NEW_WARPS = 4;                 // warps that build new-face entries
 constexpr int TM_K = TM_EPW * (TM_FG_WARPS - TM_NEW_WARPS);  // top-K speculated per round
+#ifndef TM_MERGE_WARPS_DEF
+#define TM_MERGE_WARPS_DEF 28
+#endif
+constexpr int TM_MERGE_WARPS = TM_MERGE_WARPS_DEF;            // replay + merge warps; the rest speculate meanwhile
 constexpr int TM_B = 512;                       // shared-memory queue capacity
 constexpr int TM_BATCH = TM_K + 8;
 static_assert(TM_K <= 32, "replay_warp maps one queue position per lane");
@@ -127,8 +133,7 @@ struct TmArgs {
     double *pool_g;      // global pool (struct of arrays): gain
     int2 *pool_fc;       //   (fid, cand); capacity 3n + B
 
-    int32_t *gcursor;    // global cursors when n > 65536
-    int32_t *gmc;        // global max-corr cache when it does not fit in shared memory
+    unsigned long long *gvst;  // per-vertex scan state when it does not fit in shared memory
     int check;           // check_invariants mode (tmfg.py:375-399)
 };
 
@@ -143,26 +148,63 @@ __device__ __forceinline__ long long fg_sync_clock() {
     return clock64() + (long long)(r & 0u);
 }
 
-template <bool SMEM_CURSORS>
-__device__ __forceinline__ int cur_get(const uint16_t *sc, const int32_t *gc, int w) {
-    if (SMEM_CURSORS) return sc[w];
-    return gc[w];
+// Per-vertex scan state, one 64-bit word (tmfg.py:169-182 cursors + max_corrs):
+//   bits  0-20  mc + 1   the first uninserted id of order[w] when computed (0: unknown)
+//   bits 21-41  mc2 + 1  the next uninserted id after it (0: unknown)
+//   bits 42-63  cursor   where a scan restarts: the position of mc2 (of mc if mc2 is unknown)
+// "every id before pos(mc) is inserted" and "every id between mc and mc2 is
+// inserted" are monotone facts, so a word stays a valid certificate forever:
+// mc if uninserted, else mc2 if known and uninserted, is the first uninserted id,
+// and once both are inserted every id before the cursor is.  A word is written
+// with one atomicMax (cursor in the top bits: the furthest scan wins), so readers
+// never see a cursor from one scan with ids from another.  n <= 2^21 - 1.
+#if TM_PROFILE
+__device__ unsigned long long g_tm_prof[8];   // fg vertices looked up, scanned, tail batches; bg scans
+#endif
+struct VSt {
+    int mc, mc2, cur;
+};
+__device__ __forceinline__ VSt vst_unpack(unsigned long long x) {
+    VSt r;
+    r.mc = (int)(x & 0x1fffffull) - 1;
+    r.mc2 = (int)((x >> 21) & 0x1fffffull) - 1;
+    r.cur = (int)(x >> 42);
+    return r;
 }
-template <bool SMEM_CURSORS>
-__device__ __forceinline__ void cur_set(uint16_t *sc, int32_t *gc, int w, int c) {
-    if (SMEM_CURSORS) sc[w] = (uint16_t)c;
-    else gc[w] = c;
+__device__ __forceinline__ unsigned long long vst_pack(int mc, int mc2, int cur) {
+    return ((unsigned long long)(uint32_t)cur << 42) | ((unsigned long long)(uint32_t)(mc2 + 1) << 21) |
+           (unsigned long long)(uint32_t)(mc + 1);
 }
-// cached max_corrs[w] (tmfg.py:181): order[w][cursor[w]], 0xffff / -1 = unknown
-template <bool SMEM_MC>
-__device__ __forceinline__ int mc_get(const uint16_t *sm, const int32_t *gm, int w) {
-    if (SMEM_MC) { int x = sm[w]; return x == 0xffff ? -1 : x; }
-    return gm[w];
+// the first uninserted id certified by the word, or -1 (scan from r.cur)
+__device__ __forceinline__ int vst_pick(const uint32_t *bits, const VSt &r) {
+    if (r.mc < 0) return -1;
+    if (!is_ins(bits, r.mc)) return r.mc;
+    if (r.mc2 >= 0 && !is_ins(bits, r.mc2)) return r.mc2;
+    return -1;
 }
-template <bool SMEM_MC>
-__device__ __forceinline__ void mc_set(uint16_t *sm, int32_t *gm, int w, int u) {
-    if (SMEM_MC) sm[w] = (uint16_t)u;
-    else gm[w] = u;
+
+// Warp probe of NQ x 32 consecutive ids of a sorted row (val[q] = id at offset
+// q*32 + lane, -1 past the end; ok[q] = uninserted): offset of the first
+// uninserted id (>= NQ*32: none), that id and the next uninserted one (or -1).
+template <int NQ>
+__device__ __forceinline__ unsigned probe_two(const int (&val)[NQ], const bool (&ok)[NQ], int &hit, int &hit2,
+                                              unsigned &off2) {
+    const int lane = threadIdx.x & 31;
+    int q1 = NQ, q2 = NQ, h1 = -1, h2 = -1;
+#pragma unroll
+    for (int q = NQ - 1; q >= 0; q--)
+        if (ok[q]) { q2 = q1; h2 = h1; q1 = q; h1 = val[q]; }
+    const unsigned k1 = (unsigned)(q1 * 32 + lane);
+    const unsigned best = __reduce_min_sync(0xffffffffu, k1);
+    const bool mine = best < (unsigned)(NQ * 32) && (int)(best & 31u) == lane;
+    const unsigned second = __reduce_min_sync(0xffffffffu, mine ? (unsigned)(q2 * 32 + lane) : k1);
+    const int src = mine ? h2 : h1;
+    hit = __shfl_sync(0xffffffffu, h1, best & 31u);
+    const int s2 = __shfl_sync(0xffffffffu, src, second & 31u);
+    if (best >= (unsigned)(NQ * 32)) hit = -1;
+    hit2 = second < (unsigned)(NQ * 32) ? s2 : -1;
+    off2 = second;
+    return best;
 }
 
 // One warp builds up to TM_EPW entries: refresh the 3 vertices of each face
@@ -170,33 +212,42 @@ __device__ __forceinline__ void mc_set(uint16_t *sm, int32_t *gm, int w, int u) 
 // three candidates (tmfg.py:266-277).  Cursor probes: 4 x 32 ids per vertex in
 // one batch of independent loads; rare long tails continue 16 x 32 at a time.
 
-template <bool SMEM_CURSORS, bool SMEM_MC>
-__device__ void warp_entries(const TmArgs &A, const uint32_t *bits, uint16_t *sc, uint16_t *smc, int cnt,
+template <bool SMEM_ST>
+__device__ void warp_entries(const TmArgs &A, const uint32_t *bits, unsigned long long *vst, int cnt,
                              const int (*fverts)[3], const int *fids, Ent *out, int *iters, int *mc_out) {
     const int lane = threadIdx.x & 31;
     const int n = A.n, m = n - 1;
     constexpr int NV = 3 * TM_EPW;
-    int vv[NV], cur[NV], found[NV];
+    unsigned long long *st = SMEM_ST ? vst : A.gvst;
+    int vv[NV], cur[NV], found[NV], found2[NV];
     const int nv = 3 * cnt;
-#pragma unroll
-    for (int k = 0; k < NV; k++) {
-        vv[k] = k < nv ? fverts[k / 3][k % 3] : 0;
-        cur[k] = k < nv ? cur_get<SMEM_CURSORS>(sc, A.gcursor, vv[k]) : 0;
-        found[k] = -1;
-    }
-    // a vertex whose cached max-corr is still uninserted needs no scan at all
+    // a vertex whose certified max-corr (or the id after it) is still uninserted needs no scan
     unsigned pending = 0u;
 #pragma unroll
     for (int k = 0; k < NV; k++) {
+        vv[k] = k < nv ? fverts[k / 3][k % 3] : 0;
+        // decided on lane 0 and broadcast: background warps rewrite the word and the
+        // winner's bit may be set concurrently (speculative refreshes), and every lane
+        // must take the same scan decision (full-mask collectives follow)
+        int c0 = 0, f0 = -1;
+        if (lane == 0 && k < nv) {
+            const VSt r = vst_unpack(st[vv[k]]);
+            c0 = r.cur;
+            f0 = vst_pick(bits, r);
+        }
+        cur[k] = __shfl_sync(0xffffffffu, c0, 0);
+        const int mcv = __shfl_sync(0xffffffffu, f0, 0);
+        found[k] = -1;
+        found2[k] = -1;
         if (k < nv) {
-            const int mcv = mc_get<SMEM_MC>(smc, A.gmc, vv[k]);
-            if (mcv >= 0 && !is_ins(bits, mcv)) found[k] = mcv;
+            if (mcv >= 0) found[k] = mcv;
             else pending |= 1u << k;
         }
     }
     const unsigned scanned = pending;
 #if TM_PROFILE
     long long tw0 = clock64();
+    if (lane == 0) { atomicAdd(&g_tm_prof[0], (unsigned long long)nv); atomicAdd(&g_tm_prof[1], (unsigned long long)__popc(pending)); }
 #endif
     {
         int val[NV][4];
@@ -210,17 +261,16 @@ __device__ void warp_entries(const TmArgs &A, const uint32_t *bits, uint16_t *sc
 #pragma unroll
         for (int k = 0; k < NV; k++) {
             if ((pending >> k) & 1u) {
-                int firstq = 4, hitv = -1;
+                bool ok[4];
 #pragma unroll
-                for (int q = 3; q >= 0; q--) {
-                    bool ok = val[k][q] >= 0 && !is_ins(bits, val[k][q]);
-                    if (ok) { firstq = q; hitv = val[k][q]; }
-                }
-                const unsigned key = (unsigned)(firstq * 32 + lane);
-                const unsigned best = __reduce_min_sync(0xffffffffu, key);
+                for (int q = 0; q < 4; q++) ok[q] = val[k][q] >= 0 && !is_ins(bits, val[k][q]);
+                int h1, h2;
+                unsigned o2;
+                const unsigned best = probe_two<4>(val[k], ok, h1, h2, o2);
                 if (best < 128u) {
-                    found[k] = __shfl_sync(0xffffffffu, hitv, best & 31);
-                    cur[k] += (int)best;
+                    found[k] = h1;
+                    found2[k] = h2;
+                    cur[k] += (int)(h2 >= 0 ? o2 : best);
                     pending &= ~(1u << k);
                 } else {
                     cur[k] += 128;
@@ -233,6 +283,9 @@ __device__ void warp_entries(const TmArgs &A, const uint32_t *bits, uint16_t *sc
 #endif
     while (pending) {
         (*iters)++;
+#if TM_PROFILE
+        if (lane == 0) atomicAdd(&g_tm_prof[2], 1ull);
+#endif
         const int k = __ffs(pending) - 1;
         int w = 0, c = 0;
 #pragma unroll
@@ -244,22 +297,21 @@ __device__ void warp_entries(const TmArgs &A, const uint32_t *bits, uint16_t *sc
             int idx = c + q * 32 + lane;
             val[q] = idx < m ? __ldg(A.order + (int64_t)w * m + idx) : -1;
         }
-        int firstq = 16, hitv = -1;
+        bool ok[16];
 #pragma unroll
-        for (int q = 15; q >= 0; q--) {
-            bool ok = val[q] >= 0 && !is_ins(bits, val[q]);
-            if (ok) { firstq = q; hitv = val[q]; }
-        }
-        const unsigned best = __reduce_min_sync(0xffffffffu, (unsigned)(firstq * 32 + lane));
-        const int hit = best < 512u ? __shfl_sync(0xffffffffu, hitv, best & 31) : -1;
-        const int adv = best < 512u ? (int)best : 512;
+        for (int q = 0; q < 16; q++) ok[q] = val[q] >= 0 && !is_ins(bits, val[q]);
+        int hit, hit2;
+        unsigned o2;
+        const unsigned best = probe_two<16>(val, ok, hit, hit2, o2);
+        const int adv = best < 512u ? (int)(hit2 >= 0 ? o2 : best) : 512;
+        const int cn = min(c + adv, m);
 #pragma unroll
         for (int q = 0; q < NV; q++)
             if (q == k) {
-                cur[q] = c + adv;
-                if (hit >= 0) found[q] = hit;
+                cur[q] = cn;
+                if (hit >= 0) { found[q] = hit; found2[q] = hit2; }
             }
-        if (hit >= 0 || c + adv >= m) pending &= ~(1u << k);
+        if (hit >= 0 || cn >= m) pending &= ~(1u << k);
     }
     if (lane == 0) {
         if (mc_out) {
@@ -269,10 +321,7 @@ __device__ void warp_entries(const TmArgs &A, const uint32_t *bits, uint16_t *sc
         }
 #pragma unroll
         for (int k = 0; k < NV; k++)
-            if ((scanned >> k) & 1u) {
-                cur_set<SMEM_CURSORS>(sc, A.gcursor, vv[k], cur[k]);
-                mc_set<SMEM_MC>(smc, A.gmc, vv[k], found[k]);
-            }
+            if ((scanned >> k) & 1u) atomicMax(st + vv[k], vst_pack(found[k], found2[k], min(cur[k], m)));
     }
 #if TM_PROFILE
     long long tw2 = clock64() + (found[0] & 0);
@@ -769,69 +818,195 @@ __device__ void replay_warp(const TmArgs &A, Ctl &ctl, const Ent *L, const Ent *
 // Background warp: sweep the vertices (32 per step, lane-parallel check), and for
 // every vertex whose cached max-corr is unknown or already inserted, advance its
 // cursor to the first uninserted id of its sorted row (16 x 32 ids per load batch).
-template <bool SMEM_CURSORS, bool SMEM_MC>
-__device__ void bg_sweep(const TmArgs &A, const uint32_t *bits_, uint16_t *sc_, uint16_t *smc_, const int *stop_,
-                         int bgw) {
+// Background warp: sweep the vertices 32 at a time; every lane whose vertex's
+// certified max-corr is unknown or inserted scans its own sorted row from the
+// cursor (8 ids per batch, up to 64 ids per visit), so 32 rows are in flight per
+// warp.  The result -- first two uninserted ids, or just the advanced cursor --
+// is published with one atomicMax: scan-state words only ever move forward.
+template <bool SMEM_ST>
+__device__ void bg_sweep(const TmArgs &A, const uint32_t *bits_, unsigned long long *vst, const int *stop_, int bgw) {
     const int lane = threadIdx.x & 31;
     const int n = A.n, m = n - 1;
     volatile const uint32_t *bits = bits_;
-    volatile uint16_t *sc = sc_;
-    volatile uint16_t *smc = smc_;
-    volatile int32_t *gcur = A.gcursor;
-    volatile int32_t *gmc = A.gmc;
+    volatile unsigned long long *st = SMEM_ST ? vst : A.gvst;
     volatile const int *stop = stop_;
     int w0 = bgw * 32;
-    while (!*stop) {
+    // the loop decision is lane 0's read, broadcast: lanes must leave together
+    while (!__shfl_sync(0xffffffffu, lane == 0 ? *stop : 0, 0)) {
         const int w = w0 + lane;
-        bool need = false;
         if (w < n) {
-            int mcv = SMEM_MC ? (smc[w] == 0xffff ? -1 : (int)smc[w]) : gmc[w];
-            need = (mcv < 0) || ((bits[mcv >> 5] >> (mcv & 31)) & 1u);
+            const VSt r = vst_unpack(st[w]);
             // a vertex that is itself inserted may still be refreshed (face vertex)
-        }
-        unsigned todo = __ballot_sync(0xffffffffu, need);
-        while (todo && !*stop) {
-            const int l = __ffs(todo) - 1;
-            todo &= todo - 1;
-            const int v = w0 + l;
-            int c = SMEM_CURSORS ? (int)sc[v] : gcur[v];
-            int hit = -1;
-            while (hit < 0 && c < m) {
-                int val[16];
+            if (r.cur < m && (r.mc < 0 || ((bits[r.mc >> 5] >> (r.mc & 31)) & 1u))) {
+                const int32_t *row = A.order + (int64_t)w * m;
+                int c = r.cur, hit = -1, hit2 = -1, p1 = 0, p2 = 0;
+                for (int it = 0; it < 8 && hit2 < 0 && c < m; it++) {
+                    int val[8];
 #pragma unroll
-                for (int q = 0; q < 16; q++) {
-                    int idx = c + q * 32 + lane;
-                    val[q] = idx < m ? __ldg(A.order + (int64_t)v * m + idx) : -1;
-                }
-                int firstq = 16, hv = -1;
+                    for (int q = 0; q < 8; q++) val[q] = c + q < m ? __ldg(row + c + q) : -1;
 #pragma unroll
-                for (int q = 15; q >= 0; q--) {
-                    bool ok = val[q] >= 0 && !((bits[val[q] >> 5] >> (val[q] & 31)) & 1u);
-                    if (ok) { firstq = q; hv = val[q]; }
+                    for (int q = 0; q < 8; q++) {
+                        const int u = val[q];
+                        if (u >= 0 && !((bits[u >> 5] >> (u & 31)) & 1u)) {
+                            if (hit < 0) { hit = u; p1 = c + q; }
+                            else if (hit2 < 0) { hit2 = u; p2 = c + q; }
+                        }
+                    }
+                    c = min(c + 8, m);
                 }
-                const unsigned best = __reduce_min_sync(0xffffffffu, (unsigned)(firstq * 32 + lane));
-                if (best < 512u) {
-                    hit = __shfl_sync(0xffffffffu, hv, best & 31);
-                    c += (int)best;
-                } else {
-                    c += 512;
-                }
+                const int cur = hit2 >= 0 ? p2 : (hit >= 0 ? p1 : c);
+                atomicMax((unsigned long long *)st + w, vst_pack(hit, hit2, cur));
+#if TM_PROFILE
+                atomicAdd(&g_tm_prof[3], 1ull);
+#endif
             }
-            if (lane == 0 && hit >= 0) {
-                if (SMEM_CURSORS) {
-                    if ((int)sc[v] < c) sc[v] = (uint16_t)c;
-                } else if (gcur[v] < c) gcur[v] = c;
-                if (SMEM_MC) smc[v] = (uint16_t)hit;
-                else gmc[v] = hit;
-            }
-            __syncwarp();
         }
+        __syncwarp();
         w0 += TM_BG_WARPS * 32;
         if (w0 >= n) w0 = bgw * 32;
     }
 }
 
-template <bool SMEM_CURSORS, bool SMEM_MC>
+// Helper CTA of the cluster (ranks 1..): keeps every vertex's scan-state word
+// two candidates deep -- mc and mc2 both certified uninserted -- so the
+// foreground refreshes of the leader CTA (rank 0) find their max-corr without a
+// dependent global scan.  The words live in the leader's shared memory (or in
+// global memory for large n).  Each pass a helper copies the leader's inserted
+// bitmap into its own shared memory (any snapshot is a subset of the truth, so
+// every "inserted" it sees is a fact) and works on its own copy of its vertex
+// slice's words, touching the leader only to re-read a word that looks out of
+// date and to publish improvements -- the leader's shared memory serves its own
+// critical path.  A lane scans 16 ids of its own row; rows still unresolved are
+// scanned by the whole warp, 512 ids per coalesced batch.  Every write is an
+// atomicMax of a valid certificate (see VSt).
+__host__ __device__ __forceinline__ int tm_helper_slice(int n, int nslots) {
+    const int stride = nslots * TM_T;
+    return (n + stride - 1) / stride * TM_T;   // words per helper
+}
+
+template <bool SMEM_ST>
+__device__ void cluster_helper(const TmArgs &A, const uint32_t *bits_r, unsigned long long *vst_r,
+                               const int *stop_r, int slot, int nslots, unsigned char *lsmem) {
+    const int lane = threadIdx.x & 31, tid = threadIdx.x;
+    const int n = A.n, m = n - 1;
+    const int nwords = (n + 31) >> 5;
+    uint32_t *bits = reinterpret_cast<uint32_t *>(lsmem);                                    // local snapshot
+    unsigned long long *lst = reinterpret_cast<unsigned long long *>(bits + ((nwords + 1) & ~1));   // local words
+    volatile const uint32_t *rbits = bits_r;
+    volatile unsigned long long *st = SMEM_ST ? vst_r : A.gvst;
+    volatile const int *stop = stop_r;
+    const int stride = nslots * TM_T;
+    const int nloc = tm_helper_slice(n, nslots);
+    for (int i = tid; i < nloc; i += TM_T) lst[i] = 0ull;
+#if TM_PROFILE
+    long long passes = 0;
+#endif
+    for (;;) {
+        for (int i = tid; i < nwords; i += TM_T) bits[i] = rbits[i];
+        __syncthreads();
+        if (__syncthreads_or(tid == 0 ? *stop : 0)) break;
+#if TM_PROFILE
+        passes++;
+#endif
+        for (int k = 0, w0 = slot * TM_T + (tid & ~31); w0 < n; k++, w0 += stride) {
+            const int w = w0 + lane;
+            const int li = k * TM_T + tid;
+            int a = -1, c = 0;
+            bool need = false;
+            if (w < n) {
+                VSt r = vst_unpack(lst[li]);
+                bool mc_in = r.mc >= 0 && is_ins(bits, r.mc);
+                bool mc2_in = r.mc2 >= 0 && is_ins(bits, r.mc2);
+                need = r.cur < m && !(r.mc >= 0 && !mc_in && r.mc2 >= 0 && !mc2_in);
+                if (need) {
+                    // the leader may have advanced it (its own scans): take the newer word
+                    const unsigned long long x = max(lst[li], (unsigned long long)st[w]);
+                    lst[li] = x;
+                    r = vst_unpack(x);
+                    mc_in = r.mc >= 0 && is_ins(bits, r.mc);
+                    mc2_in = r.mc2 >= 0 && is_ins(bits, r.mc2);
+                    need = r.cur < m && !(r.mc >= 0 && !mc_in && r.mc2 >= 0 && !mc2_in);
+                }
+                if (need) {
+#if TM_PROFILE
+                    atomicAdd(&g_tm_prof[3], 1ull);
+#endif
+                    // mc stays when uninserted; look for the id(s) after the cursor
+                    const int32_t *row = A.order + (int64_t)w * m;
+                    a = (r.mc >= 0 && !mc_in) ? r.mc : -1;
+                    c = r.cur;
+                    int b = -1, pb = 0;
+                    int val[16];
+#pragma unroll
+                    for (int q = 0; q < 16; q++) val[q] = c + q < m ? __ldg(row + c + q) : -1;
+#pragma unroll
+                    for (int q = 0; q < 16; q++) {
+                        const int u = val[q];
+                        if (u >= 0 && u != r.mc && !is_ins(bits, u)) {
+                            if (a < 0) a = u;
+                            else if (b < 0) { b = u; pb = c + q; }
+                        }
+                    }
+                    c = min(c + 16, m);
+                    if (b >= 0 || c >= m) {
+                        // cursor: at mc2 when found, else past everything scanned
+                        const unsigned long long x = vst_pack(a, b, b >= 0 ? pb : c);
+                        lst[li] = x;
+                        atomicMax((unsigned long long *)st + w, x);
+                        need = false;
+                    }
+                }
+            }
+            unsigned todo = __ballot_sync(0xffffffffu, need);
+#if TM_PROFILE
+            if (lane == 0 && todo) atomicAdd(&g_tm_prof[5], (unsigned long long)__popc(todo));
+#endif
+            while (todo) {
+                const int l = __ffs(todo) - 1;
+                todo &= todo - 1;
+                const int ww = w0 + l;
+                int cc = __shfl_sync(0xffffffffu, c, l), aa = __shfl_sync(0xffffffffu, a, l);
+                int bb = -1, pbb = 0;
+                const int32_t *row = A.order + (int64_t)ww * m;
+                for (int it = 0; it < 4 && bb < 0 && cc < m; it++) {
+#if TM_PROFILE
+                    if (lane == 0) atomicAdd(&g_tm_prof[6], 1ull);
+#endif
+                    int val[16];
+#pragma unroll
+                    for (int q = 0; q < 16; q++) {
+                        const int idx = cc + q * 32 + lane;
+                        val[q] = idx < m ? __ldg(row + idx) : -1;
+                    }
+                    bool ok[16];
+#pragma unroll
+                    for (int q = 0; q < 16; q++) ok[q] = val[q] >= 0 && !is_ins(bits, val[q]);
+                    int h1, h2;
+                    unsigned o2;
+                    const unsigned best = probe_two<16>(val, ok, h1, h2, o2);
+                    if (best < 512u) {
+                        if (aa < 0) {
+                            aa = h1;
+                            if (h2 >= 0) { bb = h2; pbb = cc + (int)o2; }
+                        } else {
+                            bb = h1;
+                            pbb = cc + (int)best;
+                        }
+                    }
+                    cc = min(cc + 512, m);
+                }
+                const unsigned long long x = vst_pack(aa, bb, bb >= 0 ? pbb : cc);
+                if (lane == l) lst[k * TM_T + (tid & ~31) + l] = x;
+                if (lane == 0) atomicMax((unsigned long long *)st + ww, x);
+            }
+        }
+    }
+#if TM_PROFILE
+    if (threadIdx.x == 0 && slot == 0) A.stats[30] = passes;   // helper passes over the vertices
+#endif
+}
+
+template <bool SMEM_ST>
 __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
     extern __shared__ __align__(16) unsigned char tm_smem[];
     const int n = A.n;
@@ -849,6 +1024,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
     __shared__ int rk_f[TM_BATCH], rk_src[TM_BATCH];
     __shared__ int red_ok[TM_WARPS];
     __shared__ RcEnt rcache[TM_RC];
+    __shared__ int rc_claim[TM_RC];   // round that last wrote the slot: one writer per slot per round
     __shared__ int Lmc[TM_K][3];
     __shared__ int Lcomp[TM_K];
 
@@ -856,22 +1032,29 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
     Ent *buf1 = buf0 + TM_B;
     uint32_t *bits = reinterpret_cast<uint32_t *>(buf1 + TM_B);
     const int nwords = (n + 31) >> 5;
-    uint16_t *sc = reinterpret_cast<uint16_t *>(bits + nwords);
-    uint16_t *smc = sc + (SMEM_CURSORS ? ((n + 1) & ~1) : 0);
+    unsigned long long *vst = reinterpret_cast<unsigned long long *>(bits + ((nwords + 1) & ~1));
 
-    for (int i = tid; i < nwords; i += TM_T) bits[i] = 0u;
-    if (SMEM_CURSORS) {
-        for (int i = tid; i < n; i += TM_T) sc[i] = 0;
-    } else {
-        for (int i = tid; i < n; i += TM_T) A.gcursor[i] = 0;
+    namespace cg = cooperative_groups;
+    const unsigned ncl = cg::this_cluster().num_blocks(), crank = cg::this_cluster().block_rank();
+    if (crank != 0) {
+        cg::this_cluster().sync();   // the leader has initialised its state
+        cluster_helper<SMEM_ST>(A, cg::this_cluster().map_shared_rank(bits, 0),
+                                cg::this_cluster().map_shared_rank(vst, 0),
+                                cg::this_cluster().map_shared_rank(&ctl.bg_stop, 0), (int)crank - 1,
+                                (int)ncl - 1, tm_smem);
+        cg::this_cluster().sync();   // the leader's shared memory stays alive until here
+        return;
     }
-    if (SMEM_MC) {
-        for (int i = tid; i < n; i += TM_T) smc[i] = 0xffff;
-    } else {
-        for (int i = tid; i < n; i += TM_T) A.gmc[i] = -1;
+    for (int i = tid; i < nwords; i += TM_T) bits[i] = 0u;
+#if TM_PROFILE
+    if (tid < 8) g_tm_prof[tid] = 0ull;
+#endif
+    {
+        unsigned long long *st0 = SMEM_ST ? vst : A.gvst;
+        for (int i = tid; i < n; i += TM_T) st0[i] = 0ull;
     }
     for (int i = tid; i < 3 * n; i += TM_T) A.fv[i] = make_int4(0, 0, 0, 0);
-    for (int i = tid; i < TM_RC; i += TM_T) rcache[i].fid = -1;
+    for (int i = tid; i < TM_RC; i += TM_T) { rcache[i].fid = -1; rc_claim[i] = -1; }
     __syncthreads();
     if (tid == 0) {
         int a = A.clique[0], b = A.clique[1], c = A.clique[2], d = A.clique[3];
@@ -910,14 +1093,17 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
         ctl.it_total = ctl.it_maxsum = 0;
     }
     __syncthreads();
+    if (ncl > 1) cg::this_cluster().sync();
 
     if (warp < TM_BG_WARPS) {
+        // with helper CTAs the background warps stay idle (the helpers keep the states)
+        if (ncl == 1)
         // ============ background: keep every vertex's cached max-corr fresh so the
         // foreground refreshes rarely scan (cursor / max-corr writes are monotone
         // facts -- "all ids before the cursor are inserted" -- valid in any order).
         // Background warps have the LOWEST ids: the scheduler favours high warp ids,
         // so the latency-critical foreground (replay on warp 31) keeps priority.
-        bg_sweep<SMEM_CURSORS, SMEM_MC>(A, bits, sc, smc, &ctl.bg_stop, warp);
+        bg_sweep<SMEM_ST>(A, bits, vst, &ctl.bg_stop, warp);
     } else {
     // foreground numbering: warp 31 is foreground warp 0 (replay, insertion, leader)
     const int warp = (TM_WARPS - 1) - (threadIdx.x >> 5);
@@ -925,6 +1111,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
     long long tc0 = clock64(), tc1;
     int sel = 0;   // which half of the queue buffer is current (tracked by every foreground thread)
     while (!ctl.done) {
+        const int Lc_round = ctl.L_count, size_round = ctl.size;   // stable until the merge
         if (tid == 0) { tc0 = clock64(); ctl.rounds++; }
         // ================= parallel phase: new-face entries + speculative refresh of the top-K
         int my_iters[4] = {0, 0, 0, 0};
@@ -937,7 +1124,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
                 if (warp < ctl.ne_count) {
                     int fids[1] = {ctl.ne_fid[warp]};
                     int fvv[1][3] = {{ctl.ne_v[warp][0], ctl.ne_v[warp][1], ctl.ne_v[warp][2]}};
-                    warp_entries<SMEM_CURSORS, SMEM_MC>(A, bits, sc, smc, 1, fvv, fids, &NE[warp], my_iters, nullptr);
+                    warp_entries<SMEM_ST>(A, bits, vst, 1, fvv, fids, &NE[warp], my_iters, nullptr);
                 }
             } else {
                 int base = TM_EPW * (warp - TM_NEW_WARPS);
@@ -989,7 +1176,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
                 }
                 if (cnt) {
                     int mcs[3 * TM_EPW];
-                    warp_entries<SMEM_CURSORS, SMEM_MC>(A, bits, sc, smc, cnt, fvv, fids, Lout[warp - TM_NEW_WARPS], my_iters,
+                    warp_entries<SMEM_ST>(A, bits, vst, cnt, fvv, fids, Lout[warp - TM_NEW_WARPS], my_iters,
                                                         mcs);
                     if (lane == 0)
                         for (int q = 0; q < cnt; q++) {
@@ -1005,10 +1192,10 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
 #if TM_PROFILE
         if (lane == 0 && my_iters[0]) atomicMax(&ctl.it_round_max, my_iters[0]);
         if (lane == 0) {
-            atomicMax(&ctl.ph[1], my_iters[1]);
-            atomicMax(&ctl.ph[2], my_iters[2]);
+            const int tw = (int)(clock64() - tpw0);
+            atomicMax(&ctl.ph[warp < TM_NEW_WARPS ? 1 : 2], tw);
             atomicMax(&ctl.ph[3], my_iters[3]);
-            atomicMax(&ctl.ph[0], (int)(clock64() - tpw0));
+            atomicMax(&ctl.ph[0], tw);
         }
 #endif
         tc1 = fg_sync_clock();
@@ -1017,29 +1204,77 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
             ctl.t_par += tc1 - tc0;
             tc0 = tc1;
         }
+        // Warps 0..TM_MERGE_WARPS-1 replay, publish and merge (named barrier 2 between
+        // replay and merge); the other foreground warps meanwhile refresh the queue
+        // entries just past the window (the likely stale head of the next round) into
+        // the refresh cache, and only meet the others at the end of the round.  Nobody
+        // reads the cache before then; two writers of one slot in a round would tear
+        // it, so the first to claim a slot writes it.  The winner's bit is set while
+        // the speculative refreshes run: they stay exact (every fact they use is
+        // monotone) and the cache's candidate check rejects what the winner voids.
         if (warp == 0) replay_warp(A, ctl, L, Lref, Lstale, NE, batch, tobuf, rk_g, rk_f, rk_src);
-        else if (warp == 1 && !A.check) {
-            // publish this round's computed refreshes (nobody reads the cache now).  Two
-            // window faces may share a slot: of the lanes writing one slot only the last
-            // writes (interleaved stores of two entries would tear the slot).
-            for (int i0 = 0; i0 < ctl.L_count; i0 += 32) {
-                const int i = i0 + lane;
-                const bool pub = i < ctl.L_count && Lcomp[i];
-                const int slot = pub ? (Lref[i].fid & (TM_RC - 1)) : -1 - lane;
-                const unsigned same = __match_any_sync(0xffffffffu, slot);
-                if (pub && (31 - __clz(same)) == lane) {
-                    const Ent &x = Lref[i];
-                    RcEnt &rc = rcache[slot];
-                    rc.g = x.g;
-                    rc.fid = x.fid;
-                    rc.cand = x.cand;
-                    rc.m[0] = Lmc[i][0];
-                    rc.m[1] = Lmc[i][1];
-                    rc.m[2] = Lmc[i][2];
+        else if (!A.check && (warp == 1 || warp >= TM_MERGE_WARPS)) {
+            const int round = (int)ctl.rounds;
+            if (warp == 1) {
+                for (int i0 = 0; i0 < ctl.L_count; i0 += 32) {
+                    const int i = i0 + lane;
+                    if (i < ctl.L_count && Lcomp[i]) {
+                        const Ent &x = Lref[i];
+                        const int slot = x.fid & (TM_RC - 1);
+                        if (atomicExch(&rc_claim[slot], round) != round) {
+                            RcEnt &rc = rcache[slot];
+                            rc.g = x.g;
+                            rc.fid = x.fid;
+                            rc.cand = x.cand;
+                            rc.m[0] = Lmc[i][0];
+                            rc.m[1] = Lmc[i][1];
+                            rc.m[2] = Lmc[i][2];
+                        }
+                    }
+                }
+            } else {
+                const int pos = Lc_round + (warp - TM_MERGE_WARPS);
+                const Ent *curb = sel ? buf1 : buf0;
+                if (pos < size_round) {
+                    const Ent h = curb[pos];
+                    int need = 0;
+                    if (lane == 0) {
+                        need = is_ins(bits, h.cand);
+                        if (need) {
+                            const RcEnt &rc = rcache[h.fid & (TM_RC - 1)];
+                            if (rc.fid == h.fid && rc.m[0] >= 0 && rc.m[1] >= 0 && rc.m[2] >= 0 &&
+                                !is_ins(bits, rc.m[0]) && !is_ins(bits, rc.m[1]) && !is_ins(bits, rc.m[2]))
+                                need = 0;
+                        }
+                    }
+                    if (__shfl_sync(0xffffffffu, need, 0)) {
+                        int fids[1] = {h.fid};
+                        int fvv[1][3] = {{h.a, h.b, h.c}};
+                        int mcs[3], its[4] = {0, 0, 0, 0};
+                        Ent *o = &Lout[warp - TM_MERGE_WARPS][0];
+                        warp_entries<SMEM_ST>(A, bits, vst, 1, fvv, fids, o, its, mcs);
+                        if (lane == 0) {
+                            const int slot = h.fid & (TM_RC - 1);
+                            if (atomicExch(&rc_claim[slot], round) != round) {
+                                RcEnt &rc = rcache[slot];
+                                rc.g = o->g;
+                                rc.fid = o->fid;
+                                rc.cand = o->cand;
+                                rc.m[0] = mcs[0];
+                                rc.m[1] = mcs[1];
+                                rc.m[2] = mcs[2];
+                            }
+#if TM_PROFILE
+                            atomicAdd(&g_tm_prof[7], 1ull);
+#endif
+                        }
+                    }
                 }
             }
         }
-        tc1 = fg_sync_clock();
+        if (warp < TM_MERGE_WARPS) {
+        asm volatile("bar.sync 2, %0;" ::"r"(TM_MERGE_WARPS * 32) : "memory");
+        tc1 = clock64();
         if (tid == 0) {
             ctl.t_replay += tc1 - tc0;
             tc0 = tc1;
@@ -1058,7 +1293,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
                 Ent *nxt = sel ? buf0 : buf1;
                 const int old = sz - r;
                 const int mt = tid - 32;
-                constexpr int MT = TM_FG_T - 32;
+                constexpr int MT = TM_MERGE_WARPS * 32 - 32;
                 for (int i = mt; i < old; i += MT) {
                     Ent x = cur[r + i];
                     int lo = 0, hi = nb;  // # of tobuf entries popping before x
@@ -1137,6 +1372,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
                 if (ctl.bad) ctl.done = 1;
             }
         }
+        }
         sel ^= 1;
         tc1 = fg_sync_clock();
         if (tid == 0) { ctl.t_merge += tc1 - tc0; tc0 = tc1; }
@@ -1194,8 +1430,8 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
         A.stats[8] = ctl.rounds;
         A.stats[9] = ctl.refills;
         A.stats[10] = ctl.phs[0];   // sum over rounds of the slowest warp's refresh time
-        A.stats[11] = ctl.phs[1];   //   ... of its first cursor probe
-        A.stats[12] = ctl.phs[2];   //   ... of its long-tail scan
+        A.stats[11] = ctl.phs[1];   //   ... of the slowest new-face warp
+        A.stats[12] = ctl.phs[2];   //   ... of the slowest window-refresh warp
         A.stats[13] = ctl.phs[3];   //   ... of its similarity loads
         A.stats[14] = ctl.t_refill;
         A.stats[15] = ctl.pool_count;
@@ -1204,19 +1440,25 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
         A.stats[18] = ctl.t_merge;
         A.stats[19] = ctl.t_insert;
         A.stats[20] = ctl.t_tail;
+#if TM_PROFILE
+        for (int q = 0; q < 3; q++) A.stats[21 + q] = (long long)g_tm_prof[q];
+        A.stats[29] = (long long)g_tm_prof[3];
+        A.stats[31] = (long long)(g_tm_prof[5] << 32 | g_tm_prof[6]);   // helper warp-phase vertices, batches
+        A.stats[20] = (long long)g_tm_prof[7];
+#endif
         A.stats[24] = ctl.rf_t[0];
         A.stats[25] = ctl.rf_t[1];
         A.stats[26] = ctl.rf_t[2];
         A.stats[27] = ctl.rf_t[3];
         A.stats[28] = ctl.rc_hit;
     }
+    if (ncl > 1) cooperative_groups::this_cluster().sync();   // helpers read this CTA's shared memory until here
 }
 
-size_t tm_smem_bytes(int64_t n, bool smem_cursors, bool smem_mc) {
+size_t tm_smem_bytes(int64_t n, bool smem_st) {
     size_t b = (size_t)2 * TM_B * sizeof(Ent);
-    b += (size_t)((n + 31) / 32) * 4;
-    if (smem_cursors) b += (size_t)((n + 1) & ~1) * 2;
-    if (smem_mc) b += (size_t)n * 2;
+    b += (size_t)(((n + 31) / 32 + 1) & ~1LL) * 4;
+    if (smem_st) b += (size_t)n * 8;
     return tg_align_up(b, 16) + 64;
 }
 
@@ -1241,7 +1483,7 @@ TG_API size_t tg_tmfg_workspace_bytes(int64_t n) {
     b += tg_align_up((size_t)3 * n * sizeof(int4), 256);
     b += tg_align_up((size_t)(3 * n + TM_B + 64) * sizeof(double), 256);
     b += tg_align_up((size_t)(3 * n + TM_B + 64) * sizeof(int2), 256);
-    b += tg_align_up((size_t)n * sizeof(int32_t), 256) * 2;
+    b += tg_align_up((size_t)n * sizeof(unsigned long long), 256);
     return b + 1024;
 }
 
@@ -1265,23 +1507,53 @@ TG_API int tg_tmfg_heap(const double *S, const int32_t *order, int64_t n, const 
     A.fv = ar.take<int4>((size_t)3 * n);
     A.pool_g = ar.take<double>((size_t)3 * n + TM_B + 64);
     A.pool_fc = ar.take<int2>((size_t)3 * n + TM_B + 64);
-    A.gcursor = ar.take<int32_t>((size_t)n);
-    A.gmc = ar.take<int32_t>((size_t)n);
-    if (!A.fv || !A.pool_g || !A.pool_fc || !A.gcursor || !A.gmc) return TG_ERR_WORKSPACE;
+    A.gvst = ar.take<unsigned long long>((size_t)n);
+    if (!A.fv || !A.pool_g || !A.pool_fc || !A.gvst) return TG_ERR_WORKSPACE;
     cudaStream_t st = tg_stream(stream);
-    const bool smem_cur = n <= 65535;
-    const bool smem_mc = smem_cur && tm_smem_bytes(n, true, true) <= 200 * 1024;
-    const size_t smem = tm_smem_bytes(n, smem_cur, smem_mc);
-#define TM_LAUNCH(C, M)                                                                                   \
+    if (n >= (1 << 21)) return TG_ERR_ARG;   // scan-state word packs ids in 21 bits
+    const bool smem_st = tm_smem_bytes(n, true) <= 200 * 1024;
+    const size_t smem_leader = tm_smem_bytes(n, smem_st);
+    // a cluster of 1 leader + helper CTAs (TG_TMFG_CLUSTER, default 8 = portable
+    // maximum; 1 disables the helpers); falls back to a lone CTA if it cannot be placed
+    int ncl = 8;
+    if (const char *e = std::getenv("TG_TMFG_CLUSTER")) ncl = std::atoi(e);
+    if (ncl < 1) ncl = 1;
+    if (ncl > 8) ncl = 8;
+    // helpers reuse the dynamic shared memory for a bitmap snapshot + their slice's words
+    size_t smem = smem_leader;
+    for (; ncl > 1; ncl--) {
+        const size_t hs = (size_t)((((n + 31) / 32) + 1) & ~1LL) * 4 + (size_t)tm_helper_slice((int)n, ncl - 1) * 8 + 64;
+        if (hs <= 200 * 1024) { smem = std::max(smem_leader, hs); break; }
+    }
+#define TM_LAUNCH(M)                                                                                      \
     do {                                                                                                  \
-        TG_CUDA_CHECK(cudaFuncSetAttribute(tmfg_heap_kernel<C, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+        TG_CUDA_CHECK(cudaFuncSetAttribute(tmfg_heap_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                            (int)smem));                                                  \
-        tmfg_heap_kernel<C, M><<<1, TM_T, smem, st>>>(A);                                                 \
+        cudaLaunchConfig_t cfg = {};                                                                      \
+        cudaLaunchAttribute attr[1];                                                                      \
+        cfg.blockDim = dim3(TM_T, 1, 1);                                                                  \
+        cfg.dynamicSmemBytes = smem;                                                                      \
+        cfg.stream = st;                                                                                  \
+        attr[0].id = cudaLaunchAttributeClusterDimension;                                                 \
+        attr[0].val.clusterDim.y = 1;                                                                     \
+        attr[0].val.clusterDim.z = 1;                                                                     \
+        cfg.attrs = attr;                                                                                 \
+        cfg.numAttrs = 1;                                                                                 \
+        int k = ncl;                                                                                      \
+        for (; k > 1; k--) {                                                                              \
+            cfg.gridDim = dim3(k, 1, 1);                                                                  \
+            attr[0].val.clusterDim.x = k;                                                                 \
+            int nc = 0;                                                                                   \
+            if (cudaOccupancyMaxActiveClusters(&nc, tmfg_heap_kernel<M>, &cfg) == cudaSuccess && nc > 0) break; \
+            cudaGetLastError();                                                                           \
+        }                                                                                                 \
+        cfg.gridDim = dim3(k, 1, 1);                                                                      \
+        attr[0].val.clusterDim.x = k;                                                                     \
+        TG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, tmfg_heap_kernel<M>, A));                                  \
         tg_count_launch(1);                                                                               \
     } while (0)
-    if (smem_cur && smem_mc) TM_LAUNCH(true, true);
-    else if (smem_cur) TM_LAUNCH(true, false);
-    else TM_LAUNCH(false, false);
+    if (smem_st) TM_LAUNCH(true);
+    else TM_LAUNCH(false);
 #undef TM_LAUNCH
     TG_LAUNCH_CHECK();
     return TG_OK;

@@ -1,0 +1,10 @@
+#!/bin/bash
+# build_variant.sh NAME "-DDEFINES..." : profile build of tmfg.cu with extra defines -> _lib/libtmfg_b200_NAME.so
+set -e
+D=$(cd "$(dirname "$0")/../paper_2408_09399_b200/csrc" && pwd)
+L=$D/../_lib
+/usr/local/cuda/bin/nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -DTM_PROFILE=${PROF:-1} $2 \
+  -Xcompiler -fPIC -Xcompiler -fvisibility=hidden --expt-relaxed-constexpr -ccbin /usr/bin/g++ -c $D/tmfg.cu -o /tmp/tmfg_$1.o
+objs=$(ls $L/obj/*.o | grep -v tmfg.o)
+/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -Xcompiler -fPIC $objs /tmp/tmfg_$1.o -o $L/libtmfg_b200_$1.so
+echo built $L/libtmfg_b200_$1.so
