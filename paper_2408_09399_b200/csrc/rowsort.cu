@@ -26,6 +26,7 @@
 #include "common.cuh"
 
 #include <cmath>
+#include <cstdlib>
 
 namespace {
 
@@ -296,6 +297,9 @@ __global__ void clique_screen_kernel(const double *__restrict__ screen, int64_t 
 // Radius = 8x that sum of depths (+ 50) times u ~ 1.1e-16 -> 9e-16 per level.
 __device__ __forceinline__ double rs_screen_radius(int n, double abs_sum) {
     return (double)((n + 1023) / 1024 + 60) * 9e-16 * abs_sum;
+}
+__device__ __forceinline__ double rs_screen_radius_t(int n, int threads, double abs_sum) {
+    return (double)((n + threads - 1) / threads + 60) * 9e-16 * abs_sum;
 }
 
 struct RsMisc {
@@ -696,6 +700,446 @@ row_sort_tma_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restri
 #undef RS_PH
 }
 
+// ---------------------------------------------------------------- float-key kernel
+// The production sort for n <= FK_NMAX: one 1024-thread CTA per SM, persistent over rows.
+//  * bucket arithmetic runs on float keys: fl(x) is monotone (non-strictly) in x,
+//    and so is every float step of the bucket map, so bucket(x) is monotone and
+//    equal doubles share a bucket; float-EQUAL keys are ordered by their doubles
+//    re-read through L2 (only ties at float precision take that path);
+//  * a row buffer is recycled: after the first pass the keys live in registers
+//    as floats and the buffer holds the float keys (4n B) and the (bucket, id)
+//    scatter array (4n B).  With two buffers (n <~ 12.5k) the TMA load of the
+//    next row is issued as soon as the current row's doubles are consumed;
+//  * correlation rows (every off-diagonal value in [-1, 1], no NaN) use the
+//    fixed coarse map t = (1 - f) * C/2 -- no min/max reduction; other rows use
+//    their float range, NaN keys go to the last bucket and are ordered exactly
+//    (a separate instantiation, so the common path carries no NaN logic);
+//  * float -> integer steps use the 1.5 * 2^23 magic add (round to nearest, a
+//    monotone map) on the FMA pipe; coarse bin c covers t in [c - 1/2, c + 1/2],
+//    d = t - c is exact, and fb = rn(d f_c + base_c + f_c / 2) lies in
+//    [base_c, base_c + f_c], so the map stays monotone across bins;
+//  * the coarse bins get fine buckets in proportion to a 1/4-sample histogram
+//    (up to 3 per key), one packed-u16 shared atomic per key gives bucket +
+//    arrival rank, a block scan the offsets, the (bucket, id) pairs are scattered;
+//  * the exact rank inside a bucket runs by sorted POSITION: a bucket's members
+//    are consecutive lanes of a warp, their keys come by shuffles; buckets that
+//    cross a warp boundary walk shared memory.
+constexpr int FK_T = 1024;
+constexpr float FK_MAGIC = 12582912.0f;   // 1.5 * 2^23: x + MAGIC has rn(x) in its low 22 bits
+
+struct FkPlan {
+    int n, C, NBcap, stride, nbuf;
+    float fs, hc;
+    size_t off_sidx, off_cinfo, off_misc, off_bar, off_f16, smem;
+};
+
+struct FkMisc {
+    double rsum[32], rabs[32];
+    float rmn[32], rmx[32];
+    uint32_t wsum[32];
+    double diag;
+    int nb;
+};
+
+__host__ FkPlan fk_plan(int64_t n, int nbuf, size_t smem_max, double fs_cap) {
+    FkPlan p;
+    p.n = (int)n;
+    p.nbuf = nbuf;
+    const int m = (int)n - 1;
+    p.C = rs_coarse_bins(m);   // coarse bins 0..C (C + 1 of them)
+    p.hc = 0.5f * (float)p.C;
+    p.stride = (int)((n + 2) & ~1LL);
+    p.off_sidx = tg_align_up((size_t)n * sizeof(float), 16);
+    {
+        const int need = (int)((p.off_sidx + (size_t)n * 4 + 15) / 8);
+        if (p.stride < need) p.stride = (need + 1) & ~1;
+    }
+    size_t off = (size_t)nbuf * p.stride * sizeof(double);
+    p.off_cinfo = tg_align_up(off, 16);
+    off = p.off_cinfo + (size_t)(p.C + 1) * sizeof(float2);
+    p.off_misc = tg_align_up(off, 16);
+    off = p.off_misc + sizeof(FkMisc);
+    p.off_bar = tg_align_up(off, 16);
+    off = p.off_bar + 16;
+    p.off_f16 = tg_align_up(off, 16);
+    const size_t fixed = p.off_f16 + 64;
+    double room = smem_max > fixed ? (double)(smem_max - fixed) / 2.0 : 0.0;   // u16 entries
+    double fs = (room - 2.0 * p.C - 16.0) / (double)(m > 0 ? m : 1);
+    if (fs > fs_cap) fs = fs_cap;
+    p.fs = (float)fs;
+    p.NBcap = 2 * (p.C + 1) + (int)std::ceil(fs * m) + 4;
+    p.smem = p.off_f16 + (size_t)(p.NBcap / 2 + 2) * sizeof(uint32_t);
+    if (fs < 0.45 || p.NBcap >= 65535) p.smem = (size_t)-1;
+    return p;
+}
+
+__device__ __forceinline__ int fk_rni(float x) {   // rn(x) for 0 <= x < 2^22
+    return __float_as_int(x + FK_MAGIC) & 0x3fffff;
+}
+
+// coarse bin of key f: rn((hi - f) * scale) in [0, C]; general rows clamp, NaN -> C
+template <bool ODD>
+__device__ __forceinline__ int fk_coarse(float f, float hs, float scale, int C) {
+    const float t = fmaf(f, -scale, hs);
+    if (!ODD) return fk_rni(t);
+    if (f != f) return C;
+    const float tc = fminf(fmaxf(t, 0.0f), (float)C);
+    return fk_rni(tc);
+}
+
+struct FkRow {
+    float *fkey;
+    uint32_t *sidx, *f16;
+    float2 *cinfo;
+    uint32_t *ccnt;
+    FkMisc *ms;
+    const double *row;
+    int32_t *out;
+    int n, m, vi, C, nsamp;
+    float fs, hc;
+};
+
+// phases 2-5 of one row; ODD: rows with NaN or values outside [-1, 1]
+template <bool ODD, int KPT>
+__device__ __forceinline__ void fk_row(const FkRow &R, const float (&fk)[KPT]) {
+    constexpr int NT = FK_T, W = NT / 32;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n = R.n, m = R.m, vi = R.vi, C = R.C;
+    float *fkey = R.fkey;
+    uint32_t *sidx = R.sidx, *f16 = R.f16, *ccnt = R.ccnt;
+    float2 *cinfo = R.cinfo;
+    const uint16_t *o16 = reinterpret_cast<const uint16_t *>(f16);
+    FkMisc &ms = *R.ms;
+    float hs = R.hc, scale = R.hc;   // t = hs - f * scale
+    if (ODD) {   // the row's float range, histogram again
+        float fmn = INFINITY, fmx = -INFINITY;
+#pragma unroll
+        for (int e = 0; e < KPT; e++) {
+            const int j = tid + e * NT;
+            if (j < n && j != vi) { fmn = fminf(fmn, fk[e]); fmx = fmaxf(fmx, fk[e]); }
+        }
+        for (int o = 16; o; o >>= 1) {
+            fmn = fminf(fmn, __shfl_xor_sync(0xffffffffu, fmn, o));
+            fmx = fmaxf(fmx, __shfl_xor_sync(0xffffffffu, fmx, o));
+        }
+        if (lane == 0) { ms.rmn[warp] = fmn; ms.rmx[warp] = fmx; }
+        for (int c = tid; c <= C; c += NT) ccnt[c] = 0u;
+        __syncthreads();
+        float lo = INFINITY, hi = -INFINITY;
+        for (int w = 0; w < W; w++) { lo = fminf(lo, ms.rmn[w]); hi = fmaxf(hi, ms.rmx[w]); }
+        const float wd = hi - lo;
+        scale = (wd > 0.0f && wd < INFINITY) ? (float)C / wd : 0.0f;
+        if (!(hi < INFINITY && hi > -INFINITY)) hi = 0.0f;
+        hs = hi * scale;
+#pragma unroll
+        for (int e = 0; e < KPT; e += 4) {
+            const int j = tid + e * NT;
+            if (j < n && j != vi) atomicAdd(&ccnt[fk_coarse<true>(fk[e], hs, scale, C)], 1u);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int e = 0; e < KPT; e++) {
+        const int j = tid + e * NT;
+        if (j < n) fkey[j] = fk[e];
+    }
+    // ---- 2: fine buckets per coarse bin (one thread per bin) -> per-bin (A, B)
+    {
+        const float fsc = (float)m * R.fs / (float)(R.nsamp > 0 ? R.nsamp : 1) * 0.9999f;
+        const uint32_t f = tid <= C ? 1u + (uint32_t)((float)ccnt[tid] * fsc) : 0u;
+        uint32_t incl = f;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) ms.wsum[warp] = incl;
+        __syncthreads();   // B2
+        if (tid <= C) {
+            uint32_t off = 0;
+            for (int w = 0; w < warp; w++) off += ms.wsum[w];
+            const uint32_t base = off + incl - f;
+            // d = t - c in [-1/2, 1/2] (exact): fb = rn(d f + base + f/2) in [base, base + f]
+            cinfo[tid] = make_float2((float)base + 0.5f * (float)f, (float)f);
+            if (tid == C) ms.nb = (int)(base + f) + 1;
+        }
+    }
+    __syncthreads();   // B3
+    // ---- 3: fine bucket + arrival rank (one packed-u16 shared atomic per key)
+    uint32_t pk[KPT];
+    const int nan_fb = ms.nb - 1;
+#pragma unroll
+    for (int e = 0; e < KPT; e++) {
+        const int j = tid + e * NT;
+        pk[e] = 0xffffffffu;
+        if (j < n && j != vi) {
+            const float f = fk[e];
+            float t = fmaf(f, -scale, hs);
+            if (ODD) t = fminf(fmaxf(t, 0.0f), (float)C);
+            const float y = t + FK_MAGIC;
+            const int c = __float_as_int(y) & 0x3fffff;
+            const float d = t - (y - FK_MAGIC);   // exact
+            const float2 ab = cinfo[c];
+            int fb = fk_rni(fmaf(d, ab.y, ab.x));
+            if (ODD && f != f) fb = nan_fb;
+            const uint32_t sh = (fb & 1) << 4;
+            const uint32_t old = atomicAdd(&f16[fb >> 1], 1u << sh);
+            pk[e] = __byte_perm((uint32_t)fb, old >> sh, 0x1054);   // (fb << 16) | (old >> sh) & 0xffff
+        }
+    }
+    __syncthreads();   // B4
+    for (int c = tid; c <= C; c += NT) ccnt[c] = 0u;   // next row's histogram (cinfo is dead)
+    // ---- 4: exclusive scan of the packed counters, scatter (bucket, id)
+    {
+        const int nw = (ms.nb + 2) >> 1;
+        const int per = (nw + NT - 1) / NT;
+        const int w0 = tid * per;
+        uint32_t s = 0;
+        for (int q = 0; q < per; q++) {
+            const int w = w0 + q;
+            if (w < nw) { const uint32_t x = f16[w]; s += (x + (x << 16)) >> 16; }
+        }
+        uint32_t incl = s;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) ms.wsum[warp] = incl;
+        __syncthreads();   // B5
+        uint32_t wex;
+        {
+            const uint32_t wv = ms.wsum[lane];
+            uint32_t wi = wv;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+                if (lane >= o) wi += y;
+            }
+            wex = __shfl_sync(0xffffffffu, wi - wv, warp);
+        }
+        uint32_t run = wex + incl - s;
+        for (int q = 0; q < per; q++) {
+            const int w = w0 + q;
+            if (w < nw) {
+                const uint32_t x = f16[w];
+                f16[w] = run * 0x10001u + (x << 16);    // (run, run + lo)
+                run += (x + (x << 16)) >> 16;           // lo + hi
+            }
+        }
+    }
+    __syncthreads();   // B6
+#pragma unroll
+    for (int e = 0; e < KPT; e++) {
+        if (pk[e] != 0xffffffffu)
+            sidx[o16[pk[e] >> 16] + (pk[e] & 0xffffu)] = (pk[e] & 0xffff0000u) | (uint32_t)(tid + e * NT);
+    }
+    __syncthreads();   // B7
+    // ---- 5: exact rank inside the bucket by sorted position, coalesced id store
+    const double *row = R.row;
+    int32_t *out = R.out;
+    for (int kb = warp * 32; kb < m; kb += NT) {
+        const int k = kb + lane;
+        const bool live = k < m;
+        const uint32_t sk = live ? sidx[k] : (0xfffe0000u | (uint32_t)lane);
+        const int fb = (int)(sk >> 16), j = (int)(sk & 0xffffu);
+        const float fj = fkey[j];
+        // the bucket's lanes: a run of equal fb (positions are bucket-sorted)
+        const int fprev = __shfl_up_sync(0xffffffffu, fb, 1);
+        const unsigned starts = __ballot_sync(0xffffffffu, lane == 0 || fprev != fb);
+        const unsigned le = 0xffffffffu >> (31 - lane);   // lanes <= lane
+        const int first = 31 - __clz(starts & le);
+        const unsigned above = starts & ~le;
+        const int sz = (above ? __ffs(above) - 1 : 32) - first;
+        // does the first run continue before lane 0, the last one after lane 31?
+        bool cross = false;
+        if (first == 0 && kb > 0) cross = (int)(sidx[kb - 1] >> 16) == fb;
+        if (first + sz == 32 && kb + 32 < m) cross |= (int)(sidx[kb + 32] >> 16) == fb;
+        const int smax = __reduce_max_sync(0xffffffffu, (live && !cross) ? sz : 1);
+        int rank = 0, ties = 0;
+        for (int i = 0; i < smax; i++) {
+            const float fo = __shfl_sync(0xffffffffu, fj, first + i);
+            const bool in = i < sz;
+            if (!ODD) {
+                rank += in & (fo > fj);
+                ties += in & (fo == fj);
+            } else {
+                const bool no = fo != fo, nj = fj != fj;
+                rank += in & ((fo > fj) | (nj & !no));
+                ties += in & ((fo == fj) | (nj & no));
+            }
+        }
+        if (live) {
+            int pos;
+            if (!cross) {
+                pos = kb + first + rank;
+                if (ties > 1) {   // float ties (itself included): order by the doubles, then id
+                    const double xj = __ldg(row + j);
+                    rank = 0;
+                    for (int i = 0; i < sz; i++) {
+                        const int q = kb + first + i;
+                        if (q == k) continue;
+                        const int o = (int)(sidx[q] & 0xffffu);
+                        rank += rs_before(__ldg(row + o), o, xj, j);
+                    }
+                    pos = kb + first + rank;
+                }
+            } else {
+                const int s0 = o16[fb], s1 = o16[fb + 1];
+                rank = 0;
+                int tie = 0;
+                for (int q = s0; q < s1; q++) {
+                    const float fo = fkey[sidx[q] & 0xffffu];
+                    if (!ODD) {
+                        rank += fo > fj;
+                        tie += fo == fj;
+                    } else {
+                        const bool no = fo != fo, nj = fj != fj;
+                        rank += (fo > fj) | (nj & !no);
+                        tie += (fo == fj) | (nj & no);
+                    }
+                }
+                if (tie > 1) {
+                    const double xj = __ldg(row + j);
+                    rank = 0;
+                    for (int q = s0; q < s1; q++) {
+                        const int o = (int)(sidx[q] & 0xffffu);
+                        if (o != j) rank += rs_before(__ldg(row + o), o, xj, j);
+                    }
+                }
+                pos = s0 + rank;
+            }
+            out[pos] = j;
+        }
+    }
+}
+
+template <int KPT>
+__global__ void __launch_bounds__(FK_T, 1)
+row_sort_fk_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restrict__ order,
+                   double *__restrict__ screen, FkPlan pl) {
+    extern __shared__ __align__(16) unsigned char fk_smem[];
+    constexpr int NT = FK_T, W = NT / 32;
+    const int n = (int)n64;
+    const int m = n - 1;
+    uint32_t *ccnt = reinterpret_cast<uint32_t *>(fk_smem + pl.off_cinfo);   // histogram, then (A, B)
+    FkMisc &ms = *reinterpret_cast<FkMisc *>(fk_smem + pl.off_misc);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(fk_smem + pl.off_bar);
+    uint32_t *f16 = reinterpret_cast<uint32_t *>(fk_smem + pl.off_f16);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int C = pl.C;
+    const int nw16 = pl.NBcap / 2 + 2;
+    const size_t bstride = (size_t)pl.stride * sizeof(double);
+
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;\n" ::"r"(rt_smem_u32(&bar[0])) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;\n" ::"r"(rt_smem_u32(&bar[1])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    for (int c = tid; c <= C; c += NT) ccnt[c] = 0u;
+    __syncthreads();
+    int64_t v = blockIdx.x;
+    if (tid == 0 && v < n) rt_bulk_row(reinterpret_cast<double *>(fk_smem), S + v * n64, n, &bar[0]);
+    int nsamp_all = 0;   // sampled keys: e % 4 == 0
+#pragma unroll
+    for (int e = 0; e < KPT; e += 4) {
+        const int r = n - e * NT;
+        nsamp_all += r < 0 ? 0 : (r < NT ? r : NT);
+    }
+    FkRow R;
+    R.f16 = f16;
+    R.cinfo = reinterpret_cast<float2 *>(ccnt);
+    R.ccnt = ccnt;
+    R.ms = &ms;
+    R.n = n;
+    R.m = m;
+    R.C = C;
+    R.fs = pl.fs;
+    R.hc = pl.hc;
+#if RS_DEBUG_PHASES
+    long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long pt = clock64();
+#define FK_PH(k) do { if (tid == 0) { const long long now = clock64(); ph[k] += now - pt; pt = now; } } while (0)
+#else
+#define FK_PH(k) do {} while (0)
+#endif
+    for (int it = 0; v < n; v += gridDim.x, it++) {
+        const int b = pl.nbuf == 2 ? (it & 1) : 0;
+        const unsigned parity = pl.nbuf == 2 ? (unsigned)((it >> 1) & 1) : (unsigned)(it & 1);
+        unsigned char *buf = fk_smem + (size_t)b * bstride;
+        const double *row = S + v * n64;
+        const double *vals = reinterpret_cast<const double *>(buf) + (((uintptr_t)row >> 3) & 1);
+        const int vi = (int)v;
+        rt_wait(&bar[b], parity);
+        FK_PH(0);
+        // ---- 1: doubles -> float keys (registers), screen sums, sampled coarse histogram
+        for (int i = tid; i < nw16; i += NT) f16[i] = 0u;
+        float fk[KPT];
+        double sm = 0.0, sa = 0.0;
+        bool odd = false;
+#pragma unroll
+        for (int e = 0; e < KPT; e++) {
+            const int j = tid + e * NT;
+            fk[e] = 0.0f;
+            if (j < n) {
+                const double x = vals[j];
+                sm += x;
+                sa += fabs(x);
+                const float f = __double2float_rn(x);
+                fk[e] = f;
+                if (j != vi) {
+                    odd |= !(fabsf(f) <= 1.0f);   // NaN or outside [-1, 1] at float precision
+                    if ((e & 3) == 0) atomicAdd(&ccnt[fk_coarse<true>(f, pl.hc, pl.hc, C)], 1u);
+                } else {
+                    ms.diag = x;
+                }
+            }
+        }
+        if (screen) {
+            for (int o = 16; o; o >>= 1) {
+                sm += __shfl_xor_sync(0xffffffffu, sm, o);
+                sa += __shfl_xor_sync(0xffffffffu, sa, o);
+            }
+            if (lane == 0) { ms.rsum[warp] = sm; ms.rabs[warp] = sa; }
+        }
+        const bool row_odd = __syncthreads_or(odd);   // B1: every double of the row is consumed
+        if (tid == 0) {
+            const int64_t vn = v + gridDim.x;
+            if (pl.nbuf == 2 && vn < n)
+                rt_bulk_row(reinterpret_cast<double *>(fk_smem + (size_t)(b ^ 1) * bstride), S + vn * n64, n,
+                            &bar[b ^ 1]);
+        }
+        if (screen && warp == W - 1) {
+            double s1 = ms.rsum[lane], s2 = ms.rabs[lane];
+            for (int o = 16; o; o >>= 1) {
+                s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+                s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+            }
+            if (lane == 0) {
+                screen[vi] = __dsub_rn(s1, ms.diag);
+                screen[n + vi] = rs_screen_radius_t(n, NT, s2);
+            }
+        }
+        FK_PH(1);
+        R.fkey = reinterpret_cast<float *>(buf);
+        R.sidx = reinterpret_cast<uint32_t *>(buf + pl.off_sidx);
+        R.row = row;
+        R.out = order + v * (int64_t)m;
+        R.vi = vi;
+        R.nsamp = nsamp_all - (((vi / NT) & 3) == 0 ? 1 : 0);
+        if (row_odd) fk_row<true, KPT>(R, fk);
+        else fk_row<false, KPT>(R, fk);
+        __syncthreads();   // B8: buffer b and the counters are free
+        FK_PH(6);
+        if (tid == 0 && pl.nbuf == 1) {
+            const int64_t vn = v + gridDim.x;
+            if (vn < n) rt_bulk_row(reinterpret_cast<double *>(fk_smem), S + vn * n64, n, &bar[0]);
+        }
+    }
+#if RS_DEBUG_PHASES
+    if (tid == 0)
+        for (int k = 0; k < 7; k++) atomicAdd((unsigned long long *)&g_rs_phase[k], (unsigned long long)ph[k]);
+#endif
+#undef FK_PH
+}
+
 // ---------------------------------------------------------------- large rows
 // n > 16384: the same two-level bucket algorithm; the row is read through L2,
 // the per-key (bucket, rank) pairs live in a per-CTA global scratch slice and
@@ -880,6 +1324,7 @@ row_sort_global_kernel(const double *__restrict__ S, int64_t n64, int32_t *__res
 }
 
 constexpr size_t RS_SMEM_MAX = 227 * 1024;
+constexpr int FK_NMAX = 24576;
 
 // numpy's pairwise plan for n (a pure function of n), cached per host thread
 const PwTree<PW_MAXNODES> &pw_host_plan(int n) {
@@ -908,6 +1353,31 @@ TG_API int tg_row_sort_f64(const double *S, int64_t n, int32_t *order, double *s
     cudaStream_t st = tg_stream(stream);
     int grid = tg_num_sms();
     if (grid > n) grid = (int)n;
+    if (n <= FK_NMAX && !getenv("TG_SORT_OLD")) {
+        // two row buffers (the next row's TMA overlaps this row) when they leave room
+        // for >= 1.5 fine buckets per key, else one
+        const char *fse = getenv("TG_SORT_FS");
+        const double fcap = fse ? atof(fse) : 3.0;
+        FkPlan pl = fk_plan(n, 2, RS_SMEM_MAX, fcap);
+        if (pl.smem > RS_SMEM_MAX || pl.fs < 1.5f) pl = fk_plan(n, 1, RS_SMEM_MAX, fcap);
+        if (pl.smem > RS_SMEM_MAX) return TG_ERR_ARG;
+        const int K = (int)((n + FK_T - 1) / FK_T);
+#define FK_LAUNCH(KK)                                                                                      \
+    do {                                                                                                   \
+        auto kfn = row_sort_fk_kernel<KK>;                                                                 \
+        TG_CUDA_CHECK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem)); \
+        kfn<<<grid, FK_T, pl.smem, st>>>(S, n, order, screen, pl); tg_count_launch(1);                      \
+    } while (0)
+        if (K <= 2) FK_LAUNCH(2);
+        else if (K <= 4) FK_LAUNCH(4);
+        else if (K <= 8) FK_LAUNCH(8);
+        else if (K <= 12) FK_LAUNCH(12);
+        else if (K <= 16) FK_LAUNCH(16);
+        else FK_LAUNCH(24);
+#undef FK_LAUNCH
+        TG_LAUNCH_CHECK();
+        return TG_OK;
+    }
     if (n <= 16384) {
         // preference: two row buffers (TMA of row v+grid overlaps row v) with one key per
         // fine bucket; then two keys per bucket; then a single buffer
