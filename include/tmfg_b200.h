@@ -227,7 +227,9 @@ typedef struct {
     int32_t i0;
     int32_t j0;
 } tg_gm_tile_t;
-size_t tg_group_max_workspace_bytes(int64_t n, int64_t ntiles);
+/* H: the hub count of a hub-mode oracle (0 in exact mode); the workspace holds the
+ * permuted vertex-major fp32/fp64 copies of hub_dist used by the hub-mode tiles. */
+size_t tg_group_max_workspace_bytes(int64_t n, int64_t ntiles, int64_t H);
 int tg_group_max_batch(const tg_oracle_t *oracle, const int32_t *perm, const int32_t *gid, const void *subs,
                        int64_t nsub, const void *tiles, int64_t ntiles, double *out, int64_t out_len, void *ws,
                        size_t ws_bytes, void *stream);

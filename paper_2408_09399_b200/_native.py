@@ -96,7 +96,7 @@ _PROTOS = {
     "tg_assign_vertices": (ctypes.c_int, [ctypes.POINTER(TgOracle), c_p, c_i64, c_p, c_p, c_p, c_p, c_sz, c_p]),
     "tg_group_blocks": (ctypes.c_int, [ctypes.POINTER(TgOracle), c_p, c_p, c_i64, c_p, c_p, c_p]),
     "tg_oracle_block": (ctypes.c_int, [ctypes.POINTER(TgOracle), c_p, c_i64, c_p, c_i64, ctypes.c_int32, c_p, c_p]),
-    "tg_group_max_workspace_bytes": (c_sz, [c_i64, c_i64]),
+    "tg_group_max_workspace_bytes": (c_sz, [c_i64, c_i64, c_i64]),
     "tg_group_max_batch": (ctypes.c_int, [ctypes.POINTER(TgOracle), c_p, c_p, c_p, c_i64, c_p, c_i64, c_p, c_i64,
                                           c_p, c_sz, c_p]),
     "tg_nn_chain_batch": (ctypes.c_int, [c_p, c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p]),

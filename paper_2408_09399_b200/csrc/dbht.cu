@@ -13,6 +13,7 @@
 // by max into the (group x group) matrix.  Tiles of 64x64 pairs, hub columns
 // staged in shared memory 32 hubs at a time, 4x4 register micro-tiles.
 #include "common.cuh"
+#include <cstdlib>
 
 namespace {
 
@@ -395,6 +396,153 @@ group_max_tile_kernel(tg_oracle_t o, const int32_t *__restrict__ perm, const int
                 if (o.mode == 1 || gi <= gj) atomicMax(&out[sb.out_off + (int64_t)gi * sb.m + gj], tg_dbits(best));
                 j = k;
             }
+        }
+        __syncthreads();
+    }
+}
+
+// Hub-mode group max with an fp32 screen.  For a pair (u, v) the hub estimate is
+// D = min_h fl64(hd[h,u] + hd[h,v]) (apsp.py:136-143); in fp32, d' = min_h
+// fl32(fl32(hd[h,u]) + fl32(hd[h,v])) satisfies |d' - D| <= 2^-22.8 D + 2^-147
+// (all terms >= 0).  Per tile and per (row group run, column group run) the
+// largest d' is taken; every pair with d' >= lmax' (1 - 2^-19) - 2^-140 -- a
+// superset of the pairs attaining the tile-local maximum of D -- gets its exact
+// fp64 D and only those are maxed into M.  The maximum over tiles of the exact
+// tile-local maxima is M's exact entry.  The hub distances are first laid out
+// vertex-major in the sub-problems' permuted order (hp_fill_kernel, fp32 and
+// fp64 copies), so every panel load is a coalesced row segment.
+constexpr int GH_T = 256;
+constexpr int GH_MAXC = GM_TILE * GM_TILE;
+constexpr int GH_LD = GM_HC + 1;   // panel row stride (conflict-free both ways)
+
+__global__ void hp_fill_kernel(tg_oracle_t o, const int32_t *__restrict__ perm, int64_t total, int Hp,
+                               float *__restrict__ hpf, double *__restrict__ hpd) {
+    const int64_t cnt = total * Hp;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < cnt; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = e / Hp;
+        const int h = (int)(e - g * Hp);
+        const double x = h < o.H ? o.hub_dist[(int64_t)h * o.n + perm[g]] : INFINITY;
+        hpd[e] = x;
+        hpf[e] = (float)x;
+    }
+}
+
+__global__ void __launch_bounds__(GH_T, 2)
+group_max_hub_kernel(tg_oracle_t o, const int32_t *__restrict__ gid, const GmSub *__restrict__ subs,
+                     const GmTile *__restrict__ tiles, int64_t ntiles, int Hp, const float *__restrict__ hpf,
+                     const double *__restrict__ hpd, unsigned long long *__restrict__ out,
+                     const uint64_t *__restrict__ mask) {
+    constexpr int PF = GM_TILE * GH_LD * 4, PD = GM_TILE * GH_LD * 8;
+    __shared__ __align__(16) unsigned char gh_raw[2 * PD];
+    float (*Af)[GH_LD] = reinterpret_cast<float (*)[GH_LD]>(gh_raw);     // [64 rows][32 hubs]
+    float (*Bf)[GH_LD] = reinterpret_cast<float (*)[GH_LD]>(gh_raw + PF);
+    unsigned *lmax = reinterpret_cast<unsigned *>(gh_raw + 2 * PF);      // [64 runs][64 runs]
+    double (*Ad)[GH_LD] = reinterpret_cast<double (*)[GH_LD]>(gh_raw);   // exact pass
+    double (*Bd)[GH_LD] = reinterpret_cast<double (*)[GH_LD]>(gh_raw + PD);
+    static_assert(2 * PF + GM_TILE * GM_TILE * 4 <= 2 * PD, "shared layout");
+    __shared__ uint16_t cand[GH_MAXC];
+    __shared__ int ncand;
+    __shared__ int rg[GM_TILE], cg[GM_TILE], lr[GM_TILE], lc[GM_TILE];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tx = tid & 15, ty = tid >> 4;   // 16 x 16 threads, rows ty*4.., cols tx*4..
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const GmTile tl = tiles[t];
+        const GmSub sb = subs[tl.sub];
+        const int rows = min(GM_TILE, sb.len - tl.i0), cols = min(GM_TILE, sb.len - tl.j0);
+        const int64_t rbase = sb.perm_off + tl.i0, cbase = sb.perm_off + tl.j0;
+        if (tid < GM_TILE) {
+            const int i = tid;
+            rg[i] = i < rows ? gid[rbase + i] : -1;
+            cg[i] = i < cols ? gid[cbase + i] : -1;
+        }
+        if (tid == 0) ncand = 0;
+        for (int e = tid; e < GM_TILE * GM_TILE; e += GH_T) lmax[e] = 0u;
+        __syncthreads();
+        if (warp < 2) {   // run index of each row (warp 0) / column (warp 1) group
+            const int *g = warp == 0 ? rg : cg;
+            int *l = warp == 0 ? lr : lc;
+            int carry = 0;
+            for (int base = 0; base < GM_TILE; base += 32) {
+                const int i = base + lane;
+                const unsigned b = __ballot_sync(0xffffffffu, i > 0 && g[i] != g[i - 1]);
+                l[i] = carry + __popc(b & (0xffffffffu >> (31 - lane)));
+                carry += __popc(b);
+            }
+        }
+        // ---- fp32 screen
+        float acc[4][4];
+#pragma unroll
+        for (int r = 0; r < 4; r++)
+#pragma unroll
+            for (int c = 0; c < 4; c++) acc[r][c] = INFINITY;
+        for (int h0 = 0; h0 < Hp; h0 += GM_HC) {
+            for (int e = tid; e < GM_HC * GM_TILE; e += GH_T) {
+                const int i = e >> 5, h = e & 31;
+                Af[i][h] = i < rows ? hpf[(rbase + i) * Hp + h0 + h] : INFINITY;
+                Bf[i][h] = i < cols ? hpf[(cbase + i) * Hp + h0 + h] : INFINITY;
+            }
+            __syncthreads();
+#pragma unroll 4
+            for (int h = 0; h < GM_HC; h++) {
+                float av[4], bv[4];
+#pragma unroll
+                for (int r = 0; r < 4; r++) av[r] = Af[ty * 4 + r][h];
+#pragma unroll
+                for (int c = 0; c < 4; c++) bv[c] = Bf[tx * 4 + c][h];
+#pragma unroll
+                for (int r = 0; r < 4; r++)
+#pragma unroll
+                    for (int c = 0; c < 4; c++) acc[r][c] = fminf(acc[r][c], __fadd_rn(av[r], bv[c]));
+            }
+            __syncthreads();
+        }
+        // ---- tile-local maxima per (row run, column run); override pairs are excluded
+        const uint64_t *mk = mask + (size_t)t * GM_TILE;
+        uint32_t valid = 0;
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+            const int i = ty * 4 + r;
+            const uint64_t mrow = i < rows ? mk[i] : ~0ull;
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                const int j = tx * 4 + c;
+                if (i < rows && j < cols && !((mrow >> j) & 1ull)) {
+                    valid |= 1u << (r * 4 + c);
+                    atomicMax(&lmax[lr[i] * GM_TILE + lc[j]], __float_as_uint(acc[r][c]));
+                }
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < 4; r++)
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                if (!((valid >> (r * 4 + c)) & 1u)) continue;
+                const int i = ty * 4 + r, j = tx * 4 + c;
+                const float lm = __uint_as_float(lmax[lr[i] * GM_TILE + lc[j]]);
+                const float thr = __fsub_rn(__fmul_rn(lm, 1.0f - 0x1p-19f), 0x1p-140f);
+                if (acc[r][c] >= thr) cand[atomicAdd(&ncand, 1)] = (uint16_t)((i << 6) | j);
+            }
+        __syncthreads();
+        // ---- exact fp64 estimate of the candidates (GH_T per pass over the hubs)
+        const int nc = ncand;
+        for (int cb = 0; cb < nc; cb += GH_T) {
+            const int k = cb + tid;
+            const int ci = k < nc ? (cand[k] >> 6) : 0, cj = k < nc ? (cand[k] & 63) : 0;
+            double ex = INFINITY;
+            for (int h0 = 0; h0 < Hp; h0 += GM_HC) {
+                for (int e = tid; e < GM_HC * GM_TILE; e += GH_T) {
+                    const int i = e >> 5, h = e & 31;
+                    Ad[i][h] = i < rows ? hpd[(rbase + i) * Hp + h0 + h] : INFINITY;
+                    Bd[i][h] = i < cols ? hpd[(cbase + i) * Hp + h0 + h] : INFINITY;
+                }
+                __syncthreads();
+                if (k < nc)
+#pragma unroll 8
+                    for (int h = 0; h < GM_HC; h++) ex = fmin(ex, __dadd_rn(Ad[ci][h], Bd[cj][h]));
+                __syncthreads();
+            }
+            if (k < nc) atomicMax(&out[sb.out_off + (int64_t)rg[ci] * sb.m + cg[cj]], tg_dbits(ex));
         }
         __syncthreads();
     }
@@ -847,8 +995,10 @@ TG_API int tg_group_blocks(const tg_oracle_t *o, const int32_t *perm, const int6
     return TG_OK;
 }
 
-TG_API size_t tg_group_max_workspace_bytes(int64_t n, int64_t ntiles) {
-    return tg_align_up((size_t)n * 4, 256) * 2 + tg_align_up((size_t)ntiles * GM_TILE * 8, 256) + 512;
+TG_API size_t tg_group_max_workspace_bytes(int64_t n, int64_t ntiles, int64_t H) {
+    const size_t Hp = (size_t)((H + GM_HC - 1) / GM_HC * GM_HC);
+    return tg_align_up((size_t)n * 4, 256) * 2 + tg_align_up((size_t)ntiles * GM_TILE * 8 + 8, 256) +
+           tg_align_up((size_t)n * Hp * 4, 256) + tg_align_up((size_t)n * Hp * 8, 256) + 1024;
 }
 
 TG_API int tg_group_max_batch(const tg_oracle_t *o, const int32_t *perm, const int32_t *gid, const void *subs_v,
@@ -856,7 +1006,7 @@ TG_API int tg_group_max_batch(const tg_oracle_t *o, const int32_t *perm, const i
                               void *ws, size_t ws_bytes, void *stream) {
     if (!o || !perm || !gid || !subs_v || !tiles_v || !out || nsub < 0 || ntiles < 0) return TG_ERR_ARG;
     const int64_t n = o->n;
-    if (ws_bytes < tg_group_max_workspace_bytes(n, ntiles)) return TG_ERR_WORKSPACE;
+    if (ws_bytes < tg_group_max_workspace_bytes(n, ntiles, o->mode == 1 ? o->H : 0)) return TG_ERR_WORKSPACE;
     const GmSub *subs = reinterpret_cast<const GmSub *>(subs_v);
     const GmTile *tiles = reinterpret_cast<const GmTile *>(tiles_v);
     cudaStream_t st = tg_stream(stream);
@@ -889,8 +1039,21 @@ TG_API int tg_group_max_batch(const tg_oracle_t *o, const int32_t *perm, const i
     }
     if (ntiles > 0) {
         int grid = (int)min((int64_t)tg_num_sms() * 8, ntiles);
-        group_max_tile_kernel<<<grid, GM_T, 0, st>>>(*o, perm, gid, pos, subs, tiles, ntiles,
-                                                   reinterpret_cast<unsigned long long *>(out), mask); tg_count_launch(1);
+        if (o->mode == 1 && !getenv("TG_GM_OLD")) {
+            const int Hp = (int)((o->H + GM_HC - 1) / GM_HC * GM_HC);
+            float *hpf = ar.take<float>((size_t)total_len * Hp);
+            double *hpd = ar.take<double>((size_t)total_len * Hp);
+            if (!hpf || !hpd) return TG_ERR_WORKSPACE;
+            const int64_t cnt = total_len * Hp;
+            hp_fill_kernel<<<(unsigned)min((cnt + 255) / 256, (int64_t)tg_num_sms() * 16), 256, 0, st>>>(
+                *o, perm, total_len, Hp, hpf, hpd);
+            tg_count_launch(1);
+            group_max_hub_kernel<<<grid, GH_T, 0, st>>>(*o, gid, subs, tiles, ntiles, Hp, hpf, hpd,
+                                                      reinterpret_cast<unsigned long long *>(out), mask);
+        } else
+            group_max_tile_kernel<<<grid, GM_T, 0, st>>>(*o, perm, gid, pos, subs, tiles, ntiles,
+                                                       reinterpret_cast<unsigned long long *>(out), mask);
+        tg_count_launch(1);
     }
     group_max_finalize_kernel<<<(unsigned)min(nsub, (int64_t)65535), 256, 0, st>>>(subs, nsub, o->mode, out); tg_count_launch(1);
     TG_LAUNCH_CHECK();

@@ -196,7 +196,7 @@ int group_linkages(Ctx &cx, const std::vector<std::vector<const std::vector<int3
         out_off += (int64_t)m * m;
     }
     const int64_t ntiles = (int64_t)tiles.size();
-    const size_t ws_bytes = tg_group_max_workspace_bytes(cx.n, ntiles);
+    const size_t ws_bytes = tg_group_max_workspace_bytes(cx.n, ntiles, cx.oracle->mode == 1 ? cx.oracle->H : 0);
     const size_t b_perm = tg_align_up(perm.size() * 4, 256), b_sub = tg_align_up(subs.size() * sizeof(tg_gm_sub_t), 256);
     const size_t b_tile = tg_align_up((size_t)ntiles * sizeof(tg_gm_tile_t), 256);
     const size_t b_out = tg_align_up((size_t)std::max<int64_t>(out_off, 1) * 8, 256);

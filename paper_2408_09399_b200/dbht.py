@@ -236,7 +236,7 @@ def group_max_batch(oracle, subproblems):
     tile_d = D.to_device(np.frombuffer(tile_arr.tobytes(), dtype=np.uint8).copy(), t.uint8)
     out = D.empty((max(out_len, 1),), t.float64)
     s = _oracle_struct(oracle)
-    ws = D.Workspace.get(N.size("tg_group_max_workspace_bytes", oracle.n, int(tile_arr.shape[0])))
+    ws = D.Workspace.get(N.size("tg_group_max_workspace_bytes", oracle.n, int(tile_arr.shape[0]), int(s.H) if s.mode == 1 else 0))
     N.call("tg_group_max_batch", s, N.ptr(perm_d), N.ptr(gid_d), N.ptr(sub_d), int(sub_arr.shape[0]), N.ptr(tile_d),
            int(tile_arr.shape[0]), N.ptr(out), out_len, N.ptr(ws), ws.numel(), N.stream_ptr())
     return out, sub_arr
