@@ -731,6 +731,7 @@ struct FkPlan {
     int n, C, NBcap, stride, nbuf;
     float fs, hc;
     size_t off_sidx, off_cinfo, off_misc, off_bar, off_f16, smem;
+    size_t off_sid;   // segments: slot -> id table (row_seg_kernel)
 };
 
 struct FkMisc {
@@ -795,6 +796,7 @@ struct FkRow {
     FkMisc *ms;
     const double *row;
     int32_t *out;
+    const int32_t *sid;   // slot -> column id (segments); nullptr: the slot is the id
     int n, m, vi, C, nsamp;
     float fs, hc;
 };
@@ -832,9 +834,20 @@ __device__ __forceinline__ void fk_row(const FkRow &R, const float (&fk)[KPT]) {
         if (!(hi < INFINITY && hi > -INFINITY)) hi = 0.0f;
         hs = hi * scale;
 #pragma unroll
-        for (int e = 0; e < KPT; e += 4) {
-            const int j = tid + e * NT;
-            if (j < n && j != vi) atomicAdd(&ccnt[fk_coarse<true>(fk[e], hs, scale, C)], 1u);
+        if (R.sid) {   // segment slots are grouped by value: sample every 4th slot (threads 4k)
+            if ((tid & 3) == 0) {
+#pragma unroll
+                for (int e = 0; e < KPT; e++) {
+                    const int j = tid + e * NT;
+                    if (j < n) atomicAdd(&ccnt[fk_coarse<true>(fk[e], hs, scale, C)], 1u);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < KPT; e += 4) {
+                const int j = tid + e * NT;
+                if (j < n && j != vi) atomicAdd(&ccnt[fk_coarse<true>(fk[e], hs, scale, C)], 1u);
+            }
         }
         __syncthreads();
     }
@@ -935,6 +948,7 @@ __device__ __forceinline__ void fk_row(const FkRow &R, const float (&fk)[KPT]) {
     // ---- 5: exact rank inside the bucket by sorted position, coalesced id store
     const double *row = R.row;
     int32_t *out = R.out;
+    const int32_t *sid = R.sid;
     for (int kb = warp * 32; kb < m; kb += NT) {
         const int k = kb + lane;
         const bool live = k < m;
@@ -971,13 +985,15 @@ __device__ __forceinline__ void fk_row(const FkRow &R, const float (&fk)[KPT]) {
             if (!cross) {
                 pos = kb + first + rank;
                 if (ties > 1) {   // float ties (itself included): order by the doubles, then id
-                    const double xj = __ldg(row + j);
+                    const int idj = sid ? sid[j] : j;
+                    const double xj = __ldg(row + idj);
                     rank = 0;
                     for (int i = 0; i < sz; i++) {
                         const int q = kb + first + i;
                         if (q == k) continue;
                         const int o = (int)(sidx[q] & 0xffffu);
-                        rank += rs_before(__ldg(row + o), o, xj, j);
+                        const int ido = sid ? sid[o] : o;
+                        rank += rs_before(__ldg(row + ido), ido, xj, idj);
                     }
                     pos = kb + first + rank;
                 }
@@ -997,16 +1013,18 @@ __device__ __forceinline__ void fk_row(const FkRow &R, const float (&fk)[KPT]) {
                     }
                 }
                 if (tie > 1) {
-                    const double xj = __ldg(row + j);
+                    const int idj = sid ? sid[j] : j;
+                    const double xj = __ldg(row + idj);
                     rank = 0;
                     for (int q = s0; q < s1; q++) {
                         const int o = (int)(sidx[q] & 0xffffu);
-                        if (o != j) rank += rs_before(__ldg(row + o), o, xj, j);
+                        const int ido = sid ? sid[o] : o;
+                        if (o != j) rank += rs_before(__ldg(row + ido), ido, xj, idj);
                     }
                 }
                 pos = s0 + rank;
             }
-            out[pos] = j;
+            out[pos] = sid ? sid[j] : j;
         }
     }
 }
@@ -1122,6 +1140,7 @@ row_sort_fk_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restric
         R.sidx = reinterpret_cast<uint32_t *>(buf + pl.off_sidx);
         R.row = row;
         R.out = order + v * (int64_t)m;
+        R.sid = nullptr;
         R.vi = vi;
         R.nsamp = nsamp_all - (((vi / NT) & 3) == 0 ? 1 : 0);
         if (row_odd) fk_row<true, KPT>(R, fk);
@@ -1140,13 +1159,314 @@ row_sort_fk_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restric
 #undef FK_PH
 }
 
+// ---------------------------------------------------------------- long rows (n > FK_NMAX)
+// Two passes per batch of rows, everything heavy in shared memory:
+//  1. row_part_kernel (one CTA per row): float keys, screen sums, a histogram over
+//     SP_C fixed bins of [-1, 1]; bins are grouped into segments of consecutive
+//     bins (bin start position / T, T = SEG_MAX - largest bin + 1, so a segment
+//     holds <= SEG_MAX keys) and every key is scattered as (float key, id) to its
+//     bin's slice of a per-row scratch row -- a segment's keys are exactly the
+//     output positions [P_s, P_s + cnt_s) of the row, in arbitrary order;
+//  2. row_seg_kernel (persistent CTAs pulling (row, segment) items): the
+//     float-key bucket sort of fk_row on the segment (range map from the
+//     segment's own float min/max), ids through a slot -> id table.
+// Rows with NaN / values outside [-1, 1] or one bin above SEG_MAX / 2 are listed
+// and sorted by row_sort_global_kernel afterwards.
+constexpr int SP_C = 4096;
+constexpr int SEG_MAX = 12288;
+constexpr int SEG_KPT = SEG_MAX / FK_T;
+constexpr int SP_MAXSEG = 64;
+constexpr int SP_U = 8;     // loads in flight per thread
+constexpr int SP_PT = 512;  // partition CTA size (2 per SM)   // segments per row: n <= ~390k
+
+struct SegItem {
+    int32_t v, pos0, cnt, pad;
+    int64_t soff;   // scratch offset (float2 entries)
+};
+
+template <int PT>
+__global__ void __launch_bounds__(PT, 1024 / PT)
+row_part_kernel(const double *__restrict__ S, int64_t n64, int64_t v0, int64_t v1, double *__restrict__ screen,
+                float2 *__restrict__ scratch, SegItem *__restrict__ items, int *__restrict__ nitems,
+                int32_t *__restrict__ slow, int *__restrict__ nslow) {
+    __shared__ uint32_t hist[SP_C + 1];
+    __shared__ uint32_t base[SP_C + 1];
+    __shared__ double red[2][32];
+    __shared__ uint32_t wsum[32];
+    __shared__ uint32_t maxbin;
+    __shared__ double diag;
+    __shared__ double seg_lo[SP_MAXSEG], seg_inv[SP_MAXSEG];
+    __shared__ uint8_t segof[SP_C + 1];
+    __shared__ uint32_t segcur[SP_MAXSEG], gcur[SP_MAXSEG], ccnt_s[SP_MAXSEG], coff[SP_MAXSEG];
+    extern __shared__ __align__(16) unsigned char sp_dyn[];   // SP_U * PT * 9 bytes
+    float2 *stage = reinterpret_cast<float2 *>(sp_dyn);
+    uint8_t *stg_seg = sp_dyn + SP_U * PT * sizeof(float2);
+    const int n = (int)n64, m = n - 1;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int W = PT / 32;
+    constexpr float HC = 0.5f * SP_C;
+    for (int64_t v = v0 + blockIdx.x; v < v1; v += gridDim.x) {
+        const double *row = S + v * n64;
+        const int vi = (int)v;
+        for (int c = tid; c <= SP_C; c += PT) hist[c] = 0u;
+        if (tid == 0) maxbin = 0u;
+        __syncthreads();
+        double sm = 0.0, sa = 0.0;
+        bool odd = false;
+        for (int j0 = tid; j0 < n; j0 += SP_U * PT) {
+            double x[SP_U];
+#pragma unroll
+            for (int u = 0; u < SP_U; u++) x[u] = j0 + u * PT < n ? __ldg(row + j0 + u * PT) : 0.0;
+#pragma unroll
+            for (int u = 0; u < SP_U; u++) {
+                const int j = j0 + u * PT;
+                if (j >= n) continue;
+                sm += x[u];
+                sa += fabs(x[u]);
+                if (j == vi) { diag = x[u]; continue; }
+                const float f = __double2float_rn(x[u]);
+                odd |= !(fabsf(f) <= 1.0f);
+                atomicAdd(&hist[fk_coarse<true>(f, HC, HC, SP_C)], 1u);
+            }
+        }
+        for (int o = 16; o; o >>= 1) {
+            sm += __shfl_xor_sync(0xffffffffu, sm, o);
+            sa += __shfl_xor_sync(0xffffffffu, sa, o);
+        }
+        if (lane == 0) { red[0][warp] = sm; red[1][warp] = sa; }
+        const bool row_odd = __syncthreads_or(odd);
+        if (warp == W - 1) {
+            double s1 = lane < W ? red[0][lane] : 0.0, s2 = lane < W ? red[1][lane] : 0.0;
+            for (int o = 16; o; o >>= 1) {
+                s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+                s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+            }
+            if (lane == 0 && screen) {
+                screen[vi] = __dsub_rn(s1, diag);
+                screen[n + vi] = rs_screen_radius_t(n, PT, s2);
+            }
+        }
+        // exclusive scan of the bins (4 per thread) and the largest bin
+        constexpr int BPT = SP_C / PT;   // bins per thread (+ bin SP_C on the last thread)
+        uint32_t h[BPT + 1], s = 0, hm = 0;
+#pragma unroll
+        for (int q = 0; q < BPT; q++) {
+            const int c = tid * BPT + q;
+            h[q] = hist[c];
+            s += h[q];
+            hm = max(hm, h[q]);
+        }
+        h[BPT] = (tid == PT - 1) ? hist[SP_C] : 0u;
+        s += h[BPT];
+        hm = max(hm, h[BPT]);
+        uint32_t incl = s;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        hm = __reduce_max_sync(0xffffffffu, hm);
+        if (lane == 31) wsum[warp] = incl;
+        if (lane == 0) atomicMax(&maxbin, hm);
+        __syncthreads();
+        uint32_t wex = 0;
+        for (int w = 0; w < warp; w++) wex += wsum[w];   // W <= 32 warps
+        uint32_t run = wex + incl - s;
+#pragma unroll
+        for (int q = 0; q < BPT; q++) { base[tid * BPT + q] = run; hist[tid * BPT + q] = run; run += h[q]; }
+        if (tid == PT - 1) { base[SP_C] = run; hist[SP_C] = run; }
+        __syncthreads();
+        const uint32_t mb = maxbin;
+        if (row_odd || mb > (uint32_t)(SEG_MAX / 2)) {
+            if (tid == 0) slow[atomicAdd(nslow, 1)] = vi;
+            __syncthreads();
+            continue;
+        }
+        const uint32_t T = (uint32_t)SEG_MAX - mb + 1u;   // segment s: bins starting in [s T, (s+1) T)
+        // segment s = positions [B_s, B_{s+1}), B_s = the first bin start >= s T (bin boundaries);
+        // bin c belongs to segment base[c] / T.  Its keys are re-expressed relative to the
+        // segment's value window, so float keys keep ~2^-24 of the window's width.
+        const int nseg = (int)(((uint32_t)m + T - 1u) / T);
+        for (int sg = tid; sg < nseg; sg += PT) {
+            auto bound = [&](uint32_t lim) -> int {   // first bin index with start >= lim
+                int lo = 0, hi = SP_C + 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (base[mid] < lim) lo = mid + 1;
+                    else hi = mid;
+                }
+                return lo;
+            };
+            const int cA = sg == 0 ? 0 : bound((uint32_t)sg * T);
+            const int cB = bound((uint32_t)(sg + 1) * T);   // exclusive
+            const uint32_t b0 = cA <= SP_C ? base[cA] : (uint32_t)m;
+            const uint32_t b1 = cB <= SP_C ? base[cB] : (uint32_t)m;
+            // values of bins [cA, cB): f in [1 - (cB - 1/2)/HC, 1 - (cA - 1/2)/HC], padded
+            const double vlo = 1.0 - ((double)cB - 0.5) / (double)HC - 1e-6;
+            const double vhi = 1.0 - ((double)cA - 0.5) / (double)HC + 1e-6;
+            seg_lo[sg] = vlo;
+            seg_inv[sg] = 2.0 / (vhi - vlo);   // key = 2 (x - lo) / (hi - lo) - 1 in (-1, 1)
+            if (b1 <= b0) continue;
+            SegItem it;
+            it.v = vi;
+            it.pos0 = (int32_t)b0;
+            it.cnt = (int32_t)(b1 - b0);
+            it.pad = 0;
+            it.soff = (v - v0) * (int64_t)m + b0;
+            items[atomicAdd(nitems, 1)] = it;
+        }
+        __syncthreads();
+        for (int c = tid; c <= SP_C; c += PT) segof[c] = (uint8_t)(base[c] / T);
+        if (tid < SP_MAXSEG) segcur[tid] = 0u;
+        __syncthreads();
+        if (tid < nseg) {   // scratch cursor of segment tid = its first position
+            int lo = 0, hi = SP_C + 1;
+            const uint32_t lim = (uint32_t)tid * T;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (base[mid] < lim) lo = mid + 1;
+                else hi = mid;
+            }
+            segcur[tid] = tid == 0 ? 0u : (lo <= SP_C ? base[lo] : (uint32_t)m);
+        }
+        // scatter in chunks of SP_U * PT keys: stage by segment in shared memory, then
+        // write each segment's run of the chunk contiguously at its scratch cursor
+        float2 *srow = scratch + (v - v0) * (int64_t)m;
+        for (int j0 = 0; j0 < n; j0 += SP_U * PT) {
+            if (tid < SP_MAXSEG) ccnt_s[tid] = 0u;
+            __syncthreads();
+            double x[SP_U];
+#pragma unroll
+            for (int u = 0; u < SP_U; u++) {
+                const int j = j0 + u * PT + tid;
+                x[u] = j < n ? __ldg(row + j) : 0.0;
+            }
+            int sgs[SP_U];
+            uint32_t loc[SP_U];
+#pragma unroll
+            for (int u = 0; u < SP_U; u++) {
+                const int j = j0 + u * PT + tid;
+                sgs[u] = -1;
+                if (j < n && j != vi) {
+                    const int c = fk_coarse<true>(__double2float_rn(x[u]), HC, HC, SP_C);
+                    sgs[u] = segof[c];
+                    loc[u] = atomicAdd(&ccnt_s[sgs[u]], 1u);
+                }
+            }
+            __syncthreads();
+            if (warp == 0) {   // chunk-local segment offsets + global reservation (nseg <= 64)
+                uint32_t c0 = ccnt_s[lane], c1 = ccnt_s[lane + 32];
+                uint32_t i0 = c0, i1 = c1;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y0 = __shfl_up_sync(0xffffffffu, i0, o);
+                    const uint32_t y1 = __shfl_up_sync(0xffffffffu, i1, o);
+                    if (lane >= o) { i0 += y0; i1 += y1; }
+                }
+                const uint32_t t0 = __shfl_sync(0xffffffffu, i0, 31);
+                coff[lane] = i0 - c0;
+                coff[lane + 32] = t0 + i1 - c1;
+                gcur[lane] = segcur[lane];
+                gcur[lane + 32] = segcur[lane + 32];
+                segcur[lane] += c0;
+                segcur[lane + 32] += c1;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int u = 0; u < SP_U; u++) {
+                if (sgs[u] < 0) continue;
+                const int sg = sgs[u];
+                const int j = j0 + u * PT + tid;
+                const float key = __double2float_rn(__dsub_rn(__dmul_rn(__dsub_rn(x[u], seg_lo[sg]), seg_inv[sg]), 1.0));
+                stage[coff[sg] + loc[u]] = make_float2(key, __int_as_float(j));
+                stg_seg[coff[sg] + loc[u]] = (uint8_t)sg;
+            }
+            __syncthreads();
+            const int tot = (int)(coff[SP_MAXSEG - 1] + ccnt_s[SP_MAXSEG - 1]);
+            for (int q = tid; q < tot; q += PT) {
+                const int sg = stg_seg[q];
+                srow[gcur[sg] + (uint32_t)q - coff[sg]] = stage[q];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(FK_T, 1)
+row_seg_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restrict__ order,
+               const float2 *__restrict__ scratch, const SegItem *__restrict__ items, const int *__restrict__ nitems,
+               int *__restrict__ next_item, FkPlan pl) {
+    extern __shared__ __align__(16) unsigned char fk_smem[];
+    constexpr int NT = FK_T, KPT = SEG_KPT;
+    uint32_t *ccnt = reinterpret_cast<uint32_t *>(fk_smem + pl.off_cinfo);
+    FkMisc &ms = *reinterpret_cast<FkMisc *>(fk_smem + pl.off_misc);
+    uint32_t *f16 = reinterpret_cast<uint32_t *>(fk_smem + pl.off_f16);
+    int32_t *sid = reinterpret_cast<int32_t *>(fk_smem + pl.off_sid);
+    __shared__ int sh_item;
+    const int tid = threadIdx.x;
+    const int nw16 = pl.NBcap / 2 + 2;
+    const int m_row = (int)n64 - 1;
+    for (int c = tid; c <= pl.C; c += NT) ccnt[c] = 0u;
+    FkRow R;
+    R.f16 = f16;
+    R.cinfo = reinterpret_cast<float2 *>(ccnt);
+    R.ccnt = ccnt;
+    R.ms = &ms;
+    R.fkey = reinterpret_cast<float *>(fk_smem);
+    R.sidx = reinterpret_cast<uint32_t *>(fk_smem + pl.off_sidx);
+    R.sid = sid;
+    R.vi = -1;
+    R.fs = pl.fs;
+    const int total = *nitems;
+    for (;;) {
+        __syncthreads();   // the previous item is finished with shared memory
+        if (tid == 0) sh_item = atomicAdd(next_item, 1);
+        __syncthreads();
+        const int k = sh_item;
+        if (k >= total) break;
+        const SegItem it = items[k];
+        const int cnt = it.cnt;
+        int32_t *out = order + (int64_t)it.v * m_row + it.pos0;
+        const float2 *src = scratch + it.soff;
+        if (cnt <= 1) {
+            if (cnt == 1 && tid == 0) out[0] = __float_as_int(src[0].y);
+            continue;
+        }
+        float fk[KPT];
+#pragma unroll
+        for (int e = 0; e < KPT; e++) {
+            const int s = tid + e * NT;
+            fk[e] = 0.0f;
+            if (s < cnt) {
+                const float2 pr = src[s];
+                fk[e] = pr.x;
+                sid[s] = __float_as_int(pr.y);
+            }
+        }
+        const int Ci = rs_coarse_bins(cnt);
+        const float hci = 0.5f * (float)Ci;
+        for (int i = tid; i < nw16; i += NT) f16[i] = 0u;
+        const int ns = (cnt + 3) / 4;   // slots s % 4 == 0 (fk_row samples threads 4k)
+        R.row = S + (int64_t)it.v * n64;
+        R.out = out;
+        R.n = cnt;
+        R.m = cnt;
+        R.C = Ci;
+        R.hc = hci;
+        R.nsamp = ns;
+        __syncthreads();   // sid and the cleared counters are visible
+        // the segment's own float range (fk_row's general path): a fixed map over the
+        // segment window degrades badly when the keys crowd into part of it
+        fk_row<true, KPT>(R, fk);
+    }
+}
+
 // ---------------------------------------------------------------- large rows
 // n > 16384: the same two-level bucket algorithm; the row is read through L2,
 // the per-key (bucket, rank) pairs live in a per-CTA global scratch slice and
 // the output row itself is the scatter buffer.  Counters stay in shared memory.
 __global__ void __launch_bounds__(RS_T, 1)
 row_sort_global_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restrict__ order,
-                       double *__restrict__ screen, uint32_t *__restrict__ gpk_all) {
+                       double *__restrict__ screen, uint32_t *__restrict__ gpk_all, const int32_t *__restrict__ rows,
+                       const int *__restrict__ nrows) {
     const int n = (int)n64;
     const int m = n - 1;
     extern __shared__ __align__(16) unsigned char rs_smem[];
@@ -1155,7 +1475,9 @@ row_sort_global_kernel(const double *__restrict__ S, int64_t n64, int32_t *__res
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int C = rs_coarse_bins(m);
     uint32_t *gpk = gpk_all + (size_t)blockIdx.x * 2 * n;   // [n] bucket, [n] rank/position
-    for (int64_t v = blockIdx.x; v < n; v += gridDim.x) {
+    const int64_t nv = rows ? (int64_t)*nrows : n64;
+    for (int64_t vix = blockIdx.x; vix < nv; vix += gridDim.x) {
+        const int64_t v = rows ? (int64_t)rows[vix] : vix;
         const double *row = S + v * n64;
         int32_t *out = order + v * (int64_t)m;
         for (int c = tid; c <= C; c += RS_T) ms.ccnt[c] = 0;
@@ -1324,7 +1646,7 @@ row_sort_global_kernel(const double *__restrict__ S, int64_t n64, int32_t *__res
 }
 
 constexpr size_t RS_SMEM_MAX = 227 * 1024;
-constexpr int FK_NMAX = 24576;
+constexpr int FK_NMAX = 24576;   // longer rows: row_part_kernel + row_seg_kernel
 
 // numpy's pairwise plan for n (a pure function of n), cached per host thread
 const PwTree<PW_MAXNODES> &pw_host_plan(int n) {
@@ -1340,9 +1662,19 @@ const PwTree<PW_MAXNODES> &pw_host_plan(int n) {
 
 }  // namespace
 
+// long rows: rows per partition batch (scratch = batch x (n-1) float2, <= ~512 MB)
+static int64_t seg_batch_rows(int64_t n) {
+    int64_t b = ((int64_t)512 << 20) / (8 * (n - 1));
+    if (b < tg_num_sms()) b = tg_num_sms();
+    return b < n ? b : n;
+}
+static int64_t seg_items_cap(int64_t n) { return seg_batch_rows(n) * (2 * (n - 1) / SEG_MAX + 3); }
+
 TG_API size_t tg_row_sort_workspace_bytes(int64_t n) {
-    if (n <= 16384) return 256;
-    return (size_t)tg_num_sms() * 2 * (size_t)n * sizeof(uint32_t) + 4096;
+    if (n <= FK_NMAX) return 256;
+    const size_t gk = tg_align_up((size_t)tg_num_sms() * 2 * (size_t)n * sizeof(uint32_t), 256);
+    return gk + tg_align_up((size_t)seg_batch_rows(n) * (size_t)(n - 1) * sizeof(float2), 256) +
+           tg_align_up((size_t)seg_items_cap(n) * sizeof(SegItem), 256) + tg_align_up((size_t)n * 4, 256) + 1024;
 }
 
 TG_API int tg_row_sort_f64(const double *S, int64_t n, int32_t *order, double *screen, void *ws, size_t ws_bytes,
@@ -1402,12 +1734,43 @@ TG_API int tg_row_sort_f64(const double *S, int64_t n, int32_t *order, double *s
         return TG_OK;
     }
     if (ws_bytes < tg_row_sort_workspace_bytes(n)) return TG_ERR_WORKSPACE;
-    uint32_t *gpk = reinterpret_cast<uint32_t *>(ws);
+    if (2 * (n - 1) / SEG_MAX + 2 > SP_MAXSEG) return TG_ERR_ARG;
+    TgArena ar(ws, ws_bytes);
+    uint32_t *gpk = ar.take<uint32_t>((size_t)tg_num_sms() * 2 * (size_t)n);
     int m = (int)n - 1;
     size_t smem = (size_t)(rs_fine_cap(m) + 1) * sizeof(uint32_t);
     if (smem > 160 * 1024) return TG_ERR_ARG;
     TG_CUDA_CHECK(cudaFuncSetAttribute(row_sort_global_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    row_sort_global_kernel<<<grid, RS_T, smem, st>>>(S, n, order, screen, gpk); tg_count_launch(1);
+    if (getenv("TG_SORT_OLD")) {
+        row_sort_global_kernel<<<grid, RS_T, smem, st>>>(S, n, order, screen, gpk, nullptr, nullptr); tg_count_launch(1);
+        TG_LAUNCH_CHECK();
+        return TG_OK;
+    }
+    // partition into segments per batch of rows, sort the segments in shared memory,
+    // then the listed rows (NaN, out of range, one huge bin) with the global kernel
+    const int64_t B = seg_batch_rows(n);
+    float2 *scratch = ar.take<float2>((size_t)B * (size_t)m);
+    SegItem *items = ar.take<SegItem>((size_t)seg_items_cap(n));
+    int32_t *slow = ar.take<int32_t>((size_t)n);
+    int *cnt = ar.take<int>(4);   // nitems, next_item, nslow
+    if (!scratch || !items || !slow || !cnt) return TG_ERR_WORKSPACE;
+    FkPlan sp = fk_plan(SEG_MAX, 1, RS_SMEM_MAX - (size_t)SEG_MAX * 4 - 64, 3.0);
+    sp.off_sid = tg_align_up(sp.smem, 16);
+    const size_t seg_smem = sp.off_sid + (size_t)SEG_MAX * 4;
+    if (sp.smem > RS_SMEM_MAX || seg_smem > RS_SMEM_MAX) return TG_ERR_ARG;
+    TG_CUDA_CHECK(cudaFuncSetAttribute(row_seg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)seg_smem));
+    const size_t part_smem = (size_t)SP_U * SP_PT * 9;
+    TG_CUDA_CHECK(cudaFuncSetAttribute(row_part_kernel<SP_PT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)part_smem));
+    TG_CUDA_CHECK(cudaMemsetAsync(cnt + 2, 0, sizeof(int), st));
+    for (int64_t v0 = 0; v0 < n; v0 += B) {
+        const int64_t v1 = v0 + B < n ? v0 + B : n;
+        TG_CUDA_CHECK(cudaMemsetAsync(cnt, 0, 2 * sizeof(int), st));
+        row_part_kernel<SP_PT><<<2 * grid, SP_PT, part_smem, st>>>(S, n, v0, v1, screen, scratch, items, cnt, slow, cnt + 2);
+        row_seg_kernel<<<grid, FK_T, seg_smem, st>>>(S, n, order, scratch, items, cnt, cnt + 1, sp);
+        tg_count_launch(2);
+    }
+    row_sort_global_kernel<<<grid, RS_T, smem, st>>>(S, n, order, screen, gpk, slow, cnt + 2); tg_count_launch(1);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }

@@ -142,3 +142,43 @@ def test_row_sort_heavy_ties(oracle, pkg):
     S[::2, ::2] = -0.0
     np.fill_diagonal(S, 1.0)
     assert np.array_equal(pkg.sort_neighbor_lists(S).order, oracle.sort_neighbor_lists(S))
+
+
+def _ref_row_order(row: np.ndarray, v: int) -> np.ndarray:
+    """simmatrix.py:238-246 for one row: ids by (value desc, NaN last, id asc), v removed."""
+    o = np.lexsort((np.arange(row.shape[0]), -row))
+    return o[o != v].astype(np.int32)
+
+
+def test_row_sort_long_rows_segments_and_fallback(pkg):
+    """n > 24576: partition into segments + segment sort, and the listed-row fallback
+    (NaN, values outside [-1, 1], one value bin holding most of the row)."""
+    import torch
+    from paper_2408_09399_b200 import simmatrix
+    n = 26000
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn(n, 12, generator=g, device="cuda", dtype=torch.float64)
+    x = x / x.norm(dim=1, keepdim=True)
+    S = x @ x.T
+    S.clamp_(-1.0, 1.0)
+    rng = np.random.default_rng(1)
+    S[3, rng.integers(0, n, 40)] = float("nan")                      # NaN -> fallback
+    S[10] *= 3.0                                                    # out of range -> fallback
+    S[20] = 0.5                                                     # one tie group -> fallback
+    S[30] = torch.round(S[30] * 25) / 25                            # 51 tie groups, segment path
+    S[40] = 0.0
+    S[40, ::3] = -0.0                                               # signed zeros tie
+    S[50] = 0.7 + 1e-9 * torch.rand(n, generator=g, device="cuda", dtype=torch.float64)   # one bin
+    S[60, : n // 2] = 0.9 + 1e-4 * torch.rand(n // 2, generator=g, device="cuda", dtype=torch.float64)
+    S[70] = torch.round(S[70] * 1e6) / 1e6                          # float-equal, double-distinct
+    order, screen = simmatrix.sort_rows_device(S, with_screen=True)
+    torch.cuda.synchronize()
+    rows = [3, 10, 20, 30, 40, 50, 60, 70] + list(rng.choice(n, 60, replace=False))
+    for v in rows:
+        row = S[v].cpu().numpy()
+        got = order[v].cpu().numpy()
+        assert np.array_equal(got, _ref_row_order(row, v)), v
+        if not np.isnan(row).any():
+            exact = np.sum(row) - row[v]
+            scr = screen[v].item(), screen[n + v].item()
+            assert abs(scr[0] - exact) <= scr[1] + 1e-9 * abs(exact)
