@@ -135,6 +135,7 @@ struct TmArgs {
 
     unsigned long long *gvst;  // per-vertex scan state when it does not fit in shared memory
     int check;           // check_invariants mode (tmfg.py:375-399)
+    int prefetch;        // the last helper CTA prefetches S for the queue head into L2
 };
 
 __device__ __forceinline__ bool is_ins(const uint32_t *bits, int v) { return (bits[v >> 5] >> (v & 31)) & 1u; }
@@ -1006,6 +1007,46 @@ __device__ void cluster_helper(const TmArgs &A, const uint32_t *bits_r, unsigned
 #endif
 }
 
+// Prefetcher CTA of the cluster (the last rank when A.prefetch): sweeps the head of the
+// leader's shared-memory queue and, for each face (a, b, c) there, issues L2 prefetches of
+// S[x, u] for x in the face and u in the certified max-corr candidates (mc, mc2) of its
+// vertices -- the 9 (or 18) values the face's next refresh will read (tmfg.py:266-277), so
+// that refresh finds them in L2 instead of HBM.  Reads are racy snapshots and only steer
+// prefetches (every id is range-checked); nothing it does affects results.
+constexpr int TM_PF_DEPTH = 384;   // queue entries swept per pass
+
+template <bool SMEM_ST>
+__device__ void cluster_prefetcher(const TmArgs &A, const Ent *qbuf_r, const int *sel_r, const int *size_r,
+                                   const unsigned long long *vst_r, const int *stop_r) {
+    const int tid = threadIdx.x;
+    const int n = A.n;
+    volatile const int *stop = stop_r;
+    volatile const int *selp = sel_r;
+    volatile const int *sizep = size_r;
+    volatile const unsigned long long *st = SMEM_ST ? vst_r : A.gvst;
+    // 3 threads per entry: thread (i, q) prefetches row x = vertex q of entry i at the 6 candidates
+    const int i = tid / 3, q = tid % 3;
+    while (!*stop) {
+        const int sel = *selp, size = *sizep;
+        if (i < TM_PF_DEPTH && i < size && tid < 3 * TM_PF_DEPTH) {
+            const volatile Ent *e = qbuf_r + (sel ? TM_B : 0) + i;
+            const int a = e->a, b = e->b, c = e->c;
+            if (a >= 0 && a < n && b >= 0 && b < n && c >= 0 && c < n) {
+                const int x = q == 0 ? a : (q == 1 ? b : c);
+                const double *row = A.S + (int64_t)x * n;
+                const int vv[3] = {a, b, c};
+#pragma unroll
+                for (int k = 0; k < 3; k++) {
+                    const VSt r = vst_unpack(st[vv[k]]);
+                    if (r.mc >= 0 && r.mc < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(row + r.mc));
+                    if (r.mc2 >= 0 && r.mc2 < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(row + r.mc2));
+                }
+            }
+        }
+        __nanosleep(200);
+    }
+}
+
 template <bool SMEM_ST>
 __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
     extern __shared__ __align__(16) unsigned char tm_smem[];
@@ -1038,10 +1079,18 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
     const unsigned ncl = cg::this_cluster().num_blocks(), crank = cg::this_cluster().block_rank();
     if (crank != 0) {
         cg::this_cluster().sync();   // the leader has initialised its state
-        cluster_helper<SMEM_ST>(A, cg::this_cluster().map_shared_rank(bits, 0),
-                                cg::this_cluster().map_shared_rank(vst, 0),
-                                cg::this_cluster().map_shared_rank(&ctl.bg_stop, 0), (int)crank - 1,
-                                (int)ncl - 1, tm_smem);
+        const bool pf = A.prefetch && ncl > 2;
+        if (pf && crank == ncl - 1)
+            cluster_prefetcher<SMEM_ST>(A, cg::this_cluster().map_shared_rank(buf0, 0),
+                                        cg::this_cluster().map_shared_rank(&ctl.sel, 0),
+                                        cg::this_cluster().map_shared_rank(&ctl.size, 0),
+                                        cg::this_cluster().map_shared_rank(vst, 0),
+                                        cg::this_cluster().map_shared_rank(&ctl.bg_stop, 0));
+        else
+            cluster_helper<SMEM_ST>(A, cg::this_cluster().map_shared_rank(bits, 0),
+                                    cg::this_cluster().map_shared_rank(vst, 0),
+                                    cg::this_cluster().map_shared_rank(&ctl.bg_stop, 0), (int)crank - 1,
+                                    (int)ncl - 1 - (pf ? 1 : 0), tm_smem);
         cg::this_cluster().sync();   // the leader's shared memory stays alive until here
         return;
     }
@@ -1511,6 +1560,8 @@ TG_API int tg_tmfg_heap(const double *S, const int32_t *order, int64_t n, const 
     if (!A.fv || !A.pool_g || !A.pool_fc || !A.gvst) return TG_ERR_WORKSPACE;
     cudaStream_t st = tg_stream(stream);
     if (n >= (1 << 21)) return TG_ERR_ARG;   // scan-state word packs ids in 21 bits
+    A.prefetch = 1;
+    if (const char *e = std::getenv("TG_TMFG_PREFETCH")) A.prefetch = std::atoi(e);
     const bool smem_st = tm_smem_bytes(n, true) <= 200 * 1024;
     const size_t smem_leader = tm_smem_bytes(n, smem_st);
     // a cluster of 1 leader + helper CTAs (TG_TMFG_CLUSTER, default 8 = portable
@@ -1518,17 +1569,20 @@ TG_API int tg_tmfg_heap(const double *S, const int32_t *order, int64_t n, const 
     int ncl = 8;
     if (const char *e = std::getenv("TG_TMFG_CLUSTER")) ncl = std::atoi(e);
     if (ncl < 1) ncl = 1;
-    if (ncl > 8) ncl = 8;
+    if (ncl > 16) ncl = 16;   // > 8 needs the non-portable cluster size attribute (set below)
     // helpers reuse the dynamic shared memory for a bitmap snapshot + their slice's words
     size_t smem = smem_leader;
     for (; ncl > 1; ncl--) {
-        const size_t hs = (size_t)((((n + 31) / 32) + 1) & ~1LL) * 4 + (size_t)tm_helper_slice((int)n, ncl - 1) * 8 + 64;
+        const int vslots = ncl - 1 - ((A.prefetch && ncl > 2) ? 1 : 0);
+        const size_t hs = (size_t)((((n + 31) / 32) + 1) & ~1LL) * 4 + (size_t)tm_helper_slice((int)n, vslots) * 8 + 64;
         if (hs <= 200 * 1024) { smem = std::max(smem_leader, hs); break; }
     }
 #define TM_LAUNCH(M)                                                                                      \
     do {                                                                                                  \
         TG_CUDA_CHECK(cudaFuncSetAttribute(tmfg_heap_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                            (int)smem));                                                  \
+        if (ncl > 8) cudaFuncSetAttribute(tmfg_heap_kernel<M>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1); \
+        cudaGetLastError();                                                                               \
         cudaLaunchConfig_t cfg = {};                                                                      \
         cudaLaunchAttribute attr[1];                                                                      \
         cfg.blockDim = dim3(TM_T, 1, 1);                                                                  \
