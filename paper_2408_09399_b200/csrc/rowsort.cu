@@ -752,7 +752,7 @@ __host__ FkPlan fk_plan(int64_t n, int nbuf, size_t smem_max, double fs_cap) {
     p.stride = (int)((n + 2) & ~1LL);
     p.off_sidx = tg_align_up((size_t)n * sizeof(float), 16);
     {
-        const int need = (int)((p.off_sidx + (size_t)n * 4 + 15) / 8);
+        const int need = (int)((p.off_sidx + ((size_t)n + 64) * 4 + 15) / 8);   // + sentinel pad
         if (p.stride < need) p.stride = (need + 1) & ~1;
     }
     size_t off = (size_t)nbuf * p.stride * sizeof(double);
@@ -944,11 +944,67 @@ __device__ __forceinline__ void fk_row(const FkRow &R, const float (&fk)[KPT]) {
         if (pk[e] != 0xffffffffu)
             sidx[o16[pk[e] >> 16] + (pk[e] & 0xffffu)] = (pk[e] & 0xffff0000u) | (uint32_t)(tid + e * NT);
     }
+    if (tid < 64) sidx[m + tid] = 0xffff0000u;   // sentinel bucket past the last position (never a real one)
     __syncthreads();   // B7
     // ---- 5: exact rank inside the bucket by sorted position, coalesced id store
     const double *row = R.row;
     int32_t *out = R.out;
     const int32_t *sid = R.sid;
+    if (!ODD) {
+        // Positions kb..kb+31 in the lanes; a bucket's members are a run of lanes.  Runs
+        // inside the window rank by shuffles; a run touching the window edge whose bucket
+        // continues outside (sentinel-padded reads of positions kb-1 / kb+32) walks its
+        // bucket in shared memory.  Float ties go to the doubles.
+        const unsigned le = 0xffffffffu >> (31 - lane), lt = le >> 1;
+        for (int kb = warp * 32; kb < m; kb += NT) {
+            const int k = kb + lane;
+            const uint32_t sk = sidx[k];
+            const uint32_t pv = kb > 0 ? sidx[kb - 1] : 0xfffe0000u;   // uniform address: broadcast
+            const uint32_t nv = sidx[kb + 32];
+            const int fb = (int)(sk >> 16), j = (int)(sk & 0xffffu);
+            const float fj = fkey[j];
+            const int fprev = __shfl_up_sync(0xffffffffu, fb, 1);
+            const int fnext = __shfl_down_sync(0xffffffffu, fb, 1);
+            const unsigned S0 = __ballot_sync(0xffffffffu, fprev != fb) | 1u;
+            const unsigned E0 = __ballot_sync(0xffffffffu, fnext != fb) | 0x80000000u;
+            const int first = 31 - __clz(S0 & le);
+            const int last = __ffs(E0 & ~lt) - 1;
+            const int sz = last - first + 1;
+            const bool cross = (first == 0 && (int)(pv >> 16) == fb) || (last == 31 && (int)(nv >> 16) == fb);
+            const int smax = __reduce_max_sync(0xffffffffu, cross ? 1 : sz);
+            int rank = 0, ties = 0;
+#pragma unroll 1
+            for (int i = 0; i < smax; i++) {
+                const float fo = __shfl_sync(0xffffffffu, fj, first + i);
+                const bool in = i < sz;
+                rank += in & (fo > fj);
+                ties += in & (fo == fj);
+            }
+            int pos = kb + first + rank;
+            if ((cross || ties > 1) && k < m) {   // rare: walk the bucket in shared memory
+                const int s0 = o16[fb], s1 = o16[fb + 1];
+                const int idj = sid ? sid[j] : j;
+                double xj = 0.0;
+                bool have = false;
+                rank = 0;
+                for (int q = s0; q < s1; q++) {
+                    const int o = (int)(sidx[q] & 0xffffu);
+                    if (o == j) continue;
+                    const float fo = fkey[o];
+                    if (fo != fj) {
+                        rank += fo > fj;
+                    } else {   // float tie: the doubles decide, then the id
+                        if (!have) { xj = __ldg(row + idj); have = true; }
+                        const int ido = sid ? sid[o] : o;
+                        rank += rs_before(__ldg(row + ido), ido, xj, idj);
+                    }
+                }
+                pos = s0 + rank;
+            }
+            if (k < m) out[pos] = sid ? sid[j] : j;
+        }
+        return;
+    }
     for (int kb = warp * 32; kb < m; kb += NT) {
         const int k = kb + lane;
         const bool live = k < m;
