@@ -710,8 +710,9 @@ __global__ void oracle_block_kernel(tg_oracle_t o, const int32_t *rows, int64_t 
 // and two barriers.  The value at the chain's second-to-last entry -- needed by
 // the tie rule -- is captured during the scan instead of re-read.
 constexpr int NN_SMEM_MAX = 7168;
-constexpr int NN_CTA_T = 512;
+constexpr int NN_BIG = 2048;   // larger matrices: 1024 threads, 8 row entries in flight per thread
 
+template <int NN_CTA_T, int NN_U>
 __global__ void __launch_bounds__(NN_CTA_T)
 nn_chain_cta_kernel(double *mats, const int64_t *mat_off, const int64_t *sizes, int64_t count,
                     const int64_t *merge_off, int64_t *lefts, int64_t *rights, double *heights,
@@ -728,7 +729,7 @@ nn_chain_cta_kernel(double *mats, const int64_t *mat_off, const int64_t *sizes, 
     uint8_t *s_act = reinterpret_cast<uint8_t *>(s_slot + NN_SMEM_MAX);
     for (int64_t b = blockIdx.x; b < count; b += gridDim.x) {
         const int64_t m64 = sizes[b];
-        if (m64 <= NN_WARP_MAX) continue;
+        if (m64 <= NN_WARP_MAX || (NN_CTA_T == 1024) != (m64 > NN_BIG)) continue;
         const int m = (int)m64;
         double *W = mats + mat_off[b];
         int64_t *L = lefts + merge_off[b], *R = rights + merge_off[b];
@@ -772,15 +773,15 @@ nn_chain_cta_kernel(double *mats, const int64_t *mat_off, const int64_t *sizes, 
             const double *row = W + (int64_t)x * m;
             double bv = INFINITY;
             int bi = INT_MAX;
-            for (int j0 = tid; j0 < m; j0 += 4 * NN_CTA_T) {
-                double rr[4];
+            for (int j0 = tid; j0 < m; j0 += NN_U * NN_CTA_T) {
+                double rr[NN_U];
 #pragma unroll
-                for (int u = 0; u < 4; u++) {   // all loads in flight before any use
+                for (int u = 0; u < NN_U; u++) {   // all loads in flight before any use
                     const int j = j0 + u * NN_CTA_T;
                     rr[u] = j < m ? row[j] : INFINITY;
                 }
 #pragma unroll
-                for (int u = 0; u < 4; u++) {
+                for (int u = 0; u < NN_U; u++) {
                     const int j = j0 + u * NN_CTA_T;
                     if (j < m) {
                         const double r = (act[j] && j != x) ? rr[u] : INFINITY;
@@ -825,16 +826,16 @@ nn_chain_cta_kernel(double *mats, const int64_t *mat_off, const int64_t *sizes, 
                 nm++;
                 double *Wlo = W + (int64_t)lo * m;
                 const double *Whi = W + (int64_t)hi * m;
-                for (int j0 = tid; j0 < m; j0 += 4 * NN_CTA_T) {
-                    double pv[4], qv[4];
+                for (int j0 = tid; j0 < m; j0 += NN_U * NN_CTA_T) {
+                    double pv[NN_U], qv[NN_U];
 #pragma unroll
-                    for (int u = 0; u < 4; u++) {
+                    for (int u = 0; u < NN_U; u++) {
                         const int j = j0 + u * NN_CTA_T;
                         pv[u] = j < m ? Wlo[j] : 0.0;
                         qv[u] = j < m ? Whi[j] : 0.0;
                     }
 #pragma unroll
-                    for (int u = 0; u < 4; u++) {
+                    for (int u = 0; u < NN_U; u++) {
                         const int j = j0 + u * NN_CTA_T;
                         if (j < m) {
                             const double mg = pv[u] > qv[u] ? pv[u] : (qv[u] > pv[u] ? qv[u] : pv[u]);
@@ -1074,10 +1075,17 @@ TG_API int tg_nn_chain_batch(double *mats, const int64_t *mat_off, const int64_t
                                                         active, slot, chain, aux_off); tg_count_launch(1);
     int64_t cblocks = count < (int64_t)tg_num_sms() * 2 ? count : (int64_t)tg_num_sms() * 2;
     const size_t nn_smem = (size_t)NN_SMEM_MAX * 9;
-    TG_CUDA_CHECK(cudaFuncSetAttribute(nn_chain_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nn_smem));
-    nn_chain_cta_kernel<<<(unsigned)cblocks, NN_CTA_T, nn_smem, st>>>(mats, mat_off, sizes, count, merge_off, lefts,
-                                                                      rights, heights, active, slot, chain, aux_off);
-    tg_count_launch(1);
+    // m <= NN_BIG: 512 threads (two CTAs per SM); larger: 1024 threads, one row read in flight
+    TG_CUDA_CHECK(cudaFuncSetAttribute(nn_chain_cta_kernel<512, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)nn_smem));
+    TG_CUDA_CHECK(cudaFuncSetAttribute(nn_chain_cta_kernel<1024, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)nn_smem));
+    nn_chain_cta_kernel<512, 4><<<(unsigned)cblocks, 512, nn_smem, st>>>(mats, mat_off, sizes, count, merge_off, lefts,
+                                                                        rights, heights, active, slot, chain, aux_off);
+    nn_chain_cta_kernel<1024, 8><<<(unsigned)cblocks, 1024, nn_smem, st>>>(mats, mat_off, sizes, count, merge_off,
+                                                                          lefts, rights, heights, active, slot, chain,
+                                                                          aux_off);
+    tg_count_launch(2);
     TG_LAUNCH_CHECK();
     return TG_OK;
 }
