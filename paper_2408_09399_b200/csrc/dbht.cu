@@ -427,19 +427,16 @@ __global__ void hp_fill_kernel(tg_oracle_t o, const int32_t *__restrict__ perm, 
     }
 }
 
-__global__ void __launch_bounds__(GH_T, 2)
+__global__ void __launch_bounds__(GH_T, 3)
 group_max_hub_kernel(tg_oracle_t o, const int32_t *__restrict__ gid, const GmSub *__restrict__ subs,
                      const GmTile *__restrict__ tiles, int64_t ntiles, int Hp, const float *__restrict__ hpf,
                      const double *__restrict__ hpd, unsigned long long *__restrict__ out,
                      const uint64_t *__restrict__ mask) {
-    constexpr int PF = GM_TILE * GH_LD * 4, PD = GM_TILE * GH_LD * 8;
-    __shared__ __align__(16) unsigned char gh_raw[2 * PD];
+    constexpr int PF = GM_TILE * GH_LD * 4;
+    __shared__ __align__(16) unsigned char gh_raw[2 * PF + GM_TILE * GM_TILE * 4];
     float (*Af)[GH_LD] = reinterpret_cast<float (*)[GH_LD]>(gh_raw);     // [64 rows][32 hubs]
     float (*Bf)[GH_LD] = reinterpret_cast<float (*)[GH_LD]>(gh_raw + PF);
     unsigned *lmax = reinterpret_cast<unsigned *>(gh_raw + 2 * PF);      // [64 runs][64 runs]
-    double (*Ad)[GH_LD] = reinterpret_cast<double (*)[GH_LD]>(gh_raw);   // exact pass
-    double (*Bd)[GH_LD] = reinterpret_cast<double (*)[GH_LD]>(gh_raw + PD);
-    static_assert(2 * PF + GM_TILE * GM_TILE * 4 <= 2 * PD, "shared layout");
     __shared__ uint16_t cand[GH_MAXC];
     __shared__ int ncand;
     __shared__ int rg[GM_TILE], cg[GM_TILE], lr[GM_TILE], lc[GM_TILE];
@@ -524,25 +521,17 @@ group_max_hub_kernel(tg_oracle_t o, const int32_t *__restrict__ gid, const GmSub
                 if (acc[r][c] >= thr) cand[atomicAdd(&ncand, 1)] = (uint16_t)((i << 6) | j);
             }
         __syncthreads();
-        // ---- exact fp64 estimate of the candidates (GH_T per pass over the hubs)
+        // ---- exact fp64 estimate of the candidates: one warp per candidate, lanes over the
+        // hubs of the two vertex-major rows (coalesced, L2-resident), then a warp min
         const int nc = ncand;
-        for (int cb = 0; cb < nc; cb += GH_T) {
-            const int k = cb + tid;
-            const int ci = k < nc ? (cand[k] >> 6) : 0, cj = k < nc ? (cand[k] & 63) : 0;
+        for (int k = warp; k < nc; k += GH_T / 32) {
+            const int ci = cand[k] >> 6, cj = cand[k] & 63;
+            const double *ha = hpd + (rbase + ci) * Hp, *hb = hpd + (cbase + cj) * Hp;
             double ex = INFINITY;
-            for (int h0 = 0; h0 < Hp; h0 += GM_HC) {
-                for (int e = tid; e < GM_HC * GM_TILE; e += GH_T) {
-                    const int i = e >> 5, h = e & 31;
-                    Ad[i][h] = i < rows ? hpd[(rbase + i) * Hp + h0 + h] : INFINITY;
-                    Bd[i][h] = i < cols ? hpd[(cbase + i) * Hp + h0 + h] : INFINITY;
-                }
-                __syncthreads();
-                if (k < nc)
-#pragma unroll 8
-                    for (int h = 0; h < GM_HC; h++) ex = fmin(ex, __dadd_rn(Ad[ci][h], Bd[cj][h]));
-                __syncthreads();
-            }
-            if (k < nc) atomicMax(&out[sb.out_off + (int64_t)rg[ci] * sb.m + cg[cj]], tg_dbits(ex));
+#pragma unroll 4
+            for (int h = lane; h < Hp; h += 32) ex = fmin(ex, __dadd_rn(ha[h], hb[h]));
+            for (int o = 16; o; o >>= 1) ex = fmin(ex, __shfl_xor_sync(0xffffffffu, ex, o));
+            if (lane == 0) atomicMax(&out[sb.out_off + (int64_t)rg[ci] * sb.m + cg[cj]], tg_dbits(ex));
         }
         __syncthreads();
     }
