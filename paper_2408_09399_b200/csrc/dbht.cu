@@ -516,7 +516,8 @@ group_max_hub_kernel(tg_oracle_t o, const int32_t *__restrict__ gid, const GmSub
             for (int c = 0; c < 4; c++) {
                 if (!((valid >> (r * 4 + c)) & 1u)) continue;
                 const int i = ty * 4 + r, j = tx * 4 + c;
-                const float lm = __uint_as_float(lmax[lr[i] * GM_TILE + lc[j]]);
+                // (an overflowed lmax' = inf still admits every pair near FLT_MAX)
+                const float lm = fminf(__uint_as_float(lmax[lr[i] * GM_TILE + lc[j]]), 3.4028235e38f);
                 const float thr = __fsub_rn(__fmul_rn(lm, 1.0f - 0x1p-19f), 0x1p-140f);
                 if (acc[r][c] >= thr) cand[atomicAdd(&ncand, 1)] = (uint16_t)((i << 6) | j);
             }

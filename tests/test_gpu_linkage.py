@@ -92,3 +92,38 @@ def test_group_max_batched_subproblems(small_cases, oracle, pkg):
         ref = oracle.cluster_max_matrix(oo, groups)
         off = ~np.eye(m, dtype=bool)
         assert np.array_equal(got[off], ref[off])
+
+
+def test_group_max_hub_screen_adversarial(pkg):
+    """fp32-screened hub group max on hostile hub distances: exact zeros, ties, values that
+    collide in fp32 but not fp64, denormals, values that overflow fp32, +inf -- against a
+    direct fp64 evaluation of max_{u in I, v in J} min_h (hd[h,u] + hd[h,v]) (apsp.py:136-143)."""
+    from paper_2408_09399_b200.apsp import HubOracle
+    rng = np.random.default_rng(11)
+    n, H = 300, 37
+    hd = rng.uniform(0.5, 4.0, size=(H, n))
+    hd[:, :20] = np.round(hd[:, :20], 1)                      # ties
+    hd[:, 20:40] = 1.0 + rng.integers(0, 4, size=(H, 20)) * 2.0 ** -40   # fp32-equal, fp64-distinct
+    hd[:, 40:45] = 0.0                                        # zero distances
+    hd[3, 45:50] = 1e-310                                     # denormals
+    hd[:, 50:55] = 1e39 * rng.uniform(1, 2, size=(H, 5))      # overflow fp32
+    hd[:, 55:58] = np.inf                                     # unreachable
+    nearest = np.zeros(n, dtype=np.int64)
+    o = HubOracle(hubs=np.arange(H, dtype=np.int64), hub_dist=hd, nearest_hub=nearest,
+                  nearest_dist=np.zeros(n), radii=np.zeros(n), near_indptr=np.zeros(n + 1, dtype=np.int64),
+                  near_ids=np.zeros(0, dtype=np.int64), near_dist=np.zeros(0))
+    perm = rng.permutation(n)
+    for sizes in ([300], [10] * 30, [1, 2, 3, 4, 290], [64, 65, 171]):
+        groups, s0 = [], 0
+        for sz in sizes:
+            groups.append(np.sort(perm[s0:s0 + sz]))
+            s0 += sz
+        got = pkg.dbht._cluster_max_matrix(o, groups)
+        m = len(groups)
+        for a in range(m):
+            for b in range(m):
+                if a == b:
+                    continue
+                I, J = groups[a], groups[b]
+                est = (hd[:, I][:, :, None] + hd[:, J][:, None, :]).min(axis=0)
+                assert got[a, b] == est.max(), (sizes, a, b)
