@@ -15,7 +15,7 @@ def pkg():
     return p
 
 
-@pytest.mark.parametrize("m", [2, 3, 5, 17, 48, 49, 64, 130, 400])
+@pytest.mark.parametrize("m", [2, 3, 5, 17, 48, 49, 64, 130, 400, 2049, 2600, 7300])
 def test_nn_chain_matches_oracle(m, oracle, pkg):
     rng = np.random.default_rng(m)
     A = rng.random((m, m))
