@@ -208,6 +208,26 @@ __device__ __forceinline__ unsigned probe_two(const int (&val)[NQ], const bool (
     return best;
 }
 
+// Long-tail cursor probe (16 x 32 ids of one sorted row), kept out of line: its 16
+// loads in flight would otherwise raise the register pressure of every refresh and
+// push the face / candidate ids of the common path into local memory.
+__device__ __noinline__ unsigned tail_probe(const int32_t *row, int c, int m, const uint32_t *bits, int &hit,
+                                            int &hit2, unsigned &o2) {
+    const int lane = threadIdx.x & 31;
+    int val[16];
+#pragma unroll
+    for (int q = 0; q < 16; q++) {
+        const int idx = c + q * 32 + lane;
+        val[q] = idx < m ? __ldg(row + idx) : -1;
+    }
+    bool ok[16];
+#pragma unroll
+    for (int q = 0; q < 16; q++) ok[q] = val[q] >= 0 && !is_ins(bits, val[q]);
+    return probe_two<16>(val, ok, hit, hit2, o2);
+}
+
+__shared__ int g_went[TM_WARPS][9 * TM_EPW];   // warp_entries scratch (per hardware warp)
+
 // One warp builds up to TM_EPW entries: refresh the 3 vertices of each face
 // (first uninserted id of order[w], tmfg.py:169-182) and pick the best of the
 // three candidates (tmfg.py:266-277).  Cursor probes: 4 x 32 ids per vertex in
@@ -220,6 +240,9 @@ __device__ void warp_entries(const TmArgs &A, const uint32_t *bits, unsigned lon
     const int n = A.n, m = n - 1;
     constexpr int NV = 3 * TM_EPW;
     unsigned long long *st = SMEM_ST ? vst : A.gvst;
+    // warp-uniform face vertices / candidates live in a per-warp shared-memory slot across the
+    // (register-hungry) cursor probes instead of spilling to local memory (L2 latency)
+    int *F = g_went[threadIdx.x >> 5];   // [0,NV) vertex, [NV,2NV) mc, [2NV,3NV) mc2
     int vv[NV], cur[NV], found[NV], found2[NV];
     const int nv = 3 * cnt;
     // a vertex whose certified max-corr (or the id after it) is still uninserted needs no scan
@@ -246,31 +269,37 @@ __device__ void warp_entries(const TmArgs &A, const uint32_t *bits, unsigned lon
         }
     }
     const unsigned scanned = pending;
+    if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < NV; q++) { F[q] = vv[q]; F[NV + q] = found[q]; F[2 * NV + q] = found2[q]; }
+    }
+    __syncwarp();
 #if TM_PROFILE
     long long tw0 = clock64();
     if (lane == 0) { atomicAdd(&g_tm_prof[0], (unsigned long long)nv); atomicAdd(&g_tm_prof[1], (unsigned long long)__popc(pending)); }
 #endif
     {
-        int val[NV][4];
-#pragma unroll
-        for (int k = 0; k < NV; k++)
-#pragma unroll
-            for (int q = 0; q < 4; q++) {
-                int idx = cur[k] + q * 32 + lane;
-                val[k][q] = (((pending >> k) & 1u) && idx < m) ? __ldg(A.order + (int64_t)vv[k] * m + idx) : -1;
-            }
+        // one vertex at a time (a refresh rarely has more than one to scan): keeps the
+        // probe's registers small enough that the face / candidate ids are not spilled
 #pragma unroll
         for (int k = 0; k < NV; k++) {
             if ((pending >> k) & 1u) {
+                int val[4];
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    const int idx = cur[k] + q * 32 + lane;
+                    val[q] = idx < m ? __ldg(A.order + (int64_t)F[k] * m + idx) : -1;
+                }
                 bool ok[4];
 #pragma unroll
-                for (int q = 0; q < 4; q++) ok[q] = val[k][q] >= 0 && !is_ins(bits, val[k][q]);
+                for (int q = 0; q < 4; q++) ok[q] = val[q] >= 0 && !is_ins(bits, val[q]);
                 int h1, h2;
                 unsigned o2;
-                const unsigned best = probe_two<4>(val[k], ok, h1, h2, o2);
+                const unsigned best = probe_two<4>(val, ok, h1, h2, o2);
                 if (best < 128u) {
-                    found[k] = h1;
-                    found2[k] = h2;
+                    __syncwarp();
+                    if (lane == 0) { F[NV + k] = h1; F[2 * NV + k] = h2; }
+                    __syncwarp();
                     cur[k] += (int)(h2 >= 0 ? o2 : best);
                     pending &= ~(1u << k);
                 } else {
@@ -280,7 +309,7 @@ __device__ void warp_entries(const TmArgs &A, const uint32_t *bits, unsigned lon
         }
     }
 #if TM_PROFILE
-    long long tw1 = clock64() + (found[0] & 0);
+    long long tw1 = clock64();
 #endif
     while (pending) {
         (*iters)++;
@@ -291,53 +320,43 @@ __device__ void warp_entries(const TmArgs &A, const uint32_t *bits, unsigned lon
         int w = 0, c = 0;
 #pragma unroll
         for (int q = 0; q < NV; q++)
-            if (q == k) { w = vv[q]; c = cur[q]; }
-        int val[16];
-#pragma unroll
-        for (int q = 0; q < 16; q++) {
-            int idx = c + q * 32 + lane;
-            val[q] = idx < m ? __ldg(A.order + (int64_t)w * m + idx) : -1;
-        }
-        bool ok[16];
-#pragma unroll
-        for (int q = 0; q < 16; q++) ok[q] = val[q] >= 0 && !is_ins(bits, val[q]);
+            if (q == k) c = cur[q];
+        w = F[k];
         int hit, hit2;
         unsigned o2;
-        const unsigned best = probe_two<16>(val, ok, hit, hit2, o2);
+        const unsigned best = tail_probe(A.order + (int64_t)w * m, c, m, bits, hit, hit2, o2);
         const int adv = best < 512u ? (int)(hit2 >= 0 ? o2 : best) : 512;
         const int cn = min(c + adv, m);
 #pragma unroll
         for (int q = 0; q < NV; q++)
-            if (q == k) {
-                cur[q] = cn;
-                if (hit >= 0) { found[q] = hit; found2[q] = hit2; }
-            }
+            if (q == k) cur[q] = cn;
+        if (hit >= 0) {
+            __syncwarp();
+            if (lane == 0) { F[NV + k] = hit; F[2 * NV + k] = hit2; }
+            __syncwarp();
+        }
         if (hit >= 0 || cn >= m) pending &= ~(1u << k);
     }
     if (lane == 0) {
         if (mc_out) {
 #pragma unroll
             for (int k = 0; k < NV; k++)
-                if (k < nv) mc_out[k] = found[k];
+                if (k < nv) mc_out[k] = F[NV + k];
         }
 #pragma unroll
         for (int k = 0; k < NV; k++)
-            if ((scanned >> k) & 1u) atomicMax(st + vv[k], vst_pack(found[k], found2[k], min(cur[k], m)));
+            if ((scanned >> k) & 1u) atomicMax(st + F[k], vst_pack(F[NV + k], F[2 * NV + k], min(cur[k], m)));
     }
 #if TM_PROFILE
-    long long tw2 = clock64() + (found[0] & 0);
+    long long tw2 = clock64();
 #endif
     // 9 similarity loads per entry: lane = e*9 + ci*3 + vi loads S[face_vi, cand_ci]
     double sv = 0.0;
     int my_u = -1;
     {
         const int e = lane / 9, r = lane % 9, ci = r / 3, vi = r % 3;
-        int u = -1, w = 0;
-#pragma unroll
-        for (int k = 0; k < NV; k++) {
-            if (k == e * 3 + ci) u = found[k];
-            if (k == e * 3 + vi) w = vv[k];
-        }
+        const int u = e < cnt ? F[NV + e * 3 + ci] : -1;
+        const int w = e < cnt ? F[e * 3 + vi] : 0;
         if (e < cnt && u >= 0) sv = __ldg(A.S + (int64_t)w * n + u);
         my_u = u;
     }
@@ -1048,7 +1067,7 @@ __device__ void cluster_prefetcher(const TmArgs &A, const Ent *qbuf_r, const int
 }
 
 template <bool SMEM_ST>
-__global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
+__global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constant__ TmArgs A) {
     extern __shared__ __align__(16) unsigned char tm_smem[];
     const int n = A.n;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1224,9 +1243,9 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
                     }
                 }
                 if (cnt) {
-                    int mcs[3 * TM_EPW];
                     warp_entries<SMEM_ST>(A, bits, vst, cnt, fvv, fids, Lout[warp - TM_NEW_WARPS], my_iters,
-                                                        mcs);
+                                          nullptr);
+                    const int *mcs = &g_went[threadIdx.x >> 5][3 * TM_EPW];   // the refreshed max-corrs
                     if (lane == 0)
                         for (int q = 0; q < cnt; q++) {
                             Lref[idx[q]] = Lout[warp - TM_NEW_WARPS][q];
@@ -1299,9 +1318,10 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(TmArgs A) {
                     if (__shfl_sync(0xffffffffu, need, 0)) {
                         int fids[1] = {h.fid};
                         int fvv[1][3] = {{h.a, h.b, h.c}};
-                        int mcs[3], its[4] = {0, 0, 0, 0};
+                        int its[4] = {0, 0, 0, 0};
                         Ent *o = &Lout[warp - TM_MERGE_WARPS][0];
-                        warp_entries<SMEM_ST>(A, bits, vst, 1, fvv, fids, o, its, mcs);
+                        warp_entries<SMEM_ST>(A, bits, vst, 1, fvv, fids, o, its, nullptr);
+                        const int *mcs = &g_went[threadIdx.x >> 5][3 * TM_EPW];
                         if (lane == 0) {
                             const int slot = h.fid & (TM_RC - 1);
                             if (atomicExch(&rc_claim[slot], round) != round) {
