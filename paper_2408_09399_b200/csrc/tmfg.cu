@@ -373,20 +373,18 @@ __device__ void warp_entries(const TmArgs &A, const uint32_t *bits, unsigned lon
     const int u1 = __shfl_down_sync(0xffffffffu, my_u, 3), u2 = __shfl_down_sync(0xffffffffu, my_u, 6);
     if (lane % 9 == 0 && lane / 9 < cnt) {
         const int e = lane / 9;
-        double best_g = -INFINITY;
+        double best_g = -INFINITY;   // candidates in (mc[a], mc[b], mc[c]) order (tmfg.py:272-276)
         int best_v = -1;
-        const double gs[3] = {g, g1, g2};
-        const int us[3] = {my_u, u1, u2};
-#pragma unroll
-        for (int ci = 0; ci < 3; ci++)
-            if (gs[ci] > best_g || (gs[ci] == best_g && us[ci] < best_v)) { best_g = gs[ci]; best_v = us[ci]; }
+        if (g > best_g || (g == best_g && my_u < best_v)) { best_g = g; best_v = my_u; }
+        if (g1 > best_g || (g1 == best_g && u1 < best_v)) { best_g = g1; best_v = u1; }
+        if (g2 > best_g || (g2 == best_g && u2 < best_v)) { best_g = g2; best_v = u2; }
         Ent x;
         x.g = best_g;
-        x.fid = fids[e];
+        x.fid = TM_EPW == 1 ? fids[0] : fids[e];   // constant index: the caller's array stays in registers
         x.cand = best_v;
-        x.a = fverts[e][0];
-        x.b = fverts[e][1];
-        x.c = fverts[e][2];
+        x.a = F[e * 3 + 0];
+        x.b = F[e * 3 + 1];
+        x.c = F[e * 3 + 2];
         x.opt = 0;
         out[e] = x;
     }
@@ -1176,11 +1174,18 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
     // foreground numbering: warp 31 is foreground warp 0 (replay, insertion, leader)
     const int warp = (TM_WARPS - 1) - (threadIdx.x >> 5);
     const int tid = warp * 32 + lane;
-    long long tc0 = clock64(), tc1;
+#if TM_PROFILE
+    long long tc0 = clock64(), tc1;   // round-level phase clocks (profile build only)
+#endif
     int sel = 0;   // which half of the queue buffer is current (tracked by every foreground thread)
     while (!ctl.done) {
         const int Lc_round = ctl.L_count, size_round = ctl.size;   // stable until the merge
-        if (tid == 0) { tc0 = clock64(); ctl.rounds++; }
+        if (tid == 0) {
+#if TM_PROFILE
+            tc0 = clock64();
+#endif
+            ctl.rounds++;
+        }
         // ================= parallel phase: new-face entries + speculative refresh of the top-K
         int my_iters[4] = {0, 0, 0, 0};
 #if TM_PROFILE
@@ -1266,12 +1271,16 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
             atomicMax(&ctl.ph[0], tw);
         }
 #endif
+#if TM_PROFILE
         tc1 = fg_sync_clock();
-        // ================= replay the pops (warp 0, exact sequential semantics)
         if (tid == 0) {
             ctl.t_par += tc1 - tc0;
             tc0 = tc1;
         }
+#else
+        fg_sync();
+#endif
+        // ================= replay the pops (warp 0, exact sequential semantics)
         // Warps 0..TM_MERGE_WARPS-1 replay, publish and merge (named barrier 2 between
         // replay and merge); the other foreground warps meanwhile refresh the queue
         // entries just past the window (the likely stale head of the next round) into
@@ -1343,6 +1352,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
         }
         if (warp < TM_MERGE_WARPS) {
         asm volatile("bar.sync 2, %0;" ::"r"(TM_MERGE_WARPS * 32) : "memory");
+#if TM_PROFILE
         tc1 = clock64();
         if (tid == 0) {
             ctl.t_replay += tc1 - tc0;
@@ -1352,6 +1362,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
             ctl.it_round_max = 0;
             for (int q = 0; q < 4; q++) { ctl.phs[q] += ctl.ph[q]; ctl.ph[q] = 0; }
         }
+#endif
         // ================= merge buffer[removed..size) + tobuf -> other half (warps 1..),
         // while thread 0 inserts the winner and settles the queue size: both only
         // depend on the replay's results, so one barrier closes the round
@@ -1443,15 +1454,24 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
         }
         }
         sel ^= 1;
+#if TM_PROFILE
         tc1 = fg_sync_clock();
         if (tid == 0) { ctl.t_merge += tc1 - tc0; tc0 = tc1; }
+#else
+        fg_sync();
+#endif
         if (ctl.done) break;
         // ================= refill the shared buffer from the pool when short
         if (ctl.need_refill) {
             refill<TM_FG_T>(A, ctl, sel ? buf1 : buf0, sel ? buf0 : buf1, red_e, red_ok, tid);
             if (tid == 0) ctl.L_count = min(TM_K, ctl.size);
+#if TM_PROFILE
             tc1 = fg_sync_clock();
-            if (tid == 0) { ctl.t_refill += tc1 - tc0; ctl.refills++; tc0 = tc1; }
+            if (tid == 0) { ctl.t_refill += tc1 - tc0; tc0 = tc1; }
+#else
+            fg_sync();
+#endif
+            if (tid == 0) ctl.refills++;
         }
     }
     fg_sync();
