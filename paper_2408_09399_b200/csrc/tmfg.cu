@@ -1368,6 +1368,8 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
         // depend on the replay's results, so one barrier closes the round
         {
             const int r = ctl.removed, sz = ctl.size, nb = ctl.nbuf_new;
+            // thread 0 rewrites ctl.size / sel / L_count below: every merge warp has its copy first
+            asm volatile("bar.sync 2, %0;" ::"r"(TM_MERGE_WARPS * 32) : "memory");
             if (warp > 0) {
                 Ent *cur = sel ? buf1 : buf0;
                 Ent *nxt = sel ? buf0 : buf1;

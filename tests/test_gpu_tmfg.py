@@ -109,3 +109,18 @@ def test_tmfg_matches_oracle_larger(config, n, oracle, pkg):
     assert np.array_equal(np.asarray(g.edges), ref["edges"])
     assert np.array_equal(np.asarray(g.faces), ref["faces"])
     assert g._raw_stats == {k: int(v) for k, v in ref["stats"].items()}
+
+
+def test_tmfg_repeatable_against_oracle(oracle, pkg):
+    """The persistent TMFG kernel is timing-sensitive (cluster helpers, L2 prefetcher, warps
+    racing through a round): repeated runs on one S must all give the oracle's trace."""
+    from paper_2408_09399_b200 import simmatrix, synth, tmfg
+    x, _ = synth.generate(3, n=10000)
+    Sd = simmatrix.pearson_similarity_refexact_device(x)
+    S = Sd.cpu().numpy()
+    ref = oracle.build_tmfg_heap(S, oracle.sort_neighbor_lists(S))
+    order, scr = simmatrix.sort_rows_device(Sd)
+    clique = tmfg.initial_clique_device(Sd, scr)
+    for rep in range(12):
+        out = tmfg.build_tmfg_heap_device(Sd, order, clique)
+        assert np.array_equal(out["trace"].cpu().numpy(), ref["trace"]), rep
