@@ -226,7 +226,7 @@ __device__ __noinline__ unsigned tail_probe(const int32_t *row, int c, int m, co
     return probe_two<16>(val, ok, hit, hit2, o2);
 }
 
-__shared__ int g_went[TM_WARPS][9 * TM_EPW];   // warp_entries scratch (per hardware warp)
+__shared__ int g_went[TM_WARPS][10 * TM_EPW];   // warp_entries scratch (per hardware warp)
 
 // One warp builds up to TM_EPW entries: refresh the 3 vertices of each face
 // (first uninserted id of order[w], tmfg.py:169-182) and pick the best of the
@@ -242,7 +242,7 @@ __device__ void warp_entries(const TmArgs &A, const uint32_t *bits, unsigned lon
     unsigned long long *st = SMEM_ST ? vst : A.gvst;
     // warp-uniform face vertices / candidates live in a per-warp shared-memory slot across the
     // (register-hungry) cursor probes instead of spilling to local memory (L2 latency)
-    int *F = g_went[threadIdx.x >> 5];   // [0,NV) vertex, [NV,2NV) mc, [2NV,3NV) mc2
+    int *F = g_went[threadIdx.x >> 5];   // [0,NV) vertex, [NV,2NV) mc, [2NV,3NV) mc2, [3NV,..) fid
     int vv[NV], cur[NV], found[NV], found2[NV];
     const int nv = 3 * cnt;
     // a vertex whose certified max-corr (or the id after it) is still uninserted needs no scan
@@ -272,6 +272,8 @@ __device__ void warp_entries(const TmArgs &A, const uint32_t *bits, unsigned lon
     if (lane == 0) {
 #pragma unroll
         for (int q = 0; q < NV; q++) { F[q] = vv[q]; F[NV + q] = found[q]; F[2 * NV + q] = found2[q]; }
+#pragma unroll
+        for (int q = 0; q < TM_EPW; q++) F[3 * NV + q] = q < cnt ? fids[q] : -1;
     }
     __syncwarp();
 #if TM_PROFILE
@@ -380,7 +382,7 @@ __device__ void warp_entries(const TmArgs &A, const uint32_t *bits, unsigned lon
         if (g2 > best_g || (g2 == best_g && u2 < best_v)) { best_g = g2; best_v = u2; }
         Ent x;
         x.g = best_g;
-        x.fid = TM_EPW == 1 ? fids[0] : fids[e];   // constant index: the caller's array stays in registers
+        x.fid = F[3 * NV + e];
         x.cand = best_v;
         x.a = F[e * 3 + 0];
         x.b = F[e * 3 + 1];
@@ -1238,11 +1240,14 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
                         }
                         hit = __shfl_sync(0xffffffffu, hit, 0);
                         if (stale && !hit) {
-                            idx[cnt] = i;
-                            fids[cnt] = h.fid;
-                            fvv[cnt][0] = h.a;
-                            fvv[cnt][1] = h.b;
-                            fvv[cnt][2] = h.c;
+                            // constant slot when one entry per warp: a cnt-indexed write would
+                            // put these arrays in local memory
+                            const int sl = TM_EPW == 1 ? 0 : cnt;
+                            idx[sl] = i;
+                            fids[sl] = h.fid;
+                            fvv[sl][0] = h.a;
+                            fvv[sl][1] = h.b;
+                            fvv[sl][2] = h.c;
                             cnt++;
                         }
                     }
