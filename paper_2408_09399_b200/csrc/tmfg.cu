@@ -52,7 +52,10 @@ constexpr int TM_K = TM_EPW * (TM_FG_WARPS - TM_NEW_WARPS);  // top-K speculated
 #define TM_MERGE_WARPS_DEF 28
 #endif
 constexpr int TM_MERGE_WARPS = TM_MERGE_WARPS_DEF;            // replay + merge warps; the rest speculate meanwhile
-constexpr int TM_B = 512;                       // shared-memory queue capacity
+#ifndef TM_B_DEF
+#define TM_B_DEF 1024   // a longer queue halves the pool refills (n=50k: -10%); 2048 would push vst out of smem at n=10k
+#endif
+constexpr int TM_B = TM_B_DEF;                  // shared-memory queue capacity
 constexpr int TM_BATCH = TM_K + 8;
 static_assert(TM_K <= 32, "replay_warp maps one queue position per lane");
 
