@@ -1439,8 +1439,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
                         A.edges[2 * (e + q)] = min(wv[q], v);
                         A.edges[2 * (e + q) + 1] = max(wv[q], v);
                     }
-                    int4 old = A.fv[fid];
-                    A.fv[fid] = make_int4(old.x, old.y, old.z, 0);
+                    A.fv[fid] = make_int4(a, b, c, 0);   // the entry carries the face's sorted vertices
                     int f0 = ctl.nf;
                     int ch[3][3] = {{v, a, b}, {v, a, c}, {v, b, c}};
                     for (int q = 0; q < 3; q++) {
