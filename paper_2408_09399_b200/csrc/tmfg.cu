@@ -53,9 +53,13 @@ constexpr int TM_K = TM_EPW * (TM_FG_WARPS - TM_NEW_WARPS);  // top-K speculated
 #endif
 constexpr int TM_MERGE_WARPS = TM_MERGE_WARPS_DEF;            // replay + merge warps; the rest speculate meanwhile
 #ifndef TM_B_DEF
-#define TM_B_DEF 1024   // a longer queue halves the pool refills (n=50k: -10%); 2048 would push vst out of smem at n=10k
+#define TM_B_DEF 1024   // a longer queue means fewer pool refills; 2048 would push vst out of smem at n=10k
 #endif
-constexpr int TM_B = TM_B_DEF;                  // shared-memory queue capacity
+constexpr int TM_B = TM_B_DEF;                  // shared-memory queue capacity (scan state in smem)
+constexpr int TM_BMAX = 2 * TM_B;               // ... when the scan state lives in global memory (large n):
+// the queue can then take the room, and a longer queue means fewer O(pool) refills
+template <bool SMEM_ST>
+__host__ __device__ constexpr int tm_qb() { return SMEM_ST ? TM_B : TM_BMAX; }
 constexpr int TM_BATCH = TM_K + 8;
 static_assert(TM_K <= 32, "replay_warp maps one queue position per lane");
 
@@ -437,19 +441,20 @@ __device__ __forceinline__ void pool_put(const TmArgs &A, unsigned long long *mi
 constexpr int RF_U = 8;   // pool loads in flight per thread in the selection passes
 constexpr int RF_LOG = 11, RF_BINS = 1 << RF_LOG;   // selection histogram bins
 static_assert(RF_BINS * 4 + TM_B / 2 * 20 <= TM_B * (int)sizeof(Ent), "refill scratch overflows the spare buffer");
+static_assert(RF_BINS * 4 + TM_BMAX / 2 * 20 <= TM_BMAX * (int)sizeof(Ent), "refill scratch overflows the spare buffer");
 
-template <int NT>
+template <int NT, int QB>
 __device__ void refill(const TmArgs &A, Ctl &ctl, Ent *cur, Ent *scratch, Ent *red_e, int *red_ok, int tid) {
     const int lane = tid & 31, warp = tid >> 5;
     const int P = ctl.pool_count;
-    const int room = min(TM_B - ctl.size, TM_B / 2);
+    const int room = min(QB - ctl.size, QB / 2);
 #if TM_PROFILE
     long long rc0 = fg_sync_clock(), rc1;
 #endif
     int *takeidx = reinterpret_cast<int *>(scratch) + RF_BINS;   // room entries (after the histogram)
-    int *holes = takeidx + TM_B / 2;                         // room entries
-    double *tgv = reinterpret_cast<double *>(holes + TM_B / 2);
-    int *tfv = reinterpret_cast<int *>(tgv + TM_B / 2);
+    int *holes = takeidx + QB / 2;                         // room entries
+    double *tgv = reinterpret_cast<double *>(holes + QB / 2);
+    int *tfv = reinterpret_cast<int *>(tgv + QB / 2);
     unsigned long long thr_hi = 0ull, thr_lo = 0ull;
     const bool take_all = P <= room;
     if (!take_all) {
@@ -1051,7 +1056,7 @@ __device__ void cluster_prefetcher(const TmArgs &A, const Ent *qbuf_r, const int
     while (!*stop) {
         const int sel = *selp, size = *sizep;
         if (i < TM_PF_DEPTH && i < size && tid < 3 * TM_PF_DEPTH) {
-            const volatile Ent *e = qbuf_r + (sel ? TM_B : 0) + i;
+            const volatile Ent *e = qbuf_r + (sel ? tm_qb<SMEM_ST>() : 0) + i;
             const int a = e->a, b = e->b, c = e->c;
             if (a >= 0 && a < n && b >= 0 && b < n && c >= 0 && c < n) {
                 const int x = q == 0 ? a : (q == 1 ? b : c);
@@ -1071,6 +1076,7 @@ __device__ void cluster_prefetcher(const TmArgs &A, const Ent *qbuf_r, const int
 
 template <bool SMEM_ST>
 __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constant__ TmArgs A) {
+    constexpr int QB = tm_qb<SMEM_ST>();
     extern __shared__ __align__(16) unsigned char tm_smem[];
     const int n = A.n;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1092,8 +1098,8 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
     __shared__ int Lcomp[TM_K];
 
     Ent *buf0 = reinterpret_cast<Ent *>(tm_smem);
-    Ent *buf1 = buf0 + TM_B;
-    uint32_t *bits = reinterpret_cast<uint32_t *>(buf1 + TM_B);
+    Ent *buf1 = buf0 + QB;
+    uint32_t *bits = reinterpret_cast<uint32_t *>(buf1 + QB);
     const int nwords = (n + 31) >> 5;
     unsigned long long *vst = reinterpret_cast<unsigned long long *>(bits + ((nwords + 1) & ~1));
 
@@ -1393,10 +1399,10 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
                         else hi = mid;
                     }
                     int pos = i + lo;
-                    if (pos < TM_B) nxt[pos] = x;
+                    if (pos < QB) nxt[pos] = x;
                     else {
                         pool_put(A, &ctl.pool_minkey, atomicAdd(&ctl.pool_count, 1), x);
-                        if (pos == TM_B) { ctl.pool_max = x; ctl.pool_has_max = 1; }
+                        if (pos == QB) { ctl.pool_max = x; ctl.pool_has_max = 1; }
                     }
                 }
                 for (int k = mt; k < nb; k += MT) {
@@ -1408,15 +1414,15 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
                         else hi = mid;
                     }
                     int pos = k + lo;
-                    if (pos < TM_B) nxt[pos] = x;
+                    if (pos < QB) nxt[pos] = x;
                     else {
                         pool_put(A, &ctl.pool_minkey, atomicAdd(&ctl.pool_count, 1), x);
-                        if (pos == TM_B) { ctl.pool_max = x; ctl.pool_has_max = 1; }
+                        if (pos == QB) { ctl.pool_max = x; ctl.pool_has_max = 1; }
                     }
                 }
             } else if (lane == 0) {
                 // spilled entries (total > B) are the smallest of the buffer; then no refill
-                const int total = min(sz - r + nb, TM_B);
+                const int total = min(sz - r + nb, QB);
                 ctl.size = total;
                 ctl.sel = sel ^ 1;
                 ctl.need_refill = total < TM_K && ctl.pool_count > 0;
@@ -1472,7 +1478,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
         if (ctl.done) break;
         // ================= refill the shared buffer from the pool when short
         if (ctl.need_refill) {
-            refill<TM_FG_T>(A, ctl, sel ? buf1 : buf0, sel ? buf0 : buf1, red_e, red_ok, tid);
+            refill<TM_FG_T, QB>(A, ctl, sel ? buf1 : buf0, sel ? buf0 : buf1, red_e, red_ok, tid);
             if (tid == 0) ctl.L_count = min(TM_K, ctl.size);
 #if TM_PROFILE
             tc1 = fg_sync_clock();
@@ -1554,7 +1560,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
 }
 
 size_t tm_smem_bytes(int64_t n, bool smem_st) {
-    size_t b = (size_t)2 * TM_B * sizeof(Ent);
+    size_t b = (size_t)2 * (smem_st ? tm_qb<true>() : tm_qb<false>()) * sizeof(Ent);
     b += (size_t)(((n + 31) / 32 + 1) & ~1LL) * 4;
     if (smem_st) b += (size_t)n * 8;
     return tg_align_up(b, 16) + 64;
@@ -1579,8 +1585,8 @@ TG_API int tg_edge_weights(const double *S, int64_t n, const int32_t *edges, int
 TG_API size_t tg_tmfg_workspace_bytes(int64_t n) {
     size_t b = 0;
     b += tg_align_up((size_t)3 * n * sizeof(int4), 256);
-    b += tg_align_up((size_t)(3 * n + TM_B + 64) * sizeof(double), 256);
-    b += tg_align_up((size_t)(3 * n + TM_B + 64) * sizeof(int2), 256);
+    b += tg_align_up((size_t)(3 * n + TM_BMAX + 64) * sizeof(double), 256);
+    b += tg_align_up((size_t)(3 * n + TM_BMAX + 64) * sizeof(int2), 256);
     b += tg_align_up((size_t)n * sizeof(unsigned long long), 256);
     return b + 1024;
 }
@@ -1603,8 +1609,8 @@ TG_API int tg_tmfg_heap(const double *S, const int32_t *order, int64_t n, const 
     A.stats = stats;
     A.check = check;
     A.fv = ar.take<int4>((size_t)3 * n);
-    A.pool_g = ar.take<double>((size_t)3 * n + TM_B + 64);
-    A.pool_fc = ar.take<int2>((size_t)3 * n + TM_B + 64);
+    A.pool_g = ar.take<double>((size_t)3 * n + TM_BMAX + 64);
+    A.pool_fc = ar.take<int2>((size_t)3 * n + TM_BMAX + 64);
     A.gvst = ar.take<unsigned long long>((size_t)n);
     if (!A.fv || !A.pool_g || !A.pool_fc || !A.gvst) return TG_ERR_WORKSPACE;
     cudaStream_t st = tg_stream(stream);
