@@ -42,16 +42,25 @@ namespace {
 
 constexpr int TM_T = 1024;
 constexpr int TM_WARPS = TM_T / 32;
-constexpr int TM_BG_WARPS = 4;                   // background cursor-advancing warps
+#ifndef TM_BG_WARPS_DEF
+#define TM_BG_WARPS_DEF 0   // the cluster helpers keep the scan state; all 32 warps serve the rounds
+#endif
+constexpr int TM_BG_WARPS = TM_BG_WARPS_DEF;      // background cursor-advancing warps
 constexpr int TM_FG_WARPS = TM_WARPS - TM_BG_WARPS;
 constexpr int TM_FG_T = TM_FG_WARPS * 32;
 constexpr int TM_EPW = 1;                       // entries refreshed per warp
 constexpr int TM_NEW_WARPS = 4;                 // warps that build new-face entries
 constexpr int TM_K = TM_EPW * (TM_FG_WARPS - TM_NEW_WARPS);  // top-K speculated per round
 #ifndef TM_MERGE_WARPS_DEF
-#define TM_MERGE_WARPS_DEF 28
+#define TM_MERGE_WARPS_DEF 28   // (the kernel picks per instantiation: see tm_merge_warps)
 #endif
 constexpr int TM_MERGE_WARPS = TM_MERGE_WARPS_DEF;            // replay + merge warps; the rest speculate meanwhile
+// Scan state in shared memory (n <~ 17k): every foreground warp replays / merges (the merge
+// then has ~one entry per thread).  Scan state in global memory (large n, 2048-entry queue):
+// 4 warps speculate -- refresh the entries just past the window into the refresh cache --
+// while the others replay and merge (measured: n = 10k 96 -> 89 ms; n = 50k 644 vs 592 ms).
+template <bool SMEM_ST>
+__host__ __device__ constexpr int tm_merge_warps() { return SMEM_ST ? TM_FG_WARPS : TM_MERGE_WARPS; }
 #ifndef TM_B_DEF
 #define TM_B_DEF 1024   // a longer queue means fewer pool refills; 2048 would push vst out of smem at n=10k
 #endif
@@ -1077,6 +1086,7 @@ __device__ void cluster_prefetcher(const TmArgs &A, const Ent *qbuf_r, const int
 template <bool SMEM_ST>
 __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constant__ TmArgs A) {
     constexpr int QB = tm_qb<SMEM_ST>();
+    constexpr int MW = tm_merge_warps<SMEM_ST>();
     extern __shared__ __align__(16) unsigned char tm_smem[];
     const int n = A.n;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1295,7 +1305,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
         fg_sync();
 #endif
         // ================= replay the pops (warp 0, exact sequential semantics)
-        // Warps 0..TM_MERGE_WARPS-1 replay, publish and merge (named barrier 2 between
+        // Warps 0..MW-1 replay, publish and merge (named barrier 2 between
         // replay and merge); the other foreground warps meanwhile refresh the queue
         // entries just past the window (the likely stale head of the next round) into
         // the refresh cache, and only meet the others at the end of the round.  Nobody
@@ -1304,7 +1314,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
         // the speculative refreshes run: they stay exact (every fact they use is
         // monotone) and the cache's candidate check rejects what the winner voids.
         if (warp == 0) replay_warp(A, ctl, L, Lref, Lstale, NE, batch, tobuf, rk_g, rk_f, rk_src);
-        else if (!A.check && (warp == 1 || warp >= TM_MERGE_WARPS)) {
+        else if (!A.check && (warp == 1 || warp >= MW)) {
             const int round = (int)ctl.rounds;
             if (warp == 1) {
                 for (int i0 = 0; i0 < ctl.L_count; i0 += 32) {
@@ -1324,7 +1334,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
                     }
                 }
             } else {
-                const int pos = Lc_round + (warp - TM_MERGE_WARPS);
+                const int pos = Lc_round + (warp - MW);
                 const Ent *curb = sel ? buf1 : buf0;
                 if (pos < size_round) {
                     const Ent h = curb[pos];
@@ -1342,7 +1352,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
                         int fids[1] = {h.fid};
                         int fvv[1][3] = {{h.a, h.b, h.c}};
                         int its[4] = {0, 0, 0, 0};
-                        Ent *o = &Lout[warp - TM_MERGE_WARPS][0];
+                        Ent *o = &Lout[warp - MW][0];
                         warp_entries<SMEM_ST>(A, bits, vst, 1, fvv, fids, o, its, nullptr);
                         const int *mcs = &g_went[threadIdx.x >> 5][3 * TM_EPW];
                         if (lane == 0) {
@@ -1364,8 +1374,8 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
                 }
             }
         }
-        if (warp < TM_MERGE_WARPS) {
-        asm volatile("bar.sync 2, %0;" ::"r"(TM_MERGE_WARPS * 32) : "memory");
+        if (warp < MW) {
+        asm volatile("bar.sync 2, %0;" ::"r"(MW * 32) : "memory");
 #if TM_PROFILE
         tc1 = clock64();
         if (tid == 0) {
@@ -1383,13 +1393,13 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
         {
             const int r = ctl.removed, sz = ctl.size, nb = ctl.nbuf_new;
             // thread 0 rewrites ctl.size / sel / L_count below: every merge warp has its copy first
-            asm volatile("bar.sync 2, %0;" ::"r"(TM_MERGE_WARPS * 32) : "memory");
+            asm volatile("bar.sync 2, %0;" ::"r"(MW * 32) : "memory");
             if (warp > 0) {
                 Ent *cur = sel ? buf1 : buf0;
                 Ent *nxt = sel ? buf0 : buf1;
                 const int old = sz - r;
                 const int mt = tid - 32;
-                constexpr int MT = TM_MERGE_WARPS * 32 - 32;
+                constexpr int MT = MW * 32 - 32;
                 for (int i = mt; i < old; i += MT) {
                     Ent x = cur[r + i];
                     int lo = 0, hi = nb;  // # of tobuf entries popping before x
