@@ -701,6 +701,11 @@ __global__ void oracle_block_kernel(tg_oracle_t o, const int32_t *rows, int64_t 
 // the tie rule -- is captured during the scan instead of re-read.
 constexpr int NN_SMEM_MAX = 7168;
 constexpr int NN_BIG = 2048;   // larger matrices: 1024 threads, 8 row entries in flight per thread
+#ifndef NN_SMALL_T_DEF
+#define NN_SMALL_T_DEF 512
+#define NN_SMALL_U_DEF 4
+#endif
+constexpr int NN_SMALL_T = NN_SMALL_T_DEF, NN_SMALL_U = NN_SMALL_U_DEF;
 
 template <int NN_CTA_T, int NN_U>
 __global__ void __launch_bounds__(NN_CTA_T)
@@ -1066,11 +1071,11 @@ TG_API int tg_nn_chain_batch(double *mats, const int64_t *mat_off, const int64_t
     int64_t cblocks = count < (int64_t)tg_num_sms() * 2 ? count : (int64_t)tg_num_sms() * 2;
     const size_t nn_smem = (size_t)NN_SMEM_MAX * 9;
     // m <= NN_BIG: 512 threads (two CTAs per SM); larger: 1024 threads, one row read in flight
-    TG_CUDA_CHECK(cudaFuncSetAttribute(nn_chain_cta_kernel<512, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    TG_CUDA_CHECK(cudaFuncSetAttribute(nn_chain_cta_kernel<NN_SMALL_T, NN_SMALL_U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)nn_smem));
     TG_CUDA_CHECK(cudaFuncSetAttribute(nn_chain_cta_kernel<1024, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)nn_smem));
-    nn_chain_cta_kernel<512, 4><<<(unsigned)cblocks, 512, nn_smem, st>>>(mats, mat_off, sizes, count, merge_off, lefts,
+    nn_chain_cta_kernel<NN_SMALL_T, NN_SMALL_U><<<(unsigned)cblocks, NN_SMALL_T, nn_smem, st>>>(mats, mat_off, sizes, count, merge_off, lefts,
                                                                         rights, heights, active, slot, chain, aux_off);
     nn_chain_cta_kernel<1024, 8><<<(unsigned)cblocks, 1024, nn_smem, st>>>(mats, mat_off, sizes, count, merge_off,
                                                                           lefts, rights, heights, active, slot, chain,
