@@ -4,25 +4,19 @@
 // id asc), v removed; numpy argsort + lexsort tie rule) and tmfg.py:71-79
 // select_initial_clique (numpy pairwise row sums, stable top-4).
 //
-// B200 design (one CTA of 1024 threads per row, persistent over rows):
-//   1. the row (8n bytes) is streamed into shared memory with 16-byte cp.async,
-//      double-buffered so row v+grid loads while row v is sorted;
-//   2. equalised two-level bucketing: a warp-aggregated histogram over 512
-//      linear bins of [min, max] sizes each bin's share of fine buckets
-//      (ceil(count/2)), and each bin is split linearly again -- about two keys
-//      per fine bucket whatever the value distribution; bucket ids are monotone
-//      in the value and equal values (incl. -0.0/+0.0) share a bucket;
-//   3. one shared-memory atomicAdd per key yields its rank inside the fine
-//      bucket; a block scan gives bucket starts and the ids (u16) are scattered;
-//   4. every key's exact rank inside its bucket (value desc, id asc) is counted
-//      against the other members (independent loads, cost = bucket size), and
-//      the ids are placed once more -- so the result is deterministic even though
-//      the atomic ranks are not; degenerate rows with huge tie groups stay
-//      correct (quadratic in the group size only);
-//   5. the ids stream out with 16-byte stores; optionally the same pass computes
-//      numpy's pairwise row sum from the staged row (fused initial-clique input).
-// Rows longer than the shared-memory budget (n > 16384) take the global-memory
-// variant below (same algorithm, the row and the scatter buffer live in L2).
+// B200 design (details at each kernel):
+//   * n <= 24,576: row_sort_fk_kernel -- one 1024-thread CTA per SM, persistent over
+//     rows, rows arriving by TMA bulk copies into two recycled row buffers; float keys,
+//     an equalised two-level bucket map, one packed-u16 shared atomic per key, a block
+//     scan, and the exact in-bucket rank by sorted position (warp shuffles); the same
+//     pass emits the initial-clique row-sum screen;
+//   * n > 24,576: row_part_kernel (value-bin partition of each row into segments of
+//     <= 12,288 keys, through a scratch row) + row_seg_kernel (the same bucket sort per
+//     segment in shared memory);
+//   * rows with NaN / values outside [-1, 1] / one dominant value bin at n > 24,576:
+//     row_sort_global_kernel (the bucket algorithm with the row in L2).
+// The result is deterministic although the atomic arrival ranks are not: positions come
+// from bucket offsets plus exact ranks (value desc, id asc, -0.0 == +0.0, NaN last).
 #include "common.cuh"
 
 #include <cmath>
@@ -32,7 +26,6 @@ namespace {
 
 constexpr int RS_T = 1024;
 constexpr int PW_MAXNODES = 2048;   // n <= 131072
-constexpr int PW_SMALLNODES = 512;  // n <= 16384
 
 // ---------------------------------------------------------------- pairwise tree
 // numpy's float64 add.reduce inner loop: pairwise_sum(a, n) with 8 accumulators,
@@ -332,75 +325,12 @@ __device__ __forceinline__ int rs_fine_of(double t, int c, const uint32_t *base,
     return (int)base[c] + sub;
 }
 
-// ---------------------------------------------------------------- TMA-fed kernel
-// One CTA (1024 threads) per SM, persistent over rows v = blockIdx.x + k*grid.
-//  * row v+grid is one cp.async.bulk (TMA) copy into the other row buffer,
-//    issued by one thread and tracked by an mbarrier (+ <= 2 unaligned edge
-//    doubles by cp.async, which arrive on the same mbarrier);
-//  * min / max (rounded outward to float for cheap reductions) define C linear
-//    coarse bins; a sampled histogram sizes each bin's share of the fine buckets
-//    (~fs buckets per key, fs sized to fill shared memory), each bin split
-//    linearly again: bucket ids are monotone in the value, equal values share one;
-//  * one packed-u16 shared atomic per key gives its bucket and arrival rank, a
-//    block scan the bucket offsets; (bucket, id) pairs are scattered;
-//  * the exact rank inside a bucket (value desc, id asc) runs by sorted POSITION:
-//    the lanes of a warp hold consecutive positions, so bucket walks mostly
-//    coincide and the id store is coalesced;
-//  * the same pass writes the initial-clique row-sum screen (sum, bound).
-struct RtPlan {
-    int n, C, NBcap, nbuf, stride;
-    float fs;   // fine buckets per key
-    size_t off_sidx, off_f16, off_cinfo, off_misc, off_bar, smem;
-};
-
 #ifndef RS_DEBUG_PHASES
 #define RS_DEBUG_PHASES 0
 #endif
 #if RS_DEBUG_PHASES
 __device__ long long g_rs_phase[8];
 #endif
-
-struct RtCoarse {   // per coarse bin after the allocation phase
-    double f;       // fine buckets in the bin (as double)
-    int base, last; // first / last fine bucket id
-};
-
-struct RtMisc {
-    float rmn[32], rmx[32];
-    double rsum[32], rabs[32];
-    uint32_t wsum[32];
-    uint32_t nsamp;
-};
-
-__host__ RtPlan rt_plan(int64_t n, int nbuf, size_t smem_max) {
-    RtPlan p;
-    p.n = (int)n;
-    const int m = (int)n - 1;
-    p.C = rs_coarse_bins(m);
-    p.nbuf = nbuf;
-    p.stride = (int)((n + 2) & ~1LL);   // room for the 8-byte alignment shift, 16-byte aligned buffers
-    size_t off = tg_align_up((size_t)nbuf * p.stride * sizeof(double), 16);
-    p.off_sidx = off;
-    off = tg_align_up(off + (size_t)n * sizeof(uint32_t), 16);
-    p.off_cinfo = off;   // also the coarse histogram (u32 x C) before the allocation phase
-    off = tg_align_up(off + (size_t)p.C * sizeof(RtCoarse), 16);
-    p.off_misc = off;
-    off = tg_align_up(off + sizeof(RtMisc), 16);
-    p.off_bar = off;
-    off += 2 * sizeof(uint64_t);
-    p.off_f16 = tg_align_up(off, 16);
-    // the rest: packed u16 fine-bucket counters; NB <= 2C + fs*m + 1 entries
-    const size_t fixed = p.off_f16 + 64;
-    double room = smem_max > fixed ? (double)(smem_max - fixed) / 2.0 : 0.0;   // u16 entries
-    double fs = (room - 2.0 * p.C - 8.0) / (double)(m > 0 ? m : 1);
-    if (fs > 2.0) fs = 2.0;
-    p.fs = (float)fs;
-    p.NBcap = 2 * p.C + (int)std::ceil(fs * m) + 2;
-    p.smem = p.off_f16 + (size_t)(p.NBcap / 2 + 2) * sizeof(uint32_t);
-    if (fs < 0.45 || p.NBcap >= 65535) p.smem = (size_t)-1;   // does not fit: caller tries the next layout
-    return p;
-}
-
 __device__ __forceinline__ unsigned rt_smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ void rt_bulk_row(double *buf, const double *row, int n, uint64_t *bar) {
@@ -430,274 +360,6 @@ __device__ __forceinline__ void rt_wait(uint64_t *bar, unsigned parity) {
         " @!p bra RT_WAIT_%=;\n}\n" ::"r"(rt_smem_u32(bar)),
         "r"(parity)
         : "memory");
-}
-
-template <int EMAX>
-__global__ void __launch_bounds__(RS_T, 1)
-row_sort_tma_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restrict__ order,
-                    double *__restrict__ screen, RtPlan pl) {
-    extern __shared__ __align__(16) unsigned char rs_smem[];
-    const int n = (int)n64;
-    const int m = n - 1;
-    double *vbuf = reinterpret_cast<double *>(rs_smem);
-    uint32_t *sidx = reinterpret_cast<uint32_t *>(rs_smem + pl.off_sidx);   // (bucket << 16) | id
-    RtCoarse *cinfo = reinterpret_cast<RtCoarse *>(rs_smem + pl.off_cinfo);
-    uint32_t *ccnt = reinterpret_cast<uint32_t *>(rs_smem + pl.off_cinfo);   // aliased: histogram first
-    RtMisc &ms = *reinterpret_cast<RtMisc *>(rs_smem + pl.off_misc);
-    uint64_t *bar = reinterpret_cast<uint64_t *>(rs_smem + pl.off_bar);
-    uint32_t *f16 = reinterpret_cast<uint32_t *>(rs_smem + pl.off_f16);
-    const uint16_t *o16 = reinterpret_cast<const uint16_t *>(f16);   // bucket offsets, read side
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int C = pl.C;
-    const int nw16 = pl.NBcap / 2 + 2;
-
-    if (tid == 0) {
-        // two arrivals per phase: expect_tx (TMA body) + cp.async (unaligned edges)
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;\n" ::"r"(rt_smem_u32(&bar[0])) : "memory");
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;\n" ::"r"(rt_smem_u32(&bar[1])) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    __syncthreads();
-    int64_t v = blockIdx.x;
-    if (tid == 0 && v < n) rt_bulk_row(vbuf, S + v * n64, n, &bar[0]);
-#if RS_DEBUG_PHASES
-    long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    long long pt = clock64();
-#define RS_PH(k) do { if (tid == 0) { const long long now = clock64(); ph[k] += now - pt; pt = now; } } while (0)
-#else
-#define RS_PH(k) do {} while (0)
-#endif
-    for (int it = 0; v < n; v += gridDim.x, it++) {
-        const int b = pl.nbuf == 2 ? (it & 1) : 0;
-        const unsigned parity = pl.nbuf == 2 ? (unsigned)((it >> 1) & 1) : (unsigned)(it & 1);
-        const double *row = S + v * n64;
-        const double *vals = vbuf + (size_t)b * pl.stride + (((uintptr_t)row >> 3) & 1);
-        rt_wait(&bar[b], parity);
-        RS_PH(0);
-        // ---- A: clear counters; row min / max / NaN (v excluded); row-sum screen
-        for (int i = tid; i < nw16; i += RS_T) f16[i] = 0u;
-        for (int c = tid; c < C; c += RS_T) ccnt[c] = 0u;
-        if (tid == 0) ms.nsamp = 0;
-        double mn = INFINITY, mx = -INFINITY, sm = 0.0, sa = 0.0;
-        bool nan_seen = false;
-#pragma unroll
-        for (int e = 0; e < EMAX; e++) {
-            const int j = tid + e * RS_T;
-            if (j < n) {
-                const double x = vals[j];
-                sm += x;
-                sa += fabs(x);
-                if (j != v) {
-                    mn = x < mn ? x : mn;   // NaN: never selected, flagged instead
-                    mx = x > mx ? x : mx;
-                    nan_seen |= (x != x);
-                }
-            }
-        }
-        // float bounds rounded outward: the bins only need a range that contains the row
-        float fmn = __double2float_rd(mn), fmx = __double2float_ru(mx);
-        for (int o = 16; o; o >>= 1) {
-            fmn = fminf(fmn, __shfl_xor_sync(0xffffffffu, fmn, o));
-            fmx = fmaxf(fmx, __shfl_xor_sync(0xffffffffu, fmx, o));
-        }
-        if (screen) {
-            for (int o = 16; o; o >>= 1) {
-                sm += __shfl_xor_sync(0xffffffffu, sm, o);
-                sa += __shfl_xor_sync(0xffffffffu, sa, o);
-            }
-        }
-        if (lane == 0) { ms.rmn[warp] = fmn; ms.rmx[warp] = fmx; ms.rsum[warp] = sm; ms.rabs[warp] = sa; }
-        const bool row_nan = __syncthreads_or(nan_seen);   // also: every thread is past the row wait
-        if (tid == 0 && pl.nbuf == 2) {
-            const int64_t vn = v + gridDim.x;
-            if (vn < n) rt_bulk_row(vbuf + (size_t)(b ^ 1) * pl.stride, S + vn * n64, n, &bar[b ^ 1]);
-        }
-        double rmax, cscale;
-        {
-            float a = ms.rmn[lane], bb = ms.rmx[lane];
-            for (int o = 16; o; o >>= 1) {
-                a = fminf(a, __shfl_xor_sync(0xffffffffu, a, o));
-                bb = fmaxf(bb, __shfl_xor_sync(0xffffffffu, bb, o));
-            }
-            const double w = (double)bb - (double)a;
-            rmax = (double)bb;
-            cscale = (w > 0.0 && w < INFINITY) ? (double)C / w : 0.0;
-        }
-        if (screen && warp == 1) {
-            double s1 = ms.rsum[lane], s2 = ms.rabs[lane];
-            for (int o = 16; o; o >>= 1) {
-                s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-                s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-            }
-            if (lane == 0) {
-                screen[v] = __dsub_rn(s1, vals[v]);
-                screen[n + v] = rs_screen_radius(n, s2);
-            }
-        }
-        RS_PH(1);
-        // ---- B: coarse histogram from a sample (sizes the fine buckets only)
-        int nsamp = 0;
-#pragma unroll
-        for (int e = 0; e < EMAX; e += 4) {
-            const int j = tid + e * RS_T;
-            if (j < n && j != v) {
-                double t;
-                atomicAdd(&ccnt[rs_coarse_of(vals[j], rmax, cscale, C, t)], 1u);
-                nsamp++;
-            }
-        }
-        nsamp = __reduce_add_sync(0xffffffffu, nsamp);
-        if (lane == 0 && nsamp) atomicAdd(&ms.nsamp, (uint32_t)nsamp);
-        __syncthreads();
-        RS_PH(2);
-        // ---- C: fine buckets per coarse bin + base offsets: one thread per bin (C <= 512),
-        // warp scans + a 16-entry scan of warp totals; written in place over the histogram
-        // (every read happens before the first barrier below)
-        {
-            const float scale = (float)m * pl.fs / (float)(ms.nsamp ? ms.nsamp : 1u) * 0.9999f;
-            const uint32_t f = tid < C ? 1u + (uint32_t)((float)ccnt[tid] * scale) : 0u;
-            uint32_t incl = f;
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
-            }
-            if (lane == 31 && warp < RS_CMAX / 32) ms.wsum[warp] = incl;
-            __syncthreads();
-            if (tid < C) {
-                uint32_t off = 0;
-                for (int w = 0; w < warp; w++) off += ms.wsum[w];
-                const uint32_t base = off + incl - f;
-                RtCoarse ci;
-                ci.f = (double)f;
-                ci.base = (int)base;
-                ci.last = (int)(base + f - 1);
-                cinfo[tid] = ci;
-            }
-        }
-        __syncthreads();
-        RS_PH(3);
-        // ---- D: fine bucket + arrival rank (one packed shared atomic per key)
-        uint32_t pk[EMAX];
-#pragma unroll
-        for (int e = 0; e < EMAX; e++) {
-            const int j = tid + e * RS_T;
-            pk[e] = 0xffffffffu;
-            if (j < n && j != v) {
-                const double x = vals[j];
-                int fb;
-                if (!row_nan) {
-                    const double t = (rmax - x) * cscale;
-                    int c = __double2int_rz(t);
-                    c = c < C - 1 ? c : C - 1;
-                    c = c > 0 ? c : 0;
-                    const RtCoarse ci = cinfo[c];
-                    fb = ci.base + __double2int_rz((t - (double)c) * ci.f);
-                    fb = fb < ci.last ? fb : ci.last;
-                    fb = fb > ci.base ? fb : ci.base;
-                } else {
-                    double t;
-                    const int c = rs_coarse_of(x, rmax, cscale, C, t);
-                    const RtCoarse ci = cinfo[c];
-                    const double frac = t - (double)c;
-                    int sub = (frac >= 0.0) ? (int)(frac * ci.f) : 0;
-                    fb = ci.base + sub;
-                    fb = fb < ci.last ? fb : ci.last;
-                }
-                const int sh = (fb & 1) << 4;
-                const uint32_t old = atomicAdd(&f16[fb >> 1], 1u << sh);
-                pk[e] = ((uint32_t)fb << 16) | ((old >> sh) & 0xffffu);
-            }
-        }
-        __syncthreads();
-        RS_PH(4);
-        // ---- E: exclusive scan of the packed counters, scatter ids, bucket-start bits
-        {
-            const int NB = cinfo[C - 1].last + 1;
-            const int nw = (NB + 2) >> 1;
-            const int per = (nw + RS_T - 1) / RS_T;
-            const int w0 = tid * per;
-            uint32_t s = 0;
-            for (int q = 0; q < per; q++) {
-                const int w = w0 + q;
-                if (w < nw) { const uint32_t x = f16[w]; s += (x & 0xffffu) + (x >> 16); }
-            }
-            uint32_t incl = s;
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
-            }
-            if (lane == 31) ms.wsum[warp] = incl;
-            __syncthreads();
-            uint32_t wex = 0;
-            {
-                const uint32_t wv = ms.wsum[lane];
-                uint32_t wi = wv;
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
-                    if (lane >= o) wi += y;
-                }
-                wex = __shfl_sync(0xffffffffu, wi - wv, warp);
-            }
-            uint32_t run = wex + incl - s;
-            for (int q = 0; q < per; q++) {
-                const int w = w0 + q;
-                if (w < nw) {
-                    const uint32_t x = f16[w];
-                    const uint32_t lo = run, hi = run + (x & 0xffffu);
-                    f16[w] = lo | (hi << 16);
-                    run = hi + (x >> 16);
-                }
-            }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int e = 0; e < EMAX; e++) {
-            if (pk[e] != 0xffffffffu) {
-                sidx[o16[pk[e] >> 16] + (pk[e] & 0xffffu)] = (pk[e] & 0xffff0000u) | (uint32_t)(tid + e * RS_T);
-            }
-        }
-        __syncthreads();
-        RS_PH(5);
-        // ---- F: exact rank by sorted position (value desc, id asc), coalesced id store
-        int32_t *out = order + v * (int64_t)m;
-#pragma unroll
-        for (int e = 0; e < EMAX; e++) {
-            const int k = tid + e * RS_T;
-            if (k < m) {
-                const uint32_t sk = sidx[k];
-                const int fb = (int)(sk >> 16), j = (int)(sk & 0xffffu);
-                const int s0 = o16[fb], s1 = o16[fb + 1];
-                int rank = 0;
-                if (s1 - s0 > 1) {
-                    const double xj = vals[j];
-                    if (!row_nan) {
-                        for (int q = s0; q < s1; q++) {
-                            const int o = (int)(sidx[q] & 0xffffu);
-                            const double xo = vals[o];
-                            rank += (xo > xj) | ((xo == xj) & (o < j));
-                        }
-                    } else {
-                        for (int q = s0; q < s1; q++) {
-                            const int o = (int)(sidx[q] & 0xffffu);
-                            rank += rs_before(vals[o], o, xj, j);
-                        }
-                    }
-                }
-                out[s0 + rank] = j;
-            }
-        }
-        __syncthreads();
-        RS_PH(6);
-        if (tid == 0 && pl.nbuf == 1) {
-            const int64_t vn = v + gridDim.x;
-            if (vn < n) rt_bulk_row(vbuf, S + vn * n64, n, &bar[0]);
-        }
-    }
-#if RS_DEBUG_PHASES
-    if (tid == 0)
-        for (int k = 0; k < 7; k++) atomicAdd((unsigned long long *)&g_rs_phase[k], (unsigned long long)ph[k]);
-#endif
-#undef RS_PH
 }
 
 // ---------------------------------------------------------------- float-key kernel
@@ -1741,7 +1403,7 @@ TG_API int tg_row_sort_f64(const double *S, int64_t n, int32_t *order, double *s
     cudaStream_t st = tg_stream(stream);
     int grid = tg_num_sms();
     if (grid > n) grid = (int)n;
-    if (n <= FK_NMAX && !getenv("TG_SORT_OLD")) {
+    if (n <= FK_NMAX) {
         // two row buffers (the next row's TMA overlaps this row) when they leave room
         // for >= 1.5 fine buckets per key, else one
         const char *fse = getenv("TG_SORT_FS");
@@ -1766,29 +1428,6 @@ TG_API int tg_row_sort_f64(const double *S, int64_t n, int32_t *order, double *s
         TG_LAUNCH_CHECK();
         return TG_OK;
     }
-    if (n <= 16384) {
-        // preference: two row buffers (TMA of row v+grid overlaps row v) with one key per
-        // fine bucket; then two keys per bucket; then a single buffer
-        // two row buffers (TMA of row v+grid overlaps row v) when they leave room for
-        // >= 0.45 fine buckets per key, else one
-        RtPlan pl = rt_plan(n, 2, RS_SMEM_MAX);
-        if (pl.smem > RS_SMEM_MAX) pl = rt_plan(n, 1, RS_SMEM_MAX);
-        if (pl.smem > RS_SMEM_MAX) return TG_ERR_ARG;
-        int E = (int)((n + RS_T - 1) / RS_T);
-#define RS_LAUNCH(EM)                                                                                      \
-    do {                                                                                                   \
-        auto kfn = row_sort_tma_kernel<EM>;                                                                \
-        TG_CUDA_CHECK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem)); \
-        kfn<<<grid, RS_T, pl.smem, st>>>(S, n, order, screen, pl); tg_count_launch(1);                      \
-    } while (0)
-        if (E <= 2) RS_LAUNCH(2);
-        else if (E <= 4) RS_LAUNCH(4);
-        else if (E <= 8) RS_LAUNCH(8);
-        else RS_LAUNCH(16);
-#undef RS_LAUNCH
-        TG_LAUNCH_CHECK();
-        return TG_OK;
-    }
     if (ws_bytes < tg_row_sort_workspace_bytes(n)) return TG_ERR_WORKSPACE;
     if (2 * (n - 1) / SEG_MAX + 2 > SP_MAXSEG) return TG_ERR_ARG;
     TgArena ar(ws, ws_bytes);
@@ -1797,11 +1436,6 @@ TG_API int tg_row_sort_f64(const double *S, int64_t n, int32_t *order, double *s
     size_t smem = (size_t)(rs_fine_cap(m) + 1) * sizeof(uint32_t);
     if (smem > 160 * 1024) return TG_ERR_ARG;
     TG_CUDA_CHECK(cudaFuncSetAttribute(row_sort_global_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (getenv("TG_SORT_OLD")) {
-        row_sort_global_kernel<<<grid, RS_T, smem, st>>>(S, n, order, screen, gpk, nullptr, nullptr); tg_count_launch(1);
-        TG_LAUNCH_CHECK();
-        return TG_OK;
-    }
     // partition into segments per batch of rows, sort the segments in shared memory,
     // then the listed rows (NaN, out of range, one huge bin) with the global kernel
     const int64_t B = seg_batch_rows(n);

@@ -16,6 +16,6 @@ for rep in range(3):
     simmatrix.sort_rows_device(S, with_screen=True)
     torch.cuda.synchronize()
 lib.tg_row_sort_debug_phases(buf)
-names = (["wait_row", "pass1", "alloc", "D_bucket", "E_scan", "scatter", "F_rank"] if not os.environ.get("TG_SORT_OLD") else ["wait_row", "A_minmax", "B_sample", "C_alloc", "D_bucket", "E_scan_scatter", "F_rank"])
+names = ["wait_row", "pass1", "rest (alloc .. rank)", "-", "-", "-", "end barrier"]
 per_row = [buf[k] / n for k in range(7)]
 print({names[k]: round(per_row[k]) for k in range(7)}, "total", round(sum(per_row)))
