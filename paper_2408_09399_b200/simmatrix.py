@@ -55,12 +55,12 @@ class Dataset:
         return int(self.labels.max()) + 1 if self.labels.size else 0
 
 
-def pearson_similarity_device(X):
-    """(n, L) series (host or device) -> (n, n) float64 CUDA tensor S."""
+def pearson_similarity_device(X, out=None):
+    """(n, L) series (host or device) -> (n, n) float64 CUDA tensor S (``out`` if given)."""
     t = D.torch()
     Xd = D.to_device(X, t.float64)
     n, L = (int(s) for s in Xd.shape)
-    S = D.empty((n, n), t.float64)
+    S = out if out is not None else D.empty((n, n), t.float64)
     ws = D.Workspace.get(N.size("tg_pearson_workspace_bytes", n, L))
     N.call("tg_pearson_f64", N.ptr(Xd), n, L, N.ptr(S), N.ptr(ws), ws.numel(), N.stream_ptr())
     return S
@@ -172,8 +172,8 @@ class SortedNeighborLists:
         return [(float(row[u]), int(u)) for u in self.order[v]]
 
 
-def sort_rows_device(Sd, with_screen: bool = True):
-    """(order (n, n-1) int32, screen (2n,) float64 or None) as CUDA tensors.
+def sort_rows_device(Sd, with_screen: bool = True, out=None):
+    """(order (n, n-1) int32, screen (2n,) float64 or None) as CUDA tensors (``order`` = out if given).
 
     ``screen[v]`` is row v's off-diagonal sum in the kernel's summation order and
     ``screen[n + v]`` a rigorous bound on its distance to numpy's pairwise sum
@@ -181,7 +181,7 @@ def sort_rows_device(Sd, with_screen: bool = True):
     """
     t = D.torch()
     n = int(Sd.shape[0])
-    order = D.empty((n, max(n - 1, 0)), t.int32)
+    order = out if out is not None else D.empty((n, max(n - 1, 0)), t.int32)
     screen = D.empty((2 * n,), t.float64) if (with_screen and n >= 2) else None
     if n >= 2:
         ws = D.Workspace.get(N.size("tg_row_sort_workspace_bytes", n))
