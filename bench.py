@@ -227,7 +227,7 @@ def run_b200(args, world, rank, local):
         flush.zero_()
         a, b = ev(), ev()
         a.record()
-        simmatrix.sort_rows_device(S, with_screen=True)
+        simmatrix.sort_rows_device(S, with_screen=True, out=order_buf)
         b.record()
         torch.cuda.synchronize()
         sort_ms.append(a.elapsed_time(b))
