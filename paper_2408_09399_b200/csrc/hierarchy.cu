@@ -54,6 +54,26 @@ struct DevBuf {
     T *as() const { return reinterpret_cast<T *>(p); }
 };
 
+// a non-blocking side stream that starts after everything already queued on `main`
+struct SideStream {
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev = nullptr;
+    cudaError_t open(cudaStream_t main) {
+        cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return e;
+        if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+        if ((e = cudaEventRecord(ev, main)) != cudaSuccess) return e;
+        return cudaStreamWaitEvent(st, ev, 0);
+    }
+    ~SideStream() {
+        if (st) {
+            cudaStreamSynchronize(st);
+            cudaStreamDestroy(st);
+        }
+        if (ev) cudaEventDestroy(ev);
+    }
+};
+
 struct Rec {
     int64_t l, r;
     double h;
@@ -84,52 +104,70 @@ struct Ctx {
         if (_r != TG_OK) return _r; \
     } while (0)
 
-// NN-chain every matrix of the batch (device, in place), canonicalise (stable
-// height sort, renumbering), append the records; per matrix: root handle + rows.
-int run_linkages(Ctx &cx, double *mats_dev, const std::vector<int64_t> &sizes, const std::vector<int64_t> &mat_off,
-                 const std::vector<std::vector<int64_t>> &handles, std::vector<int64_t> &roots,
-                 std::vector<Row> &rows_out) {
-    const size_t count = sizes.size();
-    std::vector<int64_t> merge_off(count + 1, 0), aux_off(count + 1, 0);
+// A batch of linkages in flight on one stream: the NN-chain of every matrix runs on the
+// device (in place); collect() waits, canonicalises (stable height sort, renumbering) and
+// appends the records.  Launch and collect are split so that two layers' device work can
+// overlap (layers 2 and 3 are independent until their records are labelled).
+struct LinkJob {
+    cudaStream_t st = nullptr;
+    DevBuf gm_buf, nn_buf;   // group-max inputs / output matrices, NN-chain outputs / scratch
+    std::vector<int64_t> sizes, mat_off, merge_off;
+    int64_t total = 0;
+    int64_t *d_l = nullptr, *d_r = nullptr;
+    double *d_h = nullptr;
+};
+
+int launch_linkages(Ctx &cx, LinkJob &job, double *mats_dev) {
+    const size_t count = job.sizes.size();
+    job.merge_off.assign(count + 1, 0);
+    std::vector<int64_t> aux_off(count + 1, 0);
     for (size_t k = 0; k < count; k++) {
-        merge_off[k + 1] = merge_off[k] + std::max<int64_t>(sizes[k] - 1, 0);
-        aux_off[k + 1] = aux_off[k] + sizes[k];
+        job.merge_off[k + 1] = job.merge_off[k] + std::max<int64_t>(job.sizes[k] - 1, 0);
+        aux_off[k + 1] = aux_off[k] + job.sizes[k];
     }
-    const int64_t total = merge_off[count], naux = aux_off[count];
-    roots.assign(count, -1);
-    if (total == 0) {
-        for (size_t k = 0; k < count; k++) roots[k] = handles[k][0];
-        return TG_OK;
-    }
+    job.total = job.merge_off[count];
+    const int64_t naux = aux_off[count];
+    if (job.total == 0) return TG_OK;
     // one device block: [mat_off | sizes | merge_off | aux_off] int64, then outputs / scratch
     const size_t nidx = 4 * (count + 1);
-    const size_t b_idx = tg_align_up(nidx * 8, 256), b_l = tg_align_up((size_t)total * 8, 256);
+    const size_t b_idx = tg_align_up(nidx * 8, 256), b_l = tg_align_up((size_t)job.total * 8, 256);
     const size_t b_h = b_l, b_slot = tg_align_up((size_t)naux * 8, 256), b_chain = tg_align_up((size_t)(naux + 1) * 8, 256);
     const size_t b_act = tg_align_up((size_t)naux, 256);
-    DevBuf buf;
-    HC(buf.alloc(b_idx + 2 * b_l + b_h + b_slot + b_chain + b_act, cx.st));
-    char *base = buf.as<char>();
+    HC(job.nn_buf.alloc(b_idx + 2 * b_l + b_h + b_slot + b_chain + b_act, job.st));
+    char *base = job.nn_buf.as<char>();
     int64_t *d_idx = reinterpret_cast<int64_t *>(base);
-    int64_t *d_l = reinterpret_cast<int64_t *>(base + b_idx);
-    int64_t *d_r = reinterpret_cast<int64_t *>(base + b_idx + b_l);
-    double *d_h = reinterpret_cast<double *>(base + b_idx + 2 * b_l);
+    job.d_l = reinterpret_cast<int64_t *>(base + b_idx);
+    job.d_r = reinterpret_cast<int64_t *>(base + b_idx + b_l);
+    job.d_h = reinterpret_cast<double *>(base + b_idx + 2 * b_l);
     int64_t *d_slot = reinterpret_cast<int64_t *>(base + b_idx + 2 * b_l + b_h);
     int64_t *d_chain = reinterpret_cast<int64_t *>(base + b_idx + 2 * b_l + b_h + b_slot);
     uint8_t *d_act = reinterpret_cast<uint8_t *>(base + b_idx + 2 * b_l + b_h + b_slot + b_chain);
     std::vector<int64_t> idx(nidx, 0);
-    std::copy(mat_off.begin(), mat_off.end(), idx.begin());
-    std::copy(sizes.begin(), sizes.end(), idx.begin() + (count + 1));
-    std::copy(merge_off.begin(), merge_off.end(), idx.begin() + 2 * (count + 1));
+    std::copy(job.mat_off.begin(), job.mat_off.end(), idx.begin());
+    std::copy(job.sizes.begin(), job.sizes.end(), idx.begin() + (count + 1));
+    std::copy(job.merge_off.begin(), job.merge_off.end(), idx.begin() + 2 * (count + 1));
     std::copy(aux_off.begin(), aux_off.end(), idx.begin() + 3 * (count + 1));
-    HC(cudaMemcpyAsync(d_idx, idx.data(), nidx * 8, cudaMemcpyHostToDevice, cx.st));
-    HR(tg_nn_chain_batch(mats_dev, d_idx, d_idx + (count + 1), (int64_t)count, d_idx + 2 * (count + 1), d_l, d_r, d_h,
-                         d_idx + 3 * (count + 1), d_act, d_slot, d_chain, cx.st));
+    HC(cudaMemcpyAsync(d_idx, idx.data(), nidx * 8, cudaMemcpyHostToDevice, job.st));
+    HR(tg_nn_chain_batch(mats_dev, d_idx, d_idx + (count + 1), (int64_t)count, d_idx + 2 * (count + 1), job.d_l,
+                         job.d_r, job.d_h, d_idx + 3 * (count + 1), d_act, d_slot, d_chain, job.st));
+    return TG_OK;
+}
+
+int collect_linkages(Ctx &cx, LinkJob &job, const std::vector<std::vector<int64_t>> &handles,
+                     std::vector<int64_t> &roots, std::vector<Row> &rows_out) {
+    const size_t count = job.sizes.size();
+    roots.assign(count, -1);
+    const int64_t total = job.total;
+    if (total == 0) {
+        for (size_t k = 0; k < count; k++) roots[k] = handles[k][0];
+        return TG_OK;
+    }
+    HC(cudaStreamSynchronize(job.st));
     std::vector<int64_t> L(total), R(total);
     std::vector<double> Hh(total);
-    HC(cudaMemcpyAsync(L.data(), d_l, total * 8, cudaMemcpyDeviceToHost, cx.st));
-    HC(cudaMemcpyAsync(R.data(), d_r, total * 8, cudaMemcpyDeviceToHost, cx.st));
-    HC(cudaMemcpyAsync(Hh.data(), d_h, total * 8, cudaMemcpyDeviceToHost, cx.st));
-    HC(cudaStreamSynchronize(cx.st));
+    HC(cudaMemcpy(L.data(), job.d_l, total * 8, cudaMemcpyDeviceToHost));
+    HC(cudaMemcpy(R.data(), job.d_r, total * 8, cudaMemcpyDeviceToHost));
+    HC(cudaMemcpy(Hh.data(), job.d_h, total * 8, cudaMemcpyDeviceToHost));
     for (int64_t q = 0; q < total; q++) {
         uint64_t bits;
         std::memcpy(&bits, &Hh[q], 8);
@@ -137,7 +175,7 @@ int run_linkages(Ctx &cx, double *mats_dev, const std::vector<int64_t> &sizes, c
     }
     std::vector<int64_t> ord, rank, local;
     for (size_t k = 0; k < count; k++) {
-        const int64_t m = sizes[k], lo = merge_off[k], nm = merge_off[k + 1] - lo;
+        const int64_t m = job.sizes[k], lo = job.merge_off[k], nm = job.merge_off[k + 1] - lo;
         // linkage.py:97-116: stable sort of the raw merges by height, id m+t -> m+rank(t)
         ord.resize(nm);
         for (int64_t t = 0; t < nm; t++) ord[t] = t;
@@ -164,14 +202,24 @@ int run_linkages(Ctx &cx, double *mats_dev, const std::vector<int64_t> &sizes, c
     return TG_OK;
 }
 
-// dbht.py:217-230 group maxima for vertex-disjoint sub-problems (one launch), then the linkages
-int group_linkages(Ctx &cx, const std::vector<std::vector<const std::vector<int32_t> *>> &subproblems,
-                   const std::vector<std::vector<int64_t>> &handles, std::vector<int64_t> &roots,
-                   std::vector<Row> &rows_out) {
+// single-stream form: launch + collect
+int run_linkages(Ctx &cx, double *mats_dev, const std::vector<int64_t> &sizes, const std::vector<int64_t> &mat_off,
+                 const std::vector<std::vector<int64_t>> &handles, std::vector<int64_t> &roots,
+                 std::vector<Row> &rows_out) {
+    LinkJob job;
+    job.st = cx.st;
+    job.sizes = sizes;
+    job.mat_off = mat_off;
+    HR(launch_linkages(cx, job, mats_dev));
+    return collect_linkages(cx, job, handles, roots, rows_out);
+}
+
+// dbht.py:217-230 group maxima for vertex-disjoint sub-problems (one launch) on job.st, then
+// the linkages (launched; collect_linkages finishes them)
+int launch_group_linkages(Ctx &cx, LinkJob &job, const std::vector<std::vector<const std::vector<int32_t> *>> &subproblems) {
     std::vector<int32_t> perm, gid;
     std::vector<tg_gm_sub_t> subs;
     std::vector<tg_gm_tile_t> tiles;
-    std::vector<int64_t> sizes, mat_off;
     int64_t out_off = 0;
     for (size_t p = 0; p < subproblems.size(); p++) {
         const auto &groups = subproblems[p];
@@ -191,8 +239,8 @@ int group_linkages(Ctx &cx, const std::vector<std::vector<const std::vector<int3
         subs.push_back(sd);
         for (int32_t i0 = 0; i0 < len; i0 += 64)
             for (int32_t j0 = 0; j0 < len; j0 += 64) tiles.push_back({(int32_t)p, i0, j0});
-        sizes.push_back(m);
-        mat_off.push_back(out_off);
+        job.sizes.push_back(m);
+        job.mat_off.push_back(out_off);
         out_off += (int64_t)m * m;
     }
     const int64_t ntiles = (int64_t)tiles.size();
@@ -200,22 +248,21 @@ int group_linkages(Ctx &cx, const std::vector<std::vector<const std::vector<int3
     const size_t b_perm = tg_align_up(perm.size() * 4, 256), b_sub = tg_align_up(subs.size() * sizeof(tg_gm_sub_t), 256);
     const size_t b_tile = tg_align_up((size_t)ntiles * sizeof(tg_gm_tile_t), 256);
     const size_t b_out = tg_align_up((size_t)std::max<int64_t>(out_off, 1) * 8, 256);
-    DevBuf buf;
-    HC(buf.alloc(2 * b_perm + b_sub + b_tile + b_out + ws_bytes, cx.st));
-    char *base = buf.as<char>();
+    HC(job.gm_buf.alloc(2 * b_perm + b_sub + b_tile + b_out + ws_bytes, job.st));
+    char *base = job.gm_buf.as<char>();
     int32_t *d_perm = reinterpret_cast<int32_t *>(base);
     int32_t *d_gid = reinterpret_cast<int32_t *>(base + b_perm);
     void *d_sub = base + 2 * b_perm;
     void *d_tile = base + 2 * b_perm + b_sub;
     double *d_out = reinterpret_cast<double *>(base + 2 * b_perm + b_sub + b_tile);
     void *d_ws = base + 2 * b_perm + b_sub + b_tile + b_out;
-    HC(cudaMemcpyAsync(d_perm, perm.data(), perm.size() * 4, cudaMemcpyHostToDevice, cx.st));
-    HC(cudaMemcpyAsync(d_gid, gid.data(), gid.size() * 4, cudaMemcpyHostToDevice, cx.st));
-    HC(cudaMemcpyAsync(d_sub, subs.data(), subs.size() * sizeof(tg_gm_sub_t), cudaMemcpyHostToDevice, cx.st));
-    HC(cudaMemcpyAsync(d_tile, tiles.data(), (size_t)ntiles * sizeof(tg_gm_tile_t), cudaMemcpyHostToDevice, cx.st));
+    HC(cudaMemcpyAsync(d_perm, perm.data(), perm.size() * 4, cudaMemcpyHostToDevice, job.st));
+    HC(cudaMemcpyAsync(d_gid, gid.data(), gid.size() * 4, cudaMemcpyHostToDevice, job.st));
+    HC(cudaMemcpyAsync(d_sub, subs.data(), subs.size() * sizeof(tg_gm_sub_t), cudaMemcpyHostToDevice, job.st));
+    HC(cudaMemcpyAsync(d_tile, tiles.data(), (size_t)ntiles * sizeof(tg_gm_tile_t), cudaMemcpyHostToDevice, job.st));
     HR(tg_group_max_batch(cx.oracle, d_perm, d_gid, d_sub, (int64_t)subs.size(), d_tile, ntiles, d_out, out_off, d_ws,
-                          ws_bytes, cx.st));
-    return run_linkages(cx, d_out, sizes, mat_off, handles, roots, rows_out);
+                          ws_bytes, job.st));
+    return launch_linkages(cx, job, d_out);
 }
 
 void stable_sort_rows(std::vector<Row> &rows) {
@@ -284,10 +331,16 @@ int build(Ctx &cx, const int64_t *vb_dev, const int64_t *vc_dev, int64_t *lefts,
         stable_sort_rows(rows1);
     }
 
-    // ---- layer 2: bubbles inside each converging group (dbht.py:264-300)
+    // ---- layers 2 (bubbles inside each converging group, dbht.py:264-300) and 3 (converging
+    // groups against each other, dbht.py:302-324): their group maxima and linkages do not
+    // depend on each other -- only layer 3's record labels need layer 2's roots -- so both
+    // are launched (layer 3 on a side stream) before either is collected
     std::vector<int64_t> conv_ids;
     std::vector<std::vector<int64_t>> conv_bubbles;   // parallel to conv_ids
     std::vector<int64_t> conv_root;
+    std::vector<std::vector<const std::vector<int32_t> *>> subproblems;
+    std::vector<std::vector<int64_t>> handles2;
+    std::vector<size_t> which;
     {
         std::vector<std::pair<int64_t, int64_t>> cb;   // (conv id, bubble) in bubble order
         for (int64_t b : bubble_ids) cb.push_back({vc[members[b][0]], b});
@@ -303,9 +356,6 @@ int build(Ctx &cx, const int64_t *vb_dev, const int64_t *vc_dev, int64_t *lefts,
             conv_bubbles.back().push_back(x.second);
         }
         conv_root.assign(conv_ids.size(), -1);
-        std::vector<std::vector<const std::vector<int32_t> *>> subproblems;
-        std::vector<std::vector<int64_t>> handles;
-        std::vector<size_t> which;
         for (size_t c = 0; c < conv_ids.size(); c++) {
             if (conv_bubbles[c].size() == 1) {
                 conv_root[c] = group_root[conv_bubbles[c][0]];
@@ -318,33 +368,42 @@ int build(Ctx &cx, const int64_t *vb_dev, const int64_t *vc_dev, int64_t *lefts,
                 hs.push_back(group_root[b]);
             }
             subproblems.push_back(std::move(groups));
-            handles.push_back(std::move(hs));
+            handles2.push_back(std::move(hs));
             which.push_back(c);
         }
-        if (!subproblems.empty()) {
-            std::vector<int64_t> roots;
-            HR(group_linkages(cx, subproblems, handles, roots, rows2));
-            for (size_t k = 0; k < which.size(); k++) conv_root[which[k]] = roots[k];
-        }
-        stable_sort_rows(rows2);
     }
-
-    // ---- layer 3: converging groups against each other (dbht.py:302-324)
-    if (conv_ids.size() > 1) {
-        std::vector<std::vector<int32_t>> cmem(conv_ids.size());
-        std::vector<const std::vector<int32_t> *> groups;
-        std::vector<int64_t> hs;
+    const bool layer3 = conv_ids.size() > 1;
+    std::vector<std::vector<int32_t>> cmem(layer3 ? conv_ids.size() : 0);
+    std::vector<const std::vector<int32_t> *> groups3;
+    if (layer3) {
         for (size_t c = 0; c < conv_ids.size(); c++) {
             for (int64_t b : conv_bubbles[c]) cmem[c].insert(cmem[c].end(), members[b].begin(), members[b].end());
             std::sort(cmem[c].begin(), cmem[c].end());
+            groups3.push_back(&cmem[c]);
         }
-        for (size_t c = 0; c < conv_ids.size(); c++) {
-            groups.push_back(&cmem[c]);
-            hs.push_back(conv_root[c]);
+    }
+    SideStream side;
+    {
+        LinkJob j2, j3;
+        j2.st = cx.st;
+        if (layer3) {
+            HC(side.open(cx.st));
+            j3.st = side.st;
+            HR(launch_group_linkages(cx, j3, {groups3}));
         }
-        std::vector<int64_t> roots;
-        HR(group_linkages(cx, {groups}, {hs}, roots, rows3));
-        stable_sort_rows(rows3);
+        if (!subproblems.empty()) HR(launch_group_linkages(cx, j2, subproblems));
+        if (!subproblems.empty()) {
+            std::vector<int64_t> roots;
+            HR(collect_linkages(cx, j2, handles2, roots, rows2));
+            for (size_t k = 0; k < which.size(); k++) conv_root[which[k]] = roots[k];
+        }
+        stable_sort_rows(rows2);
+        if (layer3) {
+            std::vector<int64_t> hs, roots;
+            for (size_t c = 0; c < conv_ids.size(); c++) hs.push_back(conv_root[c]);
+            HR(collect_linkages(cx, j3, {hs}, roots, rows3));
+            stable_sort_rows(rows3);
+        }
     }
 
     // ---- emission with the running height floor (dbht.py:326-339) + sizes (linkage.py:136-148)
