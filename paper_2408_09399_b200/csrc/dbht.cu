@@ -575,13 +575,31 @@ __global__ void group_max_override_kernel(tg_oracle_t o, const int32_t *__restri
     }
 }
 
-__global__ void group_max_finalize_kernel(const GmSub *subs, int64_t nsub, int mode, double *out) {
-    for (int64_t p = blockIdx.x; p < nsub; p += gridDim.x) {
-        GmSub sb = subs[p];
+// exact mode: the kernels fill the upper triangle only; mirror it (segment_pair_max is
+// symmetric).  32x32 tiles through shared memory so both the read and the write coalesce;
+// every block walks all sub-problems, taking every gridDim.x-th tile of each (the first
+// tile rotating with the sub-problem so that many one-tile sub-problems spread out).
+__global__ void group_max_finalize_kernel(const GmSub *subs, int64_t nsub, double *out) {
+    __shared__ double tile[32][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
+    for (int64_t p = 0; p < nsub; p++) {
+        const GmSub sb = subs[p];
+        const int m = sb.m, nt = (m + 31) / 32;
         double *M = out + sb.out_off;
-        for (int e = threadIdx.x; e < sb.m * sb.m; e += blockDim.x) {
-            int i = e / sb.m, j = e % sb.m;
-            if (mode == 0 && i > j) M[e] = M[(int64_t)j * sb.m + i];  // mirror (segment_pair_max)
+        const int64_t t0 = ((int64_t)blockIdx.x + gridDim.x - p % gridDim.x) % gridDim.x;
+        for (int64_t t = t0; t < (int64_t)nt * nt; t += gridDim.x) {
+            const int ti = (int)(t / nt), tj = (int)(t % nt);
+            if (tj > ti) continue;
+            __syncthreads();
+            for (int r = ty; r < 32; r += 8) {   // source rows j (tile tj), columns i (tile ti)
+                const int j = tj * 32 + r, i = ti * 32 + tx;
+                if (j < m && i < m) tile[r][tx] = M[(int64_t)j * m + i];
+            }
+            __syncthreads();
+            for (int r = ty; r < 32; r += 8) {   // destination rows i, columns j, i > j
+                const int i = ti * 32 + r, j = tj * 32 + tx;
+                if (i < m && j < m && i > j) M[(int64_t)i * m + j] = tile[tx][r];
+            }
         }
     }
 }
@@ -1051,7 +1069,9 @@ TG_API int tg_group_max_batch(const tg_oracle_t *o, const int32_t *perm, const i
                                                        reinterpret_cast<unsigned long long *>(out), mask);
         tg_count_launch(1);
     }
-    group_max_finalize_kernel<<<(unsigned)min(nsub, (int64_t)65535), 256, 0, st>>>(subs, nsub, o->mode, out); tg_count_launch(1);
+    if (o->mode == 0) {   // hub mode evaluates every ordered pair: nothing to mirror
+        group_max_finalize_kernel<<<(unsigned)tg_num_sms() * 8, 256, 0, st>>>(subs, nsub, out); tg_count_launch(1);
+    }
     TG_LAUNCH_CHECK();
     return TG_OK;
 }

@@ -14,6 +14,8 @@
 #include <charconv>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <chrono>
 #include <cstring>
 #include <vector>
 
@@ -45,7 +47,7 @@ struct DevBuf {
         if (cudaGetDevice(&dev) != cudaSuccess || dev == dev_done) return;
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = 1ull << 30;   // keep up to 1 GiB cached
+            uint64_t thr = 16ull << 30;   // keep up to 16 GiB cached (n = 50k layer-3 buffers exceed 1 GiB)
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
         }
         dev_done = dev;
@@ -73,6 +75,18 @@ struct SideStream {
         if (ev) cudaEventDestroy(ev);
     }
 };
+
+static const bool g_hprof = std::getenv("TG_HIER_PROFILE") != nullptr;
+static std::chrono::steady_clock::time_point g_hprof_t;
+#define HPROF(name)                                                                                      \
+    do {                                                                                                 \
+        if (g_hprof) {                                                                                   \
+            auto _t = std::chrono::steady_clock::now();                                                  \
+            if (std::strcmp(name, "t0")) std::fprintf(stderr, "[hier] %s +%.3f ms\n", name,                \
+                                        std::chrono::duration<double, std::milli>(_t - g_hprof_t).count()); \
+            g_hprof_t = _t;                                                                              \
+        }                                                                                                \
+    } while (0)
 
 struct Rec {
     int64_t l, r;
@@ -165,9 +179,11 @@ int collect_linkages(Ctx &cx, LinkJob &job, const std::vector<std::vector<int64_
     HC(cudaStreamSynchronize(job.st));
     std::vector<int64_t> L(total), R(total);
     std::vector<double> Hh(total);
-    HC(cudaMemcpy(L.data(), job.d_l, total * 8, cudaMemcpyDeviceToHost));
-    HC(cudaMemcpy(R.data(), job.d_r, total * 8, cudaMemcpyDeviceToHost));
-    HC(cudaMemcpy(Hh.data(), job.d_h, total * 8, cudaMemcpyDeviceToHost));
+    // on the job's own stream: a legacy-stream cudaMemcpy would also wait for the other layers
+    HC(cudaMemcpyAsync(L.data(), job.d_l, total * 8, cudaMemcpyDeviceToHost, job.st));
+    HC(cudaMemcpyAsync(R.data(), job.d_r, total * 8, cudaMemcpyDeviceToHost, job.st));
+    HC(cudaMemcpyAsync(Hh.data(), job.d_h, total * 8, cudaMemcpyDeviceToHost, job.st));
+    HC(cudaStreamSynchronize(job.st));
     for (int64_t q = 0; q < total; q++) {
         uint64_t bits;
         std::memcpy(&bits, &Hh[q], 8);
@@ -202,53 +218,52 @@ int collect_linkages(Ctx &cx, LinkJob &job, const std::vector<std::vector<int64_
     return TG_OK;
 }
 
-// single-stream form: launch + collect
-int run_linkages(Ctx &cx, double *mats_dev, const std::vector<int64_t> &sizes, const std::vector<int64_t> &mat_off,
-                 const std::vector<std::vector<int64_t>> &handles, std::vector<int64_t> &roots,
-                 std::vector<Row> &rows_out) {
-    LinkJob job;
-    job.st = cx.st;
-    job.sizes = sizes;
-    job.mat_off = mat_off;
-    HR(launch_linkages(cx, job, mats_dev));
-    return collect_linkages(cx, job, handles, roots, rows_out);
-}
-
 // dbht.py:217-230 group maxima for vertex-disjoint sub-problems (one launch) on job.st, then
 // the linkages (launched; collect_linkages finishes them)
 int launch_group_linkages(Ctx &cx, LinkJob &job, const std::vector<std::vector<const std::vector<int32_t> *>> &subproblems) {
     std::vector<int32_t> perm, gid;
     std::vector<tg_gm_sub_t> subs;
     std::vector<tg_gm_tile_t> tiles;
-    int64_t out_off = 0;
+    int64_t out_off = 0, total_len = 0, total_tiles = 0;
+    for (const auto &groups : subproblems) {
+        int64_t len = 0;
+        for (const auto *g : groups) len += (int64_t)g->size();
+        total_len += len;
+        total_tiles += ((len + 63) / 64) * ((len + 63) / 64);
+    }
+    perm.reserve(total_len);
+    gid.reserve(total_len);
+    tiles.resize(total_tiles);   // filled in place below (n = 50k layer 3: 611k tiles)
+    tg_gm_tile_t *tp = tiles.data();
     for (size_t p = 0; p < subproblems.size(); p++) {
         const auto &groups = subproblems[p];
         const int64_t perm_off = (int64_t)perm.size();
-        for (size_t g = 0; g < groups.size(); g++)
-            for (int32_t v : *groups[g]) {
-                perm.push_back(v);
-                gid.push_back((int32_t)g);
-            }
+        for (size_t g = 0; g < groups.size(); g++) {
+            perm.insert(perm.end(), groups[g]->begin(), groups[g]->end());
+            gid.insert(gid.end(), groups[g]->size(), (int32_t)g);
+        }
         const int32_t len = (int32_t)(perm.size() - perm_off), m = (int32_t)groups.size();
         tg_gm_sub_t sd;
         sd.perm_off = perm_off;
         sd.len = len;
         sd.m = m;
         sd.out_off = out_off;
-        sd.tile_off = (int64_t)tiles.size();
+        sd.tile_off = (int64_t)(tp - tiles.data());
         subs.push_back(sd);
         for (int32_t i0 = 0; i0 < len; i0 += 64)
-            for (int32_t j0 = 0; j0 < len; j0 += 64) tiles.push_back({(int32_t)p, i0, j0});
+            for (int32_t j0 = 0; j0 < len; j0 += 64) *tp++ = {(int32_t)p, i0, j0};
         job.sizes.push_back(m);
         job.mat_off.push_back(out_off);
         out_off += (int64_t)m * m;
     }
+    HPROF("gl_host");
     const int64_t ntiles = (int64_t)tiles.size();
     const size_t ws_bytes = tg_group_max_workspace_bytes(cx.n, ntiles, cx.oracle->mode == 1 ? cx.oracle->H : 0);
     const size_t b_perm = tg_align_up(perm.size() * 4, 256), b_sub = tg_align_up(subs.size() * sizeof(tg_gm_sub_t), 256);
     const size_t b_tile = tg_align_up((size_t)ntiles * sizeof(tg_gm_tile_t), 256);
     const size_t b_out = tg_align_up((size_t)std::max<int64_t>(out_off, 1) * 8, 256);
     HC(job.gm_buf.alloc(2 * b_perm + b_sub + b_tile + b_out + ws_bytes, job.st));
+    HPROF("gl_alloc");
     char *base = job.gm_buf.as<char>();
     int32_t *d_perm = reinterpret_cast<int32_t *>(base);
     int32_t *d_gid = reinterpret_cast<int32_t *>(base + b_perm);
@@ -260,8 +275,10 @@ int launch_group_linkages(Ctx &cx, LinkJob &job, const std::vector<std::vector<c
     HC(cudaMemcpyAsync(d_gid, gid.data(), gid.size() * 4, cudaMemcpyHostToDevice, job.st));
     HC(cudaMemcpyAsync(d_sub, subs.data(), subs.size() * sizeof(tg_gm_sub_t), cudaMemcpyHostToDevice, job.st));
     HC(cudaMemcpyAsync(d_tile, tiles.data(), (size_t)ntiles * sizeof(tg_gm_tile_t), cudaMemcpyHostToDevice, job.st));
+    HPROF("gl_h2d");
     HR(tg_group_max_batch(cx.oracle, d_perm, d_gid, d_sub, (int64_t)subs.size(), d_tile, ntiles, d_out, out_off, d_ws,
                           ws_bytes, job.st));
+    HPROF("gl_gm");
     return launch_linkages(cx, job, d_out);
 }
 
@@ -273,6 +290,7 @@ int build(Ctx &cx, const int64_t *vb_dev, const int64_t *vc_dev, int64_t *lefts,
           int64_t *sizes_out, int64_t *n_merges) {
     const int64_t n = cx.n;
     std::vector<int64_t> vb(n), vc(n);
+    HPROF("t0");
     HC(cudaMemcpyAsync(vb.data(), vb_dev, n * 8, cudaMemcpyDeviceToHost, cx.st));
     HC(cudaMemcpyAsync(vc.data(), vc_dev, n * 8, cudaMemcpyDeviceToHost, cx.st));
     HC(cudaStreamSynchronize(cx.st));
@@ -289,57 +307,65 @@ int build(Ctx &cx, const int64_t *vb_dev, const int64_t *vc_dev, int64_t *lefts,
         if (!members[b].empty()) bubble_ids.push_back(b);
     std::vector<int64_t> group_root(nb, -1);
 
-    // ---- layer 1: complete linkage inside every bubble group (dbht.py:247-262)
+    // All three layers' device work is independent: layer 1 (bubble groups) reads oracle
+    // blocks, layers 2 and 3 read group maxima of the same oracle; only the record labels
+    // chain them (layer 2's handles are layer 1's roots, layer 3's are layer 2's).  So layer 1
+    // is launched on one side stream, layer 3 on another and layer 2 on the caller's stream,
+    // and they are collected in layer order, which keeps the record numbering unchanged.
     std::vector<Row> rows1, rows2, rows3;
-    {
-        std::vector<int64_t> multi;
-        for (int64_t b : bubble_ids) {
-            if (members[b].size() > 1) multi.push_back(b);
-            else group_root[b] = members[b][0];
+    SideStream side1, side3;   // destroyed after the jobs / buffers that free on them
+    std::vector<int64_t> multi;
+    for (int64_t b : bubble_ids) {
+        if (members[b].size() > 1) multi.push_back(b);
+        else group_root[b] = members[b][0];
+    }
+    DevBuf blocks_buf;
+    LinkJob j1, j2, j3;
+    static const bool l1_serial = std::getenv("TG_HIER_SERIAL") != nullptr;   // A/B switch
+    std::vector<std::vector<int64_t>> handles1(multi.size());
+    if (!multi.empty()) {   // ---- layer 1: complete linkage inside every bubble group (dbht.py:247-262)
+        HC(side1.open(cx.st));
+        HPROF("open1");
+        j1.st = side1.st;
+        const size_t cnt = multi.size();
+        std::vector<int32_t> perm;
+        std::vector<int64_t> gst(cnt + 1, 0), boff(cnt + 1, 0);
+        for (size_t k = 0; k < cnt; k++) {
+            const auto &mem = members[multi[k]];
+            const int64_t s = (int64_t)mem.size();
+            perm.insert(perm.end(), mem.begin(), mem.end());
+            gst[k + 1] = gst[k] + s;
+            boff[k + 1] = boff[k] + s * s;
+            j1.sizes.push_back(s);
+            j1.mat_off.push_back(boff[k]);
+            handles1[k].assign(mem.begin(), mem.end());
         }
-        if (!multi.empty()) {
-            const size_t cnt = multi.size();
-            std::vector<int32_t> perm;
-            std::vector<int64_t> gst(cnt + 1, 0), boff(cnt + 1, 0), sizes(cnt), mat_off(cnt);
-            std::vector<std::vector<int64_t>> handles(cnt);
-            for (size_t k = 0; k < cnt; k++) {
-                const auto &mem = members[multi[k]];
-                const int64_t s = (int64_t)mem.size();
-                perm.insert(perm.end(), mem.begin(), mem.end());
-                gst[k + 1] = gst[k] + s;
-                boff[k + 1] = boff[k] + s * s;
-                sizes[k] = s;
-                mat_off[k] = boff[k];
-                handles[k].assign(mem.begin(), mem.end());
-            }
-            const size_t b_perm = tg_align_up(perm.size() * 4, 256), b_idx = tg_align_up((cnt + 1) * 8, 256);
-            DevBuf buf;
-            HC(buf.alloc(b_perm + 2 * b_idx + (size_t)boff[cnt] * 8, cx.st));
-            char *base = buf.as<char>();
-            int32_t *d_perm = reinterpret_cast<int32_t *>(base);
-            int64_t *d_gst = reinterpret_cast<int64_t *>(base + b_perm);
-            int64_t *d_boff = reinterpret_cast<int64_t *>(base + b_perm + b_idx);
-            double *d_blocks = reinterpret_cast<double *>(base + b_perm + 2 * b_idx);
-            HC(cudaMemcpyAsync(d_perm, perm.data(), perm.size() * 4, cudaMemcpyHostToDevice, cx.st));
-            HC(cudaMemcpyAsync(d_gst, gst.data(), (cnt + 1) * 8, cudaMemcpyHostToDevice, cx.st));
-            HC(cudaMemcpyAsync(d_boff, boff.data(), (cnt + 1) * 8, cudaMemcpyHostToDevice, cx.st));
-            HR(tg_group_blocks(cx.oracle, d_perm, d_gst, (int64_t)cnt, d_boff, d_blocks, cx.st));
+        const size_t b_perm = tg_align_up(perm.size() * 4, 256), b_idx = tg_align_up((cnt + 1) * 8, 256);
+        HC(blocks_buf.alloc(b_perm + 2 * b_idx + (size_t)boff[cnt] * 8, j1.st));
+        char *base = blocks_buf.as<char>();
+        int32_t *d_perm = reinterpret_cast<int32_t *>(base);
+        int64_t *d_gst = reinterpret_cast<int64_t *>(base + b_perm);
+        int64_t *d_boff = reinterpret_cast<int64_t *>(base + b_perm + b_idx);
+        double *d_blocks = reinterpret_cast<double *>(base + b_perm + 2 * b_idx);
+        HC(cudaMemcpyAsync(d_perm, perm.data(), perm.size() * 4, cudaMemcpyHostToDevice, j1.st));
+        HC(cudaMemcpyAsync(d_gst, gst.data(), (cnt + 1) * 8, cudaMemcpyHostToDevice, j1.st));
+        HC(cudaMemcpyAsync(d_boff, boff.data(), (cnt + 1) * 8, cudaMemcpyHostToDevice, j1.st));
+        HR(tg_group_blocks(cx.oracle, d_perm, d_gst, (int64_t)cnt, d_boff, d_blocks, j1.st));
+        HR(launch_linkages(cx, j1, d_blocks));
+        if (l1_serial) {
             std::vector<int64_t> roots;
-            HR(run_linkages(cx, d_blocks, sizes, mat_off, handles, roots, rows1));
-            for (size_t k = 0; k < cnt; k++) group_root[multi[k]] = roots[k];
+            HR(collect_linkages(cx, j1, handles1, roots, rows1));
+            for (size_t k = 0; k < multi.size(); k++) group_root[multi[k]] = roots[k];
         }
-        stable_sort_rows(rows1);
     }
 
+    HPROF("tL1");
     // ---- layers 2 (bubbles inside each converging group, dbht.py:264-300) and 3 (converging
-    // groups against each other, dbht.py:302-324): their group maxima and linkages do not
-    // depend on each other -- only layer 3's record labels need layer 2's roots -- so both
-    // are launched (layer 3 on a side stream) before either is collected
+    // groups against each other, dbht.py:302-324)
     std::vector<int64_t> conv_ids;
     std::vector<std::vector<int64_t>> conv_bubbles;   // parallel to conv_ids
     std::vector<int64_t> conv_root;
     std::vector<std::vector<const std::vector<int32_t> *>> subproblems;
-    std::vector<std::vector<int64_t>> handles2;
     std::vector<size_t> which;
     {
         std::vector<std::pair<int64_t, int64_t>> cb;   // (conv id, bubble) in bubble order
@@ -357,18 +383,10 @@ int build(Ctx &cx, const int64_t *vb_dev, const int64_t *vc_dev, int64_t *lefts,
         }
         conv_root.assign(conv_ids.size(), -1);
         for (size_t c = 0; c < conv_ids.size(); c++) {
-            if (conv_bubbles[c].size() == 1) {
-                conv_root[c] = group_root[conv_bubbles[c][0]];
-                continue;
-            }
+            if (conv_bubbles[c].size() == 1) continue;
             std::vector<const std::vector<int32_t> *> groups;
-            std::vector<int64_t> hs;
-            for (int64_t b : conv_bubbles[c]) {
-                groups.push_back(&members[b]);
-                hs.push_back(group_root[b]);
-            }
+            for (int64_t b : conv_bubbles[c]) groups.push_back(&members[b]);
             subproblems.push_back(std::move(groups));
-            handles2.push_back(std::move(hs));
             which.push_back(c);
         }
     }
@@ -376,36 +394,53 @@ int build(Ctx &cx, const int64_t *vb_dev, const int64_t *vc_dev, int64_t *lefts,
     std::vector<std::vector<int32_t>> cmem(layer3 ? conv_ids.size() : 0);
     std::vector<const std::vector<int32_t> *> groups3;
     if (layer3) {
-        for (size_t c = 0; c < conv_ids.size(); c++) {
-            for (int64_t b : conv_bubbles[c]) cmem[c].insert(cmem[c].end(), members[b].begin(), members[b].end());
-            std::sort(cmem[c].begin(), cmem[c].end());
-            groups3.push_back(&cmem[c]);
-        }
+        // cmem[c] = the union of group c's bubble members, ascending: one pass over the
+        // vertices in id order (every vertex is in exactly one bubble) instead of a sort
+        std::vector<int32_t> conv_of_bubble(nb, -1);
+        for (size_t c = 0; c < conv_ids.size(); c++)
+            for (int64_t b : conv_bubbles[c]) conv_of_bubble[b] = (int32_t)c;
+        for (int64_t v = 0; v < n; v++) cmem[conv_of_bubble[vb[v]]].push_back((int32_t)v);
+        for (size_t c = 0; c < conv_ids.size(); c++) groups3.push_back(&cmem[c]);
+        HPROF("cmem");
+        HC(side3.open(cx.st));
+        HPROF("open3");
+        j3.st = side3.st;
+        HR(launch_group_linkages(cx, j3, {groups3}));
     }
-    SideStream side;
-    {
-        LinkJob j2, j3;
-        j2.st = cx.st;
-        if (layer3) {
-            HC(side.open(cx.st));
-            j3.st = side.st;
-            HR(launch_group_linkages(cx, j3, {groups3}));
+    HPROF("tL3");
+    j2.st = cx.st;
+    if (!subproblems.empty()) HR(launch_group_linkages(cx, j2, subproblems));
+
+    if (!multi.empty() && !l1_serial) {
+        std::vector<int64_t> roots;
+        HR(collect_linkages(cx, j1, handles1, roots, rows1));
+        for (size_t k = 0; k < multi.size(); k++) group_root[multi[k]] = roots[k];
+    }
+    HPROF("tC1");
+    stable_sort_rows(rows1);
+    for (size_t c = 0; c < conv_ids.size(); c++)
+        if (conv_bubbles[c].size() == 1) conv_root[c] = group_root[conv_bubbles[c][0]];
+    if (!subproblems.empty()) {
+        std::vector<std::vector<int64_t>> handles2;
+        for (size_t c : which) {
+            std::vector<int64_t> hs;
+            for (int64_t b : conv_bubbles[c]) hs.push_back(group_root[b]);
+            handles2.push_back(std::move(hs));
         }
-        if (!subproblems.empty()) HR(launch_group_linkages(cx, j2, subproblems));
-        if (!subproblems.empty()) {
-            std::vector<int64_t> roots;
-            HR(collect_linkages(cx, j2, handles2, roots, rows2));
-            for (size_t k = 0; k < which.size(); k++) conv_root[which[k]] = roots[k];
-        }
-        stable_sort_rows(rows2);
-        if (layer3) {
-            std::vector<int64_t> hs, roots;
-            for (size_t c = 0; c < conv_ids.size(); c++) hs.push_back(conv_root[c]);
-            HR(collect_linkages(cx, j3, {hs}, roots, rows3));
-            stable_sort_rows(rows3);
-        }
+        std::vector<int64_t> roots;
+        HR(collect_linkages(cx, j2, handles2, roots, rows2));
+        for (size_t k = 0; k < which.size(); k++) conv_root[which[k]] = roots[k];
+    }
+    HPROF("tC2");
+    stable_sort_rows(rows2);
+    if (layer3) {
+        std::vector<int64_t> hs, roots;
+        for (size_t c = 0; c < conv_ids.size(); c++) hs.push_back(conv_root[c]);
+        HR(collect_linkages(cx, j3, {hs}, roots, rows3));
+        stable_sort_rows(rows3);
     }
 
+    HPROF("tC3");
     // ---- emission with the running height floor (dbht.py:326-339) + sizes (linkage.py:136-148)
     const int64_t nrec = (int64_t)cx.records.size();
     std::vector<int64_t> final_id(n + nrec);
@@ -432,6 +467,7 @@ int build(Ctx &cx, const int64_t *vb_dev, const int64_t *vc_dev, int64_t *lefts,
         }
     }
     *n_merges = k;
+    HPROF("emit");
     return TG_OK;
 }
 
