@@ -309,9 +309,9 @@ int build(Ctx &cx, const int64_t *vb_dev, const int64_t *vc_dev, int64_t *lefts,
 
     // All three layers' device work is independent: layer 1 (bubble groups) reads oracle
     // blocks, layers 2 and 3 read group maxima of the same oracle; only the record labels
-    // chain them (layer 2's handles are layer 1's roots, layer 3's are layer 2's).  So layer 1
-    // is launched on one side stream, layer 3 on another and layer 2 on the caller's stream,
-    // and they are collected in layer order, which keeps the record numbering unchanged.
+    // chain them (layer 2's handles are layer 1's roots, layer 3's are layer 2's).  So layer 3
+    // is launched on one side stream, layer 2 on the caller's stream and layer 1 on another
+    // side stream, and they are collected in layer order (record numbering unchanged).
     std::vector<Row> rows1, rows2, rows3;
     SideStream side1, side3;   // destroyed after the jobs / buffers that free on them
     std::vector<int64_t> multi;
@@ -323,42 +323,6 @@ int build(Ctx &cx, const int64_t *vb_dev, const int64_t *vc_dev, int64_t *lefts,
     LinkJob j1, j2, j3;
     static const bool l1_serial = std::getenv("TG_HIER_SERIAL") != nullptr;   // A/B switch
     std::vector<std::vector<int64_t>> handles1(multi.size());
-    if (!multi.empty()) {   // ---- layer 1: complete linkage inside every bubble group (dbht.py:247-262)
-        HC(side1.open(cx.st));
-        HPROF("open1");
-        j1.st = side1.st;
-        const size_t cnt = multi.size();
-        std::vector<int32_t> perm;
-        std::vector<int64_t> gst(cnt + 1, 0), boff(cnt + 1, 0);
-        for (size_t k = 0; k < cnt; k++) {
-            const auto &mem = members[multi[k]];
-            const int64_t s = (int64_t)mem.size();
-            perm.insert(perm.end(), mem.begin(), mem.end());
-            gst[k + 1] = gst[k] + s;
-            boff[k + 1] = boff[k] + s * s;
-            j1.sizes.push_back(s);
-            j1.mat_off.push_back(boff[k]);
-            handles1[k].assign(mem.begin(), mem.end());
-        }
-        const size_t b_perm = tg_align_up(perm.size() * 4, 256), b_idx = tg_align_up((cnt + 1) * 8, 256);
-        HC(blocks_buf.alloc(b_perm + 2 * b_idx + (size_t)boff[cnt] * 8, j1.st));
-        char *base = blocks_buf.as<char>();
-        int32_t *d_perm = reinterpret_cast<int32_t *>(base);
-        int64_t *d_gst = reinterpret_cast<int64_t *>(base + b_perm);
-        int64_t *d_boff = reinterpret_cast<int64_t *>(base + b_perm + b_idx);
-        double *d_blocks = reinterpret_cast<double *>(base + b_perm + 2 * b_idx);
-        HC(cudaMemcpyAsync(d_perm, perm.data(), perm.size() * 4, cudaMemcpyHostToDevice, j1.st));
-        HC(cudaMemcpyAsync(d_gst, gst.data(), (cnt + 1) * 8, cudaMemcpyHostToDevice, j1.st));
-        HC(cudaMemcpyAsync(d_boff, boff.data(), (cnt + 1) * 8, cudaMemcpyHostToDevice, j1.st));
-        HR(tg_group_blocks(cx.oracle, d_perm, d_gst, (int64_t)cnt, d_boff, d_blocks, j1.st));
-        HR(launch_linkages(cx, j1, d_blocks));
-        if (l1_serial) {
-            std::vector<int64_t> roots;
-            HR(collect_linkages(cx, j1, handles1, roots, rows1));
-            for (size_t k = 0; k < multi.size(); k++) group_root[multi[k]] = roots[k];
-        }
-    }
-
     HPROF("tL1");
     // ---- layers 2 (bubbles inside each converging group, dbht.py:264-300) and 3 (converging
     // groups against each other, dbht.py:302-324)
@@ -410,6 +374,44 @@ int build(Ctx &cx, const int64_t *vb_dev, const int64_t *vc_dev, int64_t *lefts,
     HPROF("tL3");
     j2.st = cx.st;
     if (!subproblems.empty()) HR(launch_group_linkages(cx, j2, subproblems));
+    // layer 1 last: its linkages are never the critical path (layer 2 is at n = 10k, layer 3
+    // at n = 50k), so its host preparation overlaps their device work
+    if (!multi.empty()) {   // ---- layer 1: complete linkage inside every bubble group (dbht.py:247-262)
+        HC(side1.open(cx.st));
+        HPROF("open1");
+        j1.st = side1.st;
+        const size_t cnt = multi.size();
+        std::vector<int32_t> perm;
+        std::vector<int64_t> gst(cnt + 1, 0), boff(cnt + 1, 0);
+        for (size_t k = 0; k < cnt; k++) {
+            const auto &mem = members[multi[k]];
+            const int64_t s = (int64_t)mem.size();
+            perm.insert(perm.end(), mem.begin(), mem.end());
+            gst[k + 1] = gst[k] + s;
+            boff[k + 1] = boff[k] + s * s;
+            j1.sizes.push_back(s);
+            j1.mat_off.push_back(boff[k]);
+            handles1[k].assign(mem.begin(), mem.end());
+        }
+        const size_t b_perm = tg_align_up(perm.size() * 4, 256), b_idx = tg_align_up((cnt + 1) * 8, 256);
+        HC(blocks_buf.alloc(b_perm + 2 * b_idx + (size_t)boff[cnt] * 8, j1.st));
+        char *base = blocks_buf.as<char>();
+        int32_t *d_perm = reinterpret_cast<int32_t *>(base);
+        int64_t *d_gst = reinterpret_cast<int64_t *>(base + b_perm);
+        int64_t *d_boff = reinterpret_cast<int64_t *>(base + b_perm + b_idx);
+        double *d_blocks = reinterpret_cast<double *>(base + b_perm + 2 * b_idx);
+        HC(cudaMemcpyAsync(d_perm, perm.data(), perm.size() * 4, cudaMemcpyHostToDevice, j1.st));
+        HC(cudaMemcpyAsync(d_gst, gst.data(), (cnt + 1) * 8, cudaMemcpyHostToDevice, j1.st));
+        HC(cudaMemcpyAsync(d_boff, boff.data(), (cnt + 1) * 8, cudaMemcpyHostToDevice, j1.st));
+        HR(tg_group_blocks(cx.oracle, d_perm, d_gst, (int64_t)cnt, d_boff, d_blocks, j1.st));
+        HR(launch_linkages(cx, j1, d_blocks));
+        if (l1_serial) {
+            std::vector<int64_t> roots;
+            HR(collect_linkages(cx, j1, handles1, roots, rows1));
+            for (size_t k = 0; k < multi.size(); k++) group_root[multi[k]] = roots[k];
+        }
+    }
+
 
     if (!multi.empty() && !l1_serial) {
         std::vector<int64_t> roots;
