@@ -70,13 +70,22 @@ _INSTALL_MAP = {
 }
 
 
+# reference module -> exception classes this package raises that the reference's callers catch
+# (tmfg.py:67-68 TraceError, simmatrix.py:18-19 DataError); install() makes this package raise
+# the reference's own classes so ``except tmfgclust.tmfg.TraceError`` keeps working.
+_EXCEPTIONS = {
+    "TraceError": ("tmfg", ["tmfg", "dbht"]),
+    "DataError": ("simmatrix", ["simmatrix", "tmfg"]),
+}
+
+
 def install(package=None) -> dict:
     """Route the reference package's hot path through this package.
 
     Rebinds the stage functions on the reference modules (and its top-level
-    re-exports).  The exact / corr TMFG builders stay the reference's own
-    (``tmfg.build_tmfg`` dispatches to ``build_tmfg_heap`` by module lookup).
-    Returns the replaced originals so ``uninstall(originals)`` can restore them.
+    re-exports), and points this package's raise sites at the reference's
+    exception classes.  Returns the replaced originals so
+    ``uninstall(originals)`` can restore them.
     """
     import importlib
     import sys
@@ -92,6 +101,12 @@ def install(package=None) -> dict:
             if hasattr(pkg, name):
                 saved[(pkg.__name__, name)] = getattr(pkg, name)
                 setattr(pkg, name, getattr(this, name))
+    for exc, (ref_mod, ours) in _EXCEPTIONS.items():
+        ref_cls = getattr(importlib.import_module(f"{pkg.__name__}.{ref_mod}"), exc)
+        for m in ours:
+            mod = importlib.import_module(f"{__name__}.{m}")
+            saved[(mod.__name__, exc)] = getattr(mod, exc)
+            setattr(mod, exc, ref_cls)
     return saved
 
 

@@ -1,17 +1,16 @@
 """Device-memory plumbing: torch owns HBM buffers and streams; kernels live in the .so.
 
 * ``to_device`` moves a host array (or passes a CUDA tensor through).
-* ``device_matrix`` keeps a single-slot identity cache of the last host matrix
-  uploaded, so the drop-in stage functions called one after another on the same
-  numpy ``S`` (as the reference pipeline does, pipeline.py:191-218) copy it to
-  HBM once.
-* ``Workspace`` hands out reusable scratch for the C ABI's ``ws`` arguments.
+* ``device_matrix`` uploads a host matrix (no cross-call cache: an in-place edit
+  of S between drop-in stage calls is always seen); ``chained_device`` reuses the
+  device S a previous stage result carries only when the caller passes that
+  same CUDA tensor.
+* ``Workspace`` hands out reusable scratch for the C ABI's ``ws`` arguments,
+  one buffer per (device, stream).
 * ``LazyHost`` materialises a host numpy view of a device tensor on first use.
 """
 
 from __future__ import annotations
-
-import weakref
 
 import numpy as np
 
@@ -50,57 +49,58 @@ def to_host(x) -> np.ndarray:
     return np.asarray(x)
 
 
-def _fingerprint(S: np.ndarray) -> tuple:
-    flat = S.reshape(-1)
-    step = max(1, flat.shape[0] // 4096)
-    sample = flat[::step]
-    return (S.shape, S.dtype.str, S.__array_interface__["data"][0], float(np.nansum(sample)),
-            int(np.isnan(sample).sum()))
-
-
-class _MatrixCache:
-    ref = None
-    fp = None
-    dev = None
-
-
 def device_matrix(S):
-    """float64 CUDA tensor for S; host arrays are uploaded once per object."""
+    """float64 CUDA tensor for S.
+
+    A CUDA tensor passes through; a host array is uploaded on every call, so a
+    drop-in stage always sees the matrix's current contents (the reference
+    re-reads S in every stage; an in-place edit between stage calls must not
+    leave a stale device copy).  Stages chained by this package pass the device
+    tensor along (``lists.S_device``, ``graph.S_device``) and upload once.
+    """
     t = torch()
     if isinstance(S, t.Tensor):
         return to_device(S, t.float64)
-    S = np.asarray(S)
-    if _MatrixCache.ref is not None and _MatrixCache.ref() is S and _MatrixCache.fp == _fingerprint(S):
-        return _MatrixCache.dev
-    dev = to_device(np.ascontiguousarray(S, dtype=np.float64), t.float64)
-    try:
-        _MatrixCache.ref = weakref.ref(S)
-        _MatrixCache.fp = _fingerprint(S)
-        _MatrixCache.dev = dev
-    except TypeError:  # pragma: no cover - non-weakrefable
-        _MatrixCache.ref = None
-    return dev
+    return to_device(np.asarray(S, dtype=np.float64), t.float64)
 
 
-def forget_cached_matrix() -> None:
-    _MatrixCache.ref = None
-    _MatrixCache.fp = None
-    _MatrixCache.dev = None
+def chained_device(obj, S):
+    """The device S carried by a previous stage's result when it IS the caller's S.
+
+    Only a CUDA tensor identical to the one the chain was built on is reused;
+    for a host array the caller's current contents are uploaded again.
+    """
+    Sd = getattr(obj, "S_device", None) if obj is not None else None
+    if Sd is not None and is_device(S) and S is Sd:
+        return Sd
+    return device_matrix(S)
 
 
 class Workspace:
-    """Grow-only scratch buffer reused by consecutive stream-ordered calls."""
+    """Grow-only scratch buffers, one per (device, stream).
 
-    _buf = None
+    Calls on one stream are ordered, so they may share a buffer; calls on
+    different streams get different buffers.
+    """
+
+    _bufs: dict = {}
 
     @classmethod
-    def get(cls, nbytes: int):
+    def get(cls, nbytes: int, stream=None):
         t = torch()
         nbytes = max(int(nbytes), 256)
-        if cls._buf is None or cls._buf.numel() < nbytes:
-            cls._buf = None
-            cls._buf = t.empty(nbytes, dtype=t.uint8, device="cuda")
-        return cls._buf
+        s = stream if stream is not None else t.cuda.current_stream()
+        key = (s.device.index if s.device.index is not None else t.cuda.current_device(), s.cuda_stream)
+        buf = cls._bufs.get(key)
+        if buf is None or buf.numel() < nbytes:
+            cls._bufs.pop(key, None)
+            buf = t.empty(nbytes, dtype=t.uint8, device=s.device)
+            cls._bufs[key] = buf
+        return buf
+
+    @classmethod
+    def release(cls) -> None:
+        cls._bufs.clear()
 
 
 def empty(shape, dtype):

@@ -225,9 +225,7 @@ def to_weighted_device(Sd, edges_dev, n: int):
 def to_weighted(graph, S) -> WeightedTmfg:
     """Attach lengths sqrt(2(1 - S[i,j])) to every TMFG edge (apsp.py:52-77)."""
     n = int(graph.n)
-    Sd = getattr(graph, "S_device", None)
-    if Sd is None or getattr(graph, "_S_host", None) is not S:
-        Sd = D.device_matrix(S)
+    Sd = D.chained_device(graph, S)
     t = D.torch()
     if hasattr(graph, "device"):
         edges = graph.device("edges")

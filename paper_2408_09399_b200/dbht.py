@@ -73,10 +73,7 @@ class BubbleAssignment:
 
 
 def _S_for(obj, S):
-    Sd = getattr(obj, "S_device", None)
-    if Sd is not None and getattr(obj, "_S_host", None) is S:
-        return Sd
-    return D.device_matrix(S)
+    return D.chained_device(obj, S)
 
 
 def build_bubble_tree(graph) -> BubbleTree:

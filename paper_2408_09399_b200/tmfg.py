@@ -198,14 +198,11 @@ def build_tmfg_heap(S, lists: SortedNeighborLists | None = None, config: BuildCo
         raise DataError(f"similarity matrix must be square, got shape {shape}")
     if not D.is_device(S):
         S = np.asarray(S, dtype=np.float64)
-    Sd = None
-    if lists is not None and getattr(lists, "S_device", None) is not None and lists.S is S:
-        Sd = lists.S_device
-    if Sd is None:
-        Sd = D.device_matrix(S)
+    Sd = D.chained_device(lists, S)
     validate_device(Sd)
     n = shape[0]
-    screen = getattr(lists, "screen_device", None) if lists is not None and lists.S is S else None
+    # the sort's fused row-sum screen is only valid for the very device S it was computed on
+    screen = getattr(lists, "screen_device", None) if getattr(lists, "S_device", None) is Sd else None
     if lists is None:
         order_dev, screen = sort_rows_device(Sd, with_screen=True)
     elif isinstance(lists, SortedNeighborLists):
