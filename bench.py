@@ -236,10 +236,14 @@ def run_b200(args, world, rank, local):
     hbm_peak, peak_kind = _peaks()
     achieved = sort_bytes / (sort_avg * 1e-3) / 1e9
     traffic = None
-    tp = REPO / "profiles" / "round1_sort_traffic.json"
+    traffic_src = None
+    tp = REPO / "profiles" / "sort_traffic.json"   # ncu --set full capture of the CURRENT sort kernel
     if tp.exists():
         try:
-            traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
+            tj = json.loads(tp.read_text())
+            if int(tj.get("n", n)) == n:
+                traffic = tj.get("dram_bytes_per_launch")
+                traffic_src = tj.get("kernel")
         except Exception:
             traffic = None
     # fp64 similarity (secondary kernel)
@@ -272,6 +276,7 @@ def run_b200(args, world, rank, local):
         x5, _ = synth.generate(5)
         X5 = torch.from_numpy(x5).to(device)
         st5 = {}
+        passes = []
         for rep_i in range(3):   # pass 1 warms up
             flush.zero_()
             torch.cuda.synchronize()
@@ -287,13 +292,16 @@ def run_b200(args, world, rank, local):
             st5 = {kk: round(v * 1e3, 2) for kk, v in rep5.stage_seconds.items()}
             st5["similarity"] = round(a.elapsed_time(a2), 2)
             ms5 = round(a.elapsed_time(b), 1)
-            # passes after the first: the fastest is reported (allocator / pool state from the
-            # n = 10k runs occasionally lands a cudaMalloc or cudaFree inside one stage)
-            if rep_i > 0 and (big is None or ms5 < big["ms"]):
-                big = {"workload": "BASELINE config 5: n=50000, L=256, hub APSP, heap TMFG", "ms": ms5,
-                       "stage_ms": st5, "passes": "best of passes 2-3 (pass 1 = warm-up)"}
+            if rep_i > 0:
+                passes.append((ms5, st5))
             del S5
             torch.cuda.empty_cache()
+        stage_names = passes[0][1].keys()
+        big = {"workload": "BASELINE config 5: n=50000, L=256, hub APSP, heap TMFG",
+               "ms": round(float(np.mean([p[0] for p in passes])), 1),
+               "ms_passes": [p[0] for p in passes],
+               "stage_ms": {kk: round(float(np.mean([p[1][kk] for p in passes])), 2) for kk in stage_names},
+               "passes": "mean of passes 2-3 (pass 1 = warm-up)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -304,13 +312,11 @@ def run_b200(args, world, rank, local):
             "metric": METRIC, "value": round(ms_max, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_max, 3), "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"BASELINE config {cfg}: n={n} series, L={L}, {mode} APSP, heap TMFG",
-                       "n": n, "L": L, "apsp": mode, "k": k, "parallelism": f"replicas{world}",
-                       "l2": "flushed (256 MB write) between timed steps; S (8n^2 B) exceeds L2"},
+            "config": workload_config(cfg, n, L, mode, k),
             "stage_ms": {kk: round(float(np.mean(vv)), 3) for kk, vv in stage.items()},
             "roofline": {"bound": "hbm", "kernel": "row_sort_fk_kernel (per-row neighbour sort)",
                          "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                         "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
+                         "frac": round(achieved / hbm_peak, 4), "traffic": traffic, "traffic_kernel": traffic_src,
                          "algorithmic_bytes": sort_bytes, "kernel_ms": round(sort_avg, 4),
                          "gkeys_per_s": round(n * (n - 1) / (sort_avg * 1e-3) / 1e9, 2),
                          "peak_kind": peak_kind},
@@ -346,13 +352,92 @@ def cpu_baseline_sample(cfg, n_override=None) -> dict:
     dt = (time.perf_counter() - t0) * 1e3
     return {"value": round(dt, 1), "unit": UNIT, "cores": orc.num_threads(), "kind": "port",
             "sample": f"one full step (Pearson + sort + heap TMFG + {mode} APSP + DBHT + cut) of config {cfg}, "
-                      f"n={x.shape[0]}, C/OpenMP + numpy oracle"}
+                      f"n={x.shape[0]}, C/OpenMP + numpy oracle", "host": host_info()}
 
 
 # ------------------------------------------------------------------ reference arm
+def host_info() -> dict:
+    """CPU model, logical cores and RAM of the host the CPU baselines run on."""
+    model = None
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    ram = None
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemTotal:"):
+                    ram = round(int(line.split()[1]) / 1024 ** 2, 1)
+                    break
+    except Exception:
+        pass
+    return {"cpu_model": model, "logical_cores": os.cpu_count(), "ram_gib": ram}
+
+
+def workload_config(cfg: int, n: int, L: int, mode: str, k: int) -> dict:
+    """The config dict both arms print (identical keys and values for the same workload)."""
+    return {"workload": f"BASELINE config {cfg}: n={n} series, L={L}, {mode} APSP, heap TMFG",
+            "n": n, "L": L, "apsp": mode, "k": k, "parallelism": "replicas",
+            "l2": "flushed (256 MB write) between timed GPU steps; S (8n^2 B) exceeds L2"}
+
+
+def _python_reference_once(cfg: int, n_override=None) -> dict | None:
+    """The unmodified reference package (baseline/_ref, Python + numba) on this host, one step.
+
+    Runs in a child process (numba threads = all cores) so its JIT and thread pool never
+    share the bench process.  Warm-up: one call of every kernel at n = 64 (JIT excluded).
+    """
+    ref = REPO / "baseline" / "_ref"
+    if not (ref / "tmfgclust").is_dir():
+        return None
+    code = f"""
+import json, sys, time
+sys.path.insert(0, {str(ref)!r}); sys.path.insert(0, {str(REPO)!r})
+import numpy as np, tmfgclust as tc
+from tmfgclust.pipeline import PipelineConfig, run_stages
+from paper_2408_09399_b200 import synth
+xs, ls = synth.generate(1, n=64)
+ds = tc.Dataset(labels=ls, series=xs)
+Ss = tc.pearson_similarity(ds)
+run_stages(PipelineConfig(apsp_mode='exact', k=3), Ss, ls)
+run_stages(PipelineConfig(apsp_mode='hub', k=3), Ss, ls)
+x, labels = synth.generate({cfg}, n={n_override!r})
+t0 = time.perf_counter()
+S = tc.pearson_similarity(tc.Dataset(labels=labels, series=x))
+sim = time.perf_counter() - t0
+mode = 'hub' if {cfg} in (3, 5) else 'exact'
+rep, *_ = run_stages(PipelineConfig(apsp_mode=mode, k=synth.num_clusters({cfg})), S, labels)
+print(json.dumps({{"similarity_s": sim, "stage_seconds": rep.stage_seconds, "digest": rep.digest,
+                  "total_s": sim + sum(rep.stage_seconds.values())}}))
+"""
+    env = dict(os.environ)
+    env.setdefault("NUMBA_CACHE_DIR", "/tmp/tg_numba_cache")
+    env["PYTHONDONTWRITEBYTECODE"] = "1"
+    try:
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=900, env=env)
+        rows = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+        if not rows:
+            return {"error": (r.stderr or r.stdout)[-300:]}
+        d = json.loads(rows[-1])
+        return {"ms": round(d["total_s"] * 1e3, 1),
+                "stage_ms": {k: round(v * 1e3, 1) for k, v in d["stage_seconds"].items()},
+                "similarity_ms": round(d["similarity_s"] * 1e3, 1), "digest": d["digest"],
+                "kind": "reference (unmodified tmfgclust, Python + numba, all cores)", "steps": 1}
+    except Exception as e:  # pragma: no cover
+        return {"error": str(e)[:300]}
+
+
 def run_reference(args, world, rank):
-    """The reference's CPU path, restated by the oracle (the reference itself is a
-    Python package that is not installed on the GPU box), on all host threads."""
+    """The reference's CPU path on all host threads.
+
+    ``value``: the oracle port (C/OpenMP + numpy restatement of the reference, outputs
+    bit-identical to it), K full steps after W full-size warm-up steps.  Beside it, once:
+    the unmodified Python reference (baseline/_ref, numba) on the same workload.
+    """
     if world > 1 and rank != 0:
         return
     from oracle import oracle as orc
@@ -360,31 +445,37 @@ def run_reference(args, world, rank):
 
     cfg = args.config
     x, labels = synth.generate(cfg, n=args.n)
+    n, L = x.shape
     k = synth.num_clusters(cfg)
     mode = "hub" if cfg in (3, 5) else args.apsp
     orc.set_threads(os.cpu_count() or 1)
-    xs, _ = synth.generate(1, n=200)
-    for _ in range(max(args.warmup, 0)):
-        Ss = orc.pearson_similarity(xs)
-        orc.run_stages(Ss, 5, mode)
-    times = []
-    steps = max(1, min(args.steps, 5))
-    for _ in range(steps):
+    for _ in range(max(args.warmup, 0)):   # full-size warm-up: S and the sort buffers first-touched
+        orc.run_stages(orc.pearson_similarity(x), k, mode)
+    times, stages = [], {}
+    for _ in range(max(args.steps, 1)):
         t0 = time.perf_counter()
         S = orc.pearson_similarity(x)
-        orc.run_stages(S, k, mode)
+        t1 = time.perf_counter()
+        r = orc.run_stages(S, k, mode)
         times.append((time.perf_counter() - t0) * 1e3)
+        stages.setdefault("similarity", []).append((t1 - t0) * 1e3)
+        for kk, vv in r["seconds"].items():
+            stages.setdefault(kk, []).append(vv * 1e3)
+        del S
     v = float(np.mean(times))
+    py_ref = None if args.no_python_reference else _python_reference_once(cfg, args.n)
     line = {
-        "metric": METRIC, "value": round(v, 1), "unit": UNIT, "n_gpus": world, "steps": steps,
+        "metric": METRIC, "value": round(v, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(v, 1), "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-        "config": {"workload": f"BASELINE config {cfg}: n={x.shape[0]} series, L={x.shape[1]}, {mode} APSP, "
-                               "heap TMFG", "n": int(x.shape[0]), "L": int(x.shape[1]), "apsp": mode, "k": k,
-                   "parallelism": "host threads"},
+        "config": workload_config(cfg, int(n), int(L), mode, k),
+        "stage_ms": {kk: round(float(np.mean(vv)), 1) for kk, vv in stages.items()},
         "cpu_baseline": {"value": round(v, 1), "unit": UNIT, "cores": orc.num_threads(), "kind": "port",
-                         "sample": f"{steps} full steps of config {cfg} (C/OpenMP + numpy restatement of the "
-                                   "reference, bit-identical outputs)"},
+                         "sample": f"{len(times)} full steps of config {cfg} (Pearson + sort + heap TMFG + {mode} "
+                                   "APSP + DBHT + cut; C/OpenMP + numpy restatement of the reference, outputs "
+                                   "bit-identical to it) after full-size warm-up",
+                         "host": host_info()},
+        "python_reference": py_ref,
         "e2e": {"value": round(v, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -401,6 +492,8 @@ def main():
     ap.add_argument("--apsp", default="hub", choices=["exact", "hub"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-50k", action="store_true", help="skip the config-5 (n=50k) side measurement")
+    ap.add_argument("--no-python-reference", action="store_true",
+                    help="reference arm: skip the one-step timing of the unmodified Python reference")
     args = ap.parse_args()
     world, rank, local = dist_setup()
     if args.impl == "reference":

@@ -230,9 +230,10 @@ typedef struct {
 /* H: the hub count of a hub-mode oracle (0 in exact mode); the workspace holds the
  * permuted vertex-major fp32/fp64 copies of hub_dist used by the hub-mode tiles. */
 size_t tg_group_max_workspace_bytes(int64_t n, int64_t ntiles, int64_t H);
-int tg_group_max_batch(const tg_oracle_t *oracle, const int32_t *perm, const int32_t *gid, const void *subs,
-                       int64_t nsub, const void *tiles, int64_t ntiles, double *out, int64_t out_len, void *ws,
-                       size_t ws_bytes, void *stream);
+/* total_len: the number of perm / gid entries (the sub-problems lie back to back). */
+int tg_group_max_batch(const tg_oracle_t *oracle, const int32_t *perm, const int32_t *gid, int64_t total_len,
+                       const void *subs, int64_t nsub, const void *tiles, int64_t ntiles, double *out, int64_t out_len,
+                       void *ws, size_t ws_bytes, void *stream);
 
 /* linkage.py:50-94 _nn_chain over a batch of dense matrices (matrix b: sizes[b]
  * x sizes[b] at mats + mat_offsets[b]; it is overwritten as the working copy).
@@ -249,10 +250,15 @@ int tg_nn_chain_batch(double *mats, const int64_t *mat_offsets, const int64_t *s
  * vertex_converging are DEVICE arrays (n); the dendrogram rows are written to
  * HOST arrays of n-1 entries (lefts, rights, heights, sizes) and *n_merges_out.
  * Host-orchestrated (a few stream synchronisations); the oracle blocks, group
- * maxima and NN-chains run on the GPU. */
+ * maxima and NN-chains run on the GPU.  Scratch comes from a memory pool owned by
+ * the library (one per device, up to 16 GiB kept cached between calls; the
+ * process's default pool is not touched). */
 int tg_build_hierarchy(const tg_oracle_t *oracle, const int64_t *vertex_bubble, const int64_t *vertex_converging,
                        int64_t n, int64_t *lefts_out, int64_t *rights_out, double *heights_out, int64_t *sizes_out,
                        int64_t *n_merges_out, void *stream);
+
+/* Trim the library's hierarchy pool to zero (returns its cached memory to the device). */
+int tg_release_cached_memory(void);
 
 /* linkage.py:181-187 serialize_dendrogram (HOST arrays): "left right height size\n"
  * per merge, height as %.17g (== Python "{:.17g}").  Needed length in *len_out;

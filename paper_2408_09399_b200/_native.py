@@ -97,10 +97,11 @@ _PROTOS = {
     "tg_group_blocks": (ctypes.c_int, [ctypes.POINTER(TgOracle), c_p, c_p, c_i64, c_p, c_p, c_p]),
     "tg_oracle_block": (ctypes.c_int, [ctypes.POINTER(TgOracle), c_p, c_i64, c_p, c_i64, ctypes.c_int32, c_p, c_p]),
     "tg_group_max_workspace_bytes": (c_sz, [c_i64, c_i64, c_i64]),
-    "tg_group_max_batch": (ctypes.c_int, [ctypes.POINTER(TgOracle), c_p, c_p, c_p, c_i64, c_p, c_i64, c_p, c_i64,
-                                          c_p, c_sz, c_p]),
+    "tg_group_max_batch": (ctypes.c_int, [ctypes.POINTER(TgOracle), c_p, c_p, c_i64, c_p, c_i64, c_p, c_i64, c_p,
+                                          c_i64, c_p, c_sz, c_p]),
     "tg_nn_chain_batch": (ctypes.c_int, [c_p, c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p]),
     "tg_serialize_dendrogram": (ctypes.c_int, [c_p, c_p, c_p, c_p, c_i64, c_p, c_sz, ctypes.POINTER(c_sz)]),
+    "tg_release_cached_memory": (ctypes.c_int, []),
     "tg_build_hierarchy": (ctypes.c_int, [ctypes.POINTER(TgOracle), c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_p]),
 }
 

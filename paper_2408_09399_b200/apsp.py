@@ -235,6 +235,33 @@ def to_weighted(graph, S) -> WeightedTmfg:
     return WeightedTmfg(n=n, indptr=indptr, neighbors=nbr, lengths=lens, strength=strength)
 
 
+def as_weighted(g) -> WeightedTmfg:
+    """This package's WeightedTmfg for ``g``: passes ours through, converts a foreign one.
+
+    The reference's own ``WeightedTmfg`` (apsp.py:23-35, host arrays, e.g. built by a
+    caller or a test) is accepted wherever the reference accepts it; its CSR is
+    uploaded on this call.
+    """
+    if isinstance(g, WeightedTmfg):
+        return g
+    return WeightedTmfg(n=g.n, indptr=g.indptr, neighbors=g.neighbors, lengths=g.lengths, strength=g.strength)
+
+
+def as_oracle(o):
+    """This package's ExactOracle / HubOracle for ``o`` (a foreign reference oracle is converted).
+
+    The caller keeps the returned object alive while raw device pointers from it are in use.
+    """
+    if isinstance(o, (ExactOracle, HubOracle)):
+        return o
+    if getattr(o, "mode", None) == "exact":
+        return ExactOracle(np.asarray(o.matrix, dtype=np.float64))
+    if getattr(o, "mode", None) == "hub":
+        return HubOracle(hubs=o.hubs, hub_dist=o.hub_dist, nearest_hub=o.nearest_hub, nearest_dist=o.nearest_dist,
+                         radii=o.radii, near_indptr=o.near_indptr, near_ids=o.near_ids, near_dist=o.near_dist)
+    raise TypeError(f"not a distance oracle: {type(o).__name__}")
+
+
 def sssp_rows_device(w: WeightedTmfg, sources_dev):
     t = D.torch()
     ip, nb, ln = w.device_csr()
@@ -248,6 +275,7 @@ def sssp_rows_device(w: WeightedTmfg, sources_dev):
 
 def apsp_exact(g: WeightedTmfg, workers: int | None = None) -> ExactOracle:
     """One search per vertex (apsp.py:164-171); ``workers`` is ignored."""
+    g = as_weighted(g)
     t = D.torch()
     src = t.arange(g.n, dtype=t.int64, device="cuda")
     return ExactOracle(sssp_rows_device(g, src))
@@ -268,11 +296,13 @@ def select_hubs_device(g: WeightedTmfg, hub_count: int):
 
 def select_hubs(g: WeightedTmfg, hub_count: int) -> np.ndarray:
     """The hub_count vertices of highest strength, (strength desc, id asc) (apsp.py:178-186)."""
+    g = as_weighted(g)
     return select_hubs_device(g, hub_count).cpu().numpy().astype(np.int64)
 
 
 def apsp_hub(g: WeightedTmfg, params: ApspParams | None = None, workers: int | None = None) -> HubOracle:
     """Hub rows, nearest-hub radii and per-vertex truncated searches (apsp.py:189-230)."""
+    g = as_weighted(g)
     params = params or ApspParams()
     hub_count = params.hub_count or default_hub_count(g.n)
     if hub_count > g.n:

@@ -1015,10 +1015,10 @@ TG_API size_t tg_group_max_workspace_bytes(int64_t n, int64_t ntiles, int64_t H)
            tg_align_up((size_t)n * Hp * 4, 256) + tg_align_up((size_t)n * Hp * 8, 256) + 1024;
 }
 
-TG_API int tg_group_max_batch(const tg_oracle_t *o, const int32_t *perm, const int32_t *gid, const void *subs_v,
-                              int64_t nsub, const void *tiles_v, int64_t ntiles, double *out, int64_t out_len,
-                              void *ws, size_t ws_bytes, void *stream) {
-    if (!o || !perm || !gid || !subs_v || !tiles_v || !out || nsub < 0 || ntiles < 0) return TG_ERR_ARG;
+TG_API int tg_group_max_batch(const tg_oracle_t *o, const int32_t *perm, const int32_t *gid, int64_t total_len,
+                              const void *subs_v, int64_t nsub, const void *tiles_v, int64_t ntiles, double *out,
+                              int64_t out_len, void *ws, size_t ws_bytes, void *stream) {
+    if (!o || !perm || !gid || !subs_v || !tiles_v || !out || nsub < 0 || ntiles < 0 || total_len < 0) return TG_ERR_ARG;
     const int64_t n = o->n;
     if (ws_bytes < tg_group_max_workspace_bytes(n, ntiles, o->mode == 1 ? o->H : 0)) return TG_ERR_WORKSPACE;
     const GmSub *subs = reinterpret_cast<const GmSub *>(subs_v);
@@ -1033,14 +1033,6 @@ TG_API int tg_group_max_batch(const tg_oracle_t *o, const int32_t *perm, const i
     TG_CUDA_CHECK(cudaMemsetAsync(pos, 0xff, (size_t)n * 4, st));
     TG_CUDA_CHECK(cudaMemsetAsync(vsub, 0xff, (size_t)n * 4, st));
     pos_fill_kernel<<<(unsigned)min(nsub, (int64_t)65535), 256, 0, st>>>(subs, nsub, perm, pos, vsub); tg_count_launch(1);
-    int64_t total_len = 0;
-    {
-        // the caller lays the sub-problems out back to back: total = last offset + length
-        GmSub last;
-        TG_CUDA_CHECK(cudaMemcpyAsync(&last, subs + nsub - 1, sizeof(GmSub), cudaMemcpyDeviceToHost, st));
-        TG_CUDA_CHECK(cudaStreamSynchronize(st));
-        total_len = last.perm_off + last.len;
-    }
     if (o->mode == 1 && ntiles > 0) {
         TG_CUDA_CHECK(cudaMemsetAsync(mask, 0, (size_t)ntiles * GM_TILE * 8, st));
         const int64_t blocks = min((total_len * 32 + 255) / 256, (int64_t)tg_num_sms() * 16);
@@ -1053,7 +1045,7 @@ TG_API int tg_group_max_batch(const tg_oracle_t *o, const int32_t *perm, const i
     }
     if (ntiles > 0) {
         int grid = (int)min((int64_t)tg_num_sms() * 8, ntiles);
-        if (o->mode == 1 && !getenv("TG_GM_OLD")) {
+        if (o->mode == 1) {
             const int Hp = (int)((o->H + GM_HC - 1) / GM_HC * GM_HC);
             float *hpf = ar.take<float>((size_t)total_len * Hp);
             double *hpd = ar.take<double>((size_t)total_len * Hp);

@@ -17,7 +17,39 @@
 #include <cstdlib>
 #include <chrono>
 #include <cstring>
+#include <mutex>
 #include <vector>
+
+// The hierarchy's per-layer buffers come from a pool owned by this library (one per device),
+// not from the process-wide default pool: it keeps up to 16 GiB cached between calls (the
+// n = 50k layer-3 buffers exceed 1 GiB, and a release threshold of 0 would unmap and remap them
+// on every call) without changing the default pool's policy for anyone else.
+// tg_release_cached_memory() trims it.
+static std::mutex g_pool_mu;
+static cudaMemPool_t g_pools[64];
+
+static cudaError_t tg_hier_pool(cudaMemPool_t *out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (!g_pools[dev]) {
+        cudaMemPoolProps props;
+        std::memset(&props, 0, sizeof(props));
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaMemPool_t pool;
+        if ((e = cudaMemPoolCreate(&pool, &props)) != cudaSuccess) return e;
+        uint64_t thr = 16ull << 30;
+        if ((e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr)) != cudaSuccess) return e;
+        g_pools[dev] = pool;
+    }
+    *out = g_pools[dev];
+    return cudaSuccess;
+}
 
 namespace {
 
@@ -36,21 +68,10 @@ struct DevBuf {
     }
     cudaError_t alloc(size_t bytes, cudaStream_t s) {
         st = s;
-        keep_pool_memory();
-        return cudaMallocAsync(&p, bytes ? bytes : 16, s);
-    }
-    // the default pool returns freed memory to the OS at every synchronisation
-    // (release threshold 0): keep it, so per-layer buffers are recycled cheaply
-    static void keep_pool_memory() {
-        static thread_local int dev_done = -1;
-        int dev = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess || dev == dev_done) return;
         cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = 16ull << 30;   // keep up to 16 GiB cached (n = 50k layer-3 buffers exceed 1 GiB)
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
-        dev_done = dev;
+        cudaError_t e = tg_hier_pool(&pool);
+        if (e != cudaSuccess) return e;
+        return cudaMallocFromPoolAsync(&p, bytes ? bytes : 16, pool, s);
     }
     template <class T>
     T *as() const { return reinterpret_cast<T *>(p); }
@@ -276,8 +297,8 @@ int launch_group_linkages(Ctx &cx, LinkJob &job, const std::vector<std::vector<c
     HC(cudaMemcpyAsync(d_sub, subs.data(), subs.size() * sizeof(tg_gm_sub_t), cudaMemcpyHostToDevice, job.st));
     HC(cudaMemcpyAsync(d_tile, tiles.data(), (size_t)ntiles * sizeof(tg_gm_tile_t), cudaMemcpyHostToDevice, job.st));
     HPROF("gl_h2d");
-    HR(tg_group_max_batch(cx.oracle, d_perm, d_gid, d_sub, (int64_t)subs.size(), d_tile, ntiles, d_out, out_off, d_ws,
-                          ws_bytes, job.st));
+    HR(tg_group_max_batch(cx.oracle, d_perm, d_gid, (int64_t)perm.size(), d_sub, (int64_t)subs.size(), d_tile, ntiles,
+                          d_out, out_off, d_ws, ws_bytes, job.st));
     HPROF("gl_gm");
     return launch_linkages(cx, job, d_out);
 }
@@ -323,6 +344,9 @@ int build(Ctx &cx, const int64_t *vb_dev, const int64_t *vc_dev, int64_t *lefts,
     LinkJob j1, j2, j3;
     static const bool l1_serial = std::getenv("TG_HIER_SERIAL") != nullptr;   // A/B switch
     std::vector<std::vector<int64_t>> handles1(multi.size());
+    // fork layer 1's stream BEFORE anything of layers 2/3 is queued on cx.st: its event then
+    // covers only the work that produced the assignment, so layer 1 never waits for layer 2
+    if (!multi.empty()) HC(side1.open(cx.st));
     HPROF("tL1");
     // ---- layers 2 (bubbles inside each converging group, dbht.py:264-300) and 3 (converging
     // groups against each other, dbht.py:302-324)
@@ -377,8 +401,6 @@ int build(Ctx &cx, const int64_t *vb_dev, const int64_t *vc_dev, int64_t *lefts,
     // layer 1 last: its linkages are never the critical path (layer 2 is at n = 10k, layer 3
     // at n = 50k), so its host preparation overlaps their device work
     if (!multi.empty()) {   // ---- layer 1: complete linkage inside every bubble group (dbht.py:247-262)
-        HC(side1.open(cx.st));
-        HPROF("open1");
         j1.st = side1.st;
         const size_t cnt = multi.size();
         std::vector<int32_t> perm;
@@ -519,4 +541,18 @@ TG_API int tg_serialize_dendrogram(const int64_t *lefts, const int64_t *rights, 
     }
     *len_out = used;
     return (out && used > cap) ? TG_ERR_CAPACITY : TG_OK;
+}
+
+// Return the hierarchy pool's cached memory (kept between tg_build_hierarchy calls) to the device.
+TG_API int tg_release_cached_memory(void) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    for (int d = 0; d < 64; d++)
+        if (g_pools[d]) {
+            cudaError_t e = cudaMemPoolTrimTo(g_pools[d], 0);
+            if (e != cudaSuccess) {
+                tg_set_last_error(e, __FILE__, __LINE__);
+                return TG_ERR_CUDA;
+            }
+        }
+    return TG_OK;
 }

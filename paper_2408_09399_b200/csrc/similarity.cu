@@ -328,11 +328,8 @@ TG_API int tg_pearson_f64(const double *X, int64_t n, int64_t L, double *S, void
     size_t smem = (size_t)2 * PSTAGES * PBM * PSTR * sizeof(double);
     size_t smem_epi = (size_t)PBM * TSTR * sizeof(double);
     if (smem_epi > smem) smem = smem_epi;
-    static bool attr = false;
-    if (!attr) {
-        TG_CUDA_CHECK(cudaFuncSetAttribute(syrk_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    // per call: the attribute is per device, and a cached flag would skip a second device
+    TG_CUDA_CHECK(cudaFuncSetAttribute(syrk_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     syrk_dmma_kernel<<<(unsigned)tiles, PTHREADS, smem, st>>>(Xc, inv, n, Lp, S); tg_count_launch(1);
     TG_LAUNCH_CHECK();
     return TG_OK;

@@ -19,7 +19,7 @@ import numpy as np
 
 from . import _device as D
 from . import _native as N
-from .apsp import _oracle_struct
+from .apsp import _oracle_struct, as_oracle
 from .linkage import Dendrogram, canonicalize_batch, dendrogram_from_merges, nn_chain_raw_batch
 from .tmfg import TraceError
 
@@ -161,6 +161,7 @@ def bubble_sinks(dtree: DirectedBubbleTree, graph) -> np.ndarray:
 
 def assign_vertices(graph, dtree: DirectedBubbleTree, oracle) -> BubbleAssignment:
     """Assign each vertex to its closest containing bubble (dbht.py:178-214)."""
+    oracle = as_oracle(oracle)
     t = D.torch()
     Sd = getattr(dtree, "_S_device", None)
     if Sd is None:
@@ -176,7 +177,6 @@ def assign_vertices(graph, dtree: DirectedBubbleTree, oracle) -> BubbleAssignmen
     N.call("tg_assign_vertices", s, N.ptr(b), m, N.ptr(sinks), N.ptr(vb), N.ptr(vc), N.ptr(ws), ws.numel(),
            N.stream_ptr())
     a = BubbleAssignment(vertex_bubble=vb.cpu().numpy(), vertex_converging=vc.cpu().numpy())
-    a._vb_dev, a._vc_dev = vb, vc   # device copies for build_hierarchy
     return a
 
 
@@ -225,6 +225,7 @@ def group_max_batch(oracle, subproblems):
     Returns the concatenated m x m max matrices (flat CUDA tensor) and the
     sub-problem descriptors (``out_off``, ``m`` ...).
     """
+    oracle = as_oracle(oracle)
     t = D.torch()
     perm, gid, sub_arr, tile_arr, out_len = group_layout(subproblems)
     perm_d = D.to_device(perm, t.int32)
@@ -234,7 +235,8 @@ def group_max_batch(oracle, subproblems):
     out = D.empty((max(out_len, 1),), t.float64)
     s = _oracle_struct(oracle)
     ws = D.Workspace.get(N.size("tg_group_max_workspace_bytes", oracle.n, int(tile_arr.shape[0]), int(s.H) if s.mode == 1 else 0))
-    N.call("tg_group_max_batch", s, N.ptr(perm_d), N.ptr(gid_d), N.ptr(sub_d), int(sub_arr.shape[0]), N.ptr(tile_d),
+    N.call("tg_group_max_batch", s, N.ptr(perm_d), N.ptr(gid_d), int(perm.shape[0]), N.ptr(sub_d),
+           int(sub_arr.shape[0]), N.ptr(tile_d),
            int(tile_arr.shape[0]), N.ptr(out), out_len, N.ptr(ws), ws.numel(), N.stream_ptr())
     return out, sub_arr
 
@@ -278,11 +280,10 @@ def build_hierarchy(assignment: BubbleAssignment, dtree: DirectedBubbleTree, ora
     canonicalisation, records and the height-floor emission are C++ host code.
     """
     t = D.torch()
-    vb = getattr(assignment, "_vb_dev", None)
-    vc = getattr(assignment, "_vc_dev", None)
-    if vb is None or vc is None:
-        vb = D.to_device(np.asarray(assignment.vertex_bubble, dtype=np.int64), t.int64)
-        vc = D.to_device(np.asarray(assignment.vertex_converging, dtype=np.int64), t.int64)
+    oracle = as_oracle(oracle)
+    # O(n) upload of the caller's current arrays (no stale device copy if they were edited)
+    vb = D.to_device(np.asarray(assignment.vertex_bubble, dtype=np.int64), t.int64)
+    vc = D.to_device(np.asarray(assignment.vertex_converging, dtype=np.int64), t.int64)
     n = int(vb.shape[0])
     k = max(n - 1, 0)
     lefts = np.empty(max(k, 1), dtype=np.int64)

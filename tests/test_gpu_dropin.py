@@ -119,3 +119,29 @@ def test_reference_test_suite_under_install(ref):
     print(out[-3000:])
     assert "rebound to the B200 path" in out
     assert r.returncode == 0, out[-6000:]
+
+
+def test_in_place_edit_between_stage_calls_is_seen(oracle):
+    """An in-place edit of S between sort_neighbor_lists and build_tmfg_heap (and before
+    to_weighted) gives the reference's result for the edited S: no stale device copy."""
+    import paper_2408_09399_b200 as p
+    from paper_2408_09399_b200 import synth
+    p._native.load()
+    x, _ = synth.generate(2, n=600, seed=11)
+    S = oracle.pearson_similarity(x)
+    order0 = oracle.sort_neighbor_lists(S)
+    ref0 = oracle.build_tmfg_heap(S, order0)
+    lists = p.sort_neighbor_lists(S)
+    # weaken an edge the unedited TMFG inserts early, far from any strided sample position
+    a, b = (int(v) for v in ref0["edges"][40])
+    S[a, b] = S[b, a] = -0.25
+    ref1 = oracle.build_tmfg_heap(S, order0)
+    assert not np.array_equal(ref1["trace"], ref0["trace"]), "edit must change the reference's result"
+    g = p.build_tmfg_heap(S, lists)
+    assert np.array_equal(g.trace, ref1["trace"])
+    assert np.array_equal(g.edges, ref1["edges"])
+    assert np.array_equal(g.weights, ref1["weights"])
+    S[int(ref1["edges"][7][0]), int(ref1["edges"][7][1])] = 0.5   # asymmetric edit: lengths read S[e0, e1]
+    w = p.to_weighted(g, S)
+    wref = oracle.to_weighted(ref1, S)
+    assert np.array_equal(w.lengths, wref["lengths"])
