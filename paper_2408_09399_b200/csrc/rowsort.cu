@@ -431,7 +431,7 @@ __host__ FkPlan fk_plan(int64_t n, int nbuf, size_t smem_max, double fs_cap) {
     if (fs > fs_cap) fs = fs_cap;
     p.fs = (float)fs;
     p.NBcap = 2 * (p.C + 1) + (int)std::ceil(fs * m) + 4;
-    p.smem = p.off_f16 + (size_t)(p.NBcap / 2 + 2) * sizeof(uint32_t);
+    p.smem = p.off_f16 + (size_t)(p.NBcap / 2 + 2 + 16) * sizeof(uint32_t);
     if (fs < 0.45 || p.NBcap >= 65535) p.smem = (size_t)-1;
     return p;
 }
@@ -875,6 +875,418 @@ row_sort_fk_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restric
         for (int k = 0; k < 7; k++) atomicAdd((unsigned long long *)&g_rs_phase[k], (unsigned long long)ph[k]);
 #endif
 #undef FK_PH
+}
+
+// ---------------------------------------------------------------- v2: rank by bucket walk
+// The production sort for n <= FK_NMAX.  Same bucket map, counters and screen as the
+// float-key kernel above, with fewer instructions per key where they were spent:
+//  * the scatter writes (float key, column id) pairs, so the rank of a key inside its
+//    bucket is a walk over the bucket's few pairs in shared memory by the key's own lane
+//    (singleton buckets -- most of them -- cost nothing); no run detection, shuffles or
+//    window-edge walks by sorted position;
+//  * the ranked ids land in shared memory and leave by one TMA bulk store per row
+//    (cp.async.bulk.global.shared::cta; the 16-byte aligned body, scalar edges), so the
+//    id store costs one STS per key and the next row's TMA load into the buffer waits
+//    only for that store's reads (cp.async.bulk.wait_group.read).
+// Ties at float precision still go to the doubles (re-read through L2), then the id.
+__device__ __forceinline__ void v2_bulk_store(int32_t *g, const void *smem, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(g), "r"(rt_smem_u32(smem)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void v2_bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+
+template <bool ODD, int KPT>
+__device__ __forceinline__ void v2_row(const FkRow &R, const float (&fk)[KPT], unsigned char *buf) {
+    constexpr int NT = FK_T, W = NT / 32;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n = R.n, m = R.m, vi = R.vi, C = R.C;
+    uint32_t *f16 = R.f16, *ccnt = R.ccnt;
+    uint32_t *cinfo32 = R.ccnt;   // per coarse bin: fine base | fine count << 16
+    const uint16_t *o16 = reinterpret_cast<const uint16_t *>(f16);
+    FkMisc &ms = *R.ms;
+    uint2 *P = reinterpret_cast<uint2 *>(buf);   // scattered (float key bits, column id)
+    float hs = R.hc, scale = R.hc;               // t = hs - f * scale
+    if (ODD) {   // the row's float range, histogram again
+        float fmn = INFINITY, fmx = -INFINITY;
+#pragma unroll
+        for (int e = 0; e < KPT; e++) {
+            const int j = tid + e * NT;
+            if (j < n && j != vi) { fmn = fminf(fmn, fk[e]); fmx = fmaxf(fmx, fk[e]); }
+        }
+        for (int o = 16; o; o >>= 1) {
+            fmn = fminf(fmn, __shfl_xor_sync(0xffffffffu, fmn, o));
+            fmx = fmaxf(fmx, __shfl_xor_sync(0xffffffffu, fmx, o));
+        }
+        if (lane == 0) { ms.rmn[warp] = fmn; ms.rmx[warp] = fmx; }
+        for (int c = tid; c <= C; c += NT) ccnt[c] = 0u;
+        __syncthreads();
+        float lo = INFINITY, hi = -INFINITY;
+        for (int w = 0; w < W; w++) { lo = fminf(lo, ms.rmn[w]); hi = fmaxf(hi, ms.rmx[w]); }
+        const float wd = hi - lo;
+        scale = (wd > 0.0f && wd < INFINITY) ? (float)C / wd : 0.0f;
+        if (!(hi < INFINITY && hi > -INFINITY)) hi = 0.0f;
+        hs = hi * scale;
+#pragma unroll
+        for (int e = 0; e < KPT; e += 4) {
+            const int j = tid + e * NT;
+            if (j < n && j != vi) atomicAdd(&ccnt[fk_coarse<true>(fk[e], hs, scale, C)], 1u);
+        }
+        __syncthreads();
+    }
+    // ---- 2: fine buckets per coarse bin (one thread per bin) -> per-bin (A, B)
+    {
+        const float fsc = (float)m * R.fs / (float)(R.nsamp > 0 ? R.nsamp : 1) * 0.9999f;
+        const uint32_t f = tid <= C ? 1u + (uint32_t)((float)ccnt[tid] * fsc) : 0u;
+        uint32_t incl = f;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) ms.wsum[warp] = incl;
+        __syncthreads();
+        if (tid <= C) {
+            uint32_t off = 0;
+            for (int w = 0; w < warp; w++) off += ms.wsum[w];
+            const uint32_t base = off + incl - f;
+            cinfo32[tid] = base | (f << 16);   // fb = rn((d + 1/2) f + base): the same value as v1's map
+            if (tid == C) ms.nb = (int)(base + f) + 1;
+        }
+    }
+    __syncthreads();
+    // ---- 3: fine bucket + arrival rank (one packed-u16 shared atomic per key); the loads,
+    // then the atomics, are issued back to back (independent across keys)
+    uint32_t pk[KPT];
+    const int nan_fb = ms.nb - 1;
+    constexpr int G3 = 6;   // keys per batch
+#pragma unroll
+    for (int e0 = 0; e0 < KPT; e0 += G3) {
+        uint32_t ab[G3];
+        float dd[G3];
+#pragma unroll
+        for (int g = 0; g < G3; g++) {
+            const int e = e0 + g;
+            if (e >= KPT) break;
+            float t = fmaf(fk[e], -scale, hs);
+            if (ODD) t = fminf(fmaxf(t, 0.0f), (float)C);
+            const float y = t + FK_MAGIC;
+            const int c = __float_as_int(y) & 0x3fffff;
+            dd[g] = t - (y - FK_MAGIC);   // exact
+            const int j = tid + e * NT;
+            ab[g] = (j < n) ? cinfo32[c] : 0u;
+        }
+#pragma unroll
+        for (int g = 0; g < G3; g++) {
+            const int e = e0 + g;
+            if (e >= KPT) break;
+            const int j = tid + e * NT;
+            pk[e] = 0xffffffffu;
+            if (j < n && j != vi) {
+                int fb = fk_rni(fmaf(dd[g] + 0.5f, (float)(ab[g] >> 16), (float)(ab[g] & 0xffffu)));
+                if (ODD && fk[e] != fk[e]) fb = nan_fb;
+                const uint32_t sh = (fb & 1) << 4;
+                const uint32_t old = atomicAdd(&f16[fb >> 1], 1u << sh);
+                pk[e] = __byte_perm((uint32_t)fb, old >> sh, 0x1054);   // (fb << 16) | arrival
+            }
+        }
+    }
+    __syncthreads();
+    for (int c = tid; c <= C; c += NT) ccnt[c] = 0u;   // next row's histogram (cinfo is dead)
+    // ---- 4: exclusive scan of the packed counters.  Warp w owns a contiguous range of words and
+    // walks it 128 words (one 16-byte load per lane, conflict-free) at a time.
+    {
+        const int nw = (ms.nb + 2) >> 1;
+        const int per = ((nw + W - 1) / W + 127) & ~127;   // words per warp
+        const int w0 = warp * per;
+        uint32_t s = 0;   // the warp's total (lane 31 after the loop)
+        for (int q = 0; q < per; q += 128) {
+            const int w = w0 + q + 4 * lane;
+            uint32_t t = 0;
+            if (w < nw) {
+                const uint4 x = *reinterpret_cast<const uint4 *>(f16 + w);
+                t = ((x.x + (x.x << 16)) >> 16) + ((x.y + (x.y << 16)) >> 16) + ((x.z + (x.z << 16)) >> 16) +
+                    ((x.w + (x.w << 16)) >> 16);
+            }
+            s += __reduce_add_sync(0xffffffffu, t);
+        }
+        if (lane == 0) ms.wsum[warp] = s;
+        __syncthreads();
+        uint32_t run;
+        {
+            const uint32_t wv = ms.wsum[lane];
+            uint32_t wi = wv;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+                if (lane >= o) wi += y;
+            }
+            run = __shfl_sync(0xffffffffu, wi - wv, warp);   // words before this warp's range
+        }
+        for (int q = 0; q < per; q += 128) {
+            const int w = w0 + q + 4 * lane;
+            uint4 x = make_uint4(0u, 0u, 0u, 0u);
+            if (w < nw) x = *reinterpret_cast<const uint4 *>(f16 + w);
+            const uint32_t c0 = (x.x + (x.x << 16)) >> 16, c1 = (x.y + (x.y << 16)) >> 16;
+            const uint32_t c2 = (x.z + (x.z << 16)) >> 16, c3 = (x.w + (x.w << 16)) >> 16;
+            const uint32_t t = c0 + c1 + c2 + c3;
+            uint32_t incl = t;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            uint32_t r = run + incl - t;
+            if (w < nw) {
+                x.x = r * 0x10001u + (x.x << 16); r += c0;
+                x.y = r * 0x10001u + (x.y << 16); r += c1;
+                x.z = r * 0x10001u + (x.z << 16); r += c2;
+                x.w = r * 0x10001u + (x.w << 16);
+                *reinterpret_cast<uint4 *>(f16 + w) = x;
+            }
+            run += __shfl_sync(0xffffffffu, incl, 31);
+        }
+    }
+    __syncthreads();
+    // ---- 5: scatter (key, id) to bucket offset + arrival (offset loads batched, then the stores);
+    // pk becomes (bucket start s0, position of the key's pair)
+    {
+        uint32_t s0[KPT];
+#pragma unroll
+        for (int e = 0; e < KPT; e++) s0[e] = pk[e] != 0xffffffffu ? o16[pk[e] >> 16] : 0u;
+#pragma unroll
+        for (int e = 0; e < KPT; e++) {
+            if (pk[e] != 0xffffffffu) {
+                const uint32_t p = s0[e] + (pk[e] & 0xffffu);
+                P[p] = make_uint2(__float_as_uint(fk[e]), (uint32_t)(tid + e * NT));
+                pk[e] = (pk[e] & 0xffff0000u) | s0[e];   // (bucket, bucket start)
+            }
+        }
+    }
+    __syncthreads();
+    // ---- 6: rank inside the bucket: a fixed 4-slot compare (predicated loads, no loop) covers
+    // buckets of <= 4 keys -- nearly all of them; larger buckets and float ties walk the bucket
+    const double *row = R.row;
+    constexpr int G = 4;   // keys per batch (bounds the registers of the batched loads)
+#pragma unroll
+    for (int e0 = 0; e0 < KPT; e0 += G) {
+        int s0[G], cc[G];
+        float kq[G][4];
+#pragma unroll
+        for (int g = 0; g < G; g++) {
+            const int e = e0 + g;
+            s0[g] = 0;
+            cc[g] = 0;
+            if (e < KPT && pk[e] != 0xffffffffu) {
+                const int fb = (int)(pk[e] >> 16);
+                s0[g] = (int)(pk[e] & 0xffffu);
+                cc[g] = (int)o16[fb + 1] - s0[g];
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < G; g++) {   // a singleton bucket holds only the key itself: no loads
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+                kq[g][i] = (cc[g] > 1 && i < cc[g]) ? __uint_as_float(P[s0[g] + i].x) : (ODD ? 0.0f : -INFINITY);
+        }
+#pragma unroll
+        for (int g = 0; g < G; g++) {
+            const int e = e0 + g;
+            if (e >= KPT || pk[e] == 0xffffffffu) continue;
+            const int j = tid + e * NT;
+            const float fj = fk[e];
+            const int c = cc[g];
+            int rank = 0, tie = 0;
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                const float fo = kq[g][i];
+                const bool in = c > 1 && i < c;
+                if (!ODD) {   // absent slots hold -inf: never above or equal to a key in [-1, 1]
+                    rank += fo > fj;
+                    tie += fo == fj;
+                } else {
+                    const bool no = fo != fo, nj = fj != fj;
+                    rank += in & ((fo > fj) | (nj & !no));
+                    tie += in & ((fo == fj) | (nj & no));
+                }
+            }
+            if (c > 4) {
+                for (int q = s0[g] + 4; q < s0[g] + c; q++) {
+                    const float fo = __uint_as_float(P[q].x);
+                    if (!ODD) {
+                        rank += fo > fj;
+                        tie += fo == fj;
+                    } else {
+                        const bool no = fo != fo, nj = fj != fj;
+                        rank += (fo > fj) | (nj & !no);
+                        tie += (fo == fj) | (nj & no);
+                    }
+                }
+            }
+            if (tie > 1) {   // float ties (itself included): the doubles decide, then the id
+                const double xj = __ldg(row + j);
+                rank = 0;
+                for (int q = s0[g]; q < s0[g] + c; q++) {
+                    const uint2 o = P[q];
+                    if ((int)o.y == j) continue;
+                    const float fo = __uint_as_float(o.x);
+                    const bool feq = ODD ? ((fo == fj) | ((fo != fo) & (fj != fj))) : (fo == fj);
+                    if (!feq) {
+                        if (!ODD) rank += fo > fj;
+                        else rank += (fo > fj) | ((fj != fj) & (fo == fo));
+                    } else {
+                        rank += rs_before(__ldg(row + o.y), (int)o.y, xj, j);
+                    }
+                }
+            }
+            pk[e] = (uint32_t)(s0[g] + rank);
+        }
+    }
+    __syncthreads();   // every walk is done: the buffer takes the ranked ids
+    int32_t *out32 = reinterpret_cast<int32_t *>(buf) + (int)(((uintptr_t)R.out >> 2) & 3);
+#pragma unroll
+    for (int e = 0; e < KPT; e++)
+        if (pk[e] != 0xffffffffu) out32[pk[e]] = tid + e * NT;
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic writes -> bulk-store reads
+    __syncthreads();
+}
+
+template <int KPT>
+__global__ void __launch_bounds__(FK_T, 1)
+row_sort_v2_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restrict__ order,
+                   double *__restrict__ screen, FkPlan pl) {
+    extern __shared__ __align__(16) unsigned char fk_smem[];
+    constexpr int NT = FK_T, W = NT / 32;
+    const int n = (int)n64;
+    const int m = n - 1;
+    uint32_t *ccnt = reinterpret_cast<uint32_t *>(fk_smem + pl.off_cinfo);   // histogram, then (A, B)
+    FkMisc &ms = *reinterpret_cast<FkMisc *>(fk_smem + pl.off_misc);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(fk_smem + pl.off_bar);
+    uint32_t *f16 = reinterpret_cast<uint32_t *>(fk_smem + pl.off_f16);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int C = pl.C;
+    const int nw16 = pl.NBcap / 2 + 2;
+    const size_t bstride = (size_t)pl.stride * sizeof(double);
+
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;\n" ::"r"(rt_smem_u32(&bar[0])) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;\n" ::"r"(rt_smem_u32(&bar[1])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    for (int c = tid; c <= C; c += NT) ccnt[c] = 0u;
+    __syncthreads();
+    int64_t v = blockIdx.x;
+    if (tid == 0 && v < n) rt_bulk_row(reinterpret_cast<double *>(fk_smem), S + v * n64, n, &bar[0]);
+    int nsamp_all = 0;   // sampled keys: e % 4 == 0
+#pragma unroll
+    for (int e = 0; e < KPT; e += 4) {
+        const int r = n - e * NT;
+        nsamp_all += r < 0 ? 0 : (r < NT ? r : NT);
+    }
+    FkRow R;
+    R.f16 = f16;
+    R.cinfo = reinterpret_cast<float2 *>(ccnt);
+    R.ccnt = ccnt;
+    R.ms = &ms;
+    R.n = n;
+    R.m = m;
+    R.C = C;
+    R.fs = pl.fs;
+    R.hc = pl.hc;
+    R.sid = nullptr;
+    R.fkey = nullptr;
+    R.sidx = nullptr;
+    for (int it = 0; v < n; v += gridDim.x, it++) {
+        const int b = pl.nbuf == 2 ? (it & 1) : 0;
+        const unsigned parity = pl.nbuf == 2 ? (unsigned)((it >> 1) & 1) : (unsigned)(it & 1);
+        unsigned char *buf = fk_smem + (size_t)b * bstride;
+        const double *row = S + v * n64;
+        const double *vals = reinterpret_cast<const double *>(buf) + (((uintptr_t)row >> 3) & 1);
+        const int vi = (int)v;
+        for (int i = 4 * tid; i < nw16 + 8; i += 4 * NT)   // + the 16-byte scan's overhang
+            *reinterpret_cast<uint4 *>(f16 + i) = make_uint4(0u, 0u, 0u, 0u);
+        rt_wait(&bar[b], parity);
+        // ---- 1: doubles -> float keys (registers), screen sums, sampled coarse histogram
+        float fk[KPT];
+        double sm = 0.0, sa = 0.0;
+        bool odd = false;
+#pragma unroll
+        for (int e = 0; e < KPT; e++) {
+            const int j = tid + e * NT;
+            fk[e] = 0.0f;
+            if (j < n) {
+                const double x = vals[j];
+                sm += x;
+                sa += fabs(x);
+                const float f = __double2float_rn(x);
+                fk[e] = f;
+                if (j != vi) {
+                    odd |= !(fabsf(f) <= 1.0f);   // NaN or outside [-1, 1] at float precision
+                    if ((e & 3) == 0) atomicAdd(&ccnt[fk_coarse<true>(f, pl.hc, pl.hc, C)], 1u);
+                } else {
+                    ms.diag = x;
+                }
+            }
+        }
+        if (screen) {
+            for (int o = 16; o; o >>= 1) {
+                sm += __shfl_xor_sync(0xffffffffu, sm, o);
+                sa += __shfl_xor_sync(0xffffffffu, sa, o);
+            }
+            if (lane == 0) { ms.rsum[warp] = sm; ms.rabs[warp] = sa; }
+        }
+        const bool row_odd = __syncthreads_or(odd);   // every double of the row is consumed
+        if (tid == 0) {
+            const int64_t vn = v + gridDim.x;
+            if (pl.nbuf == 2 && vn < n) {
+                v2_bulk_wait_read();   // the previous row's id store out of the other buffer
+                rt_bulk_row(reinterpret_cast<double *>(fk_smem + (size_t)(b ^ 1) * bstride), S + vn * n64, n,
+                            &bar[b ^ 1]);
+            }
+        }
+        if (screen && warp == W - 1) {
+            double s1 = ms.rsum[lane], s2 = ms.rabs[lane];
+            for (int o = 16; o; o >>= 1) {
+                s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+                s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+            }
+            if (lane == 0) {
+                screen[vi] = __dsub_rn(s1, ms.diag);
+                screen[n + vi] = rs_screen_radius_t(n, NT, s2);
+            }
+        }
+        R.row = row;
+        R.out = order + v * (int64_t)m;
+        R.vi = vi;
+        R.nsamp = nsamp_all - (((vi / NT) & 3) == 0 ? 1 : 0);
+        if (row_odd) v2_row<true, KPT>(R, fk, buf);
+        else v2_row<false, KPT>(R, fk, buf);
+        // ---- 7: the ranked ids leave by a bulk store (16-byte aligned body) + scalar edges
+        {
+            int32_t *g = R.out;
+            const int a = (int)(((uintptr_t)g >> 2) & 3);
+            const int32_t *out32 = reinterpret_cast<const int32_t *>(buf) + a;
+            const int h = (4 - a) & 3;
+            const int p0 = h < m ? h : m;
+            const int p1 = p0 + ((m - p0) & ~3);
+            if (tid == 0 && p1 > p0) v2_bulk_store(g + p0, out32 + p0, (unsigned)((p1 - p0) * 4));
+            if (warp == 1) {
+                if (lane < p0) g[lane] = out32[lane];
+                else if (lane >= 4 && lane - 4 < m - p1) g[p1 + lane - 4] = out32[p1 + lane - 4];
+            }
+        }
+        if (pl.nbuf == 1) {
+            __syncthreads();   // warp 1's edge reads of the buffer are done before it is refilled
+            if (tid == 0) {
+                const int64_t vn = v + gridDim.x;
+                if (vn < n) {
+                    v2_bulk_wait_read();
+                    rt_bulk_row(reinterpret_cast<double *>(fk_smem), S + vn * n64, n, &bar[0]);
+                }
+            }
+        }
+    }
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
 // ---------------------------------------------------------------- long rows (n > FK_NMAX)
@@ -1412,15 +1824,17 @@ TG_API int tg_row_sort_f64(const double *S, int64_t n, int32_t *order, double *s
         if (pl.smem > RS_SMEM_MAX || pl.fs < 1.5f) pl = fk_plan(n, 1, RS_SMEM_MAX, fcap);
         if (pl.smem > RS_SMEM_MAX) return TG_ERR_ARG;
         const int K = (int)((n + FK_T - 1) / FK_T);
+        static const bool v1 = getenv("TG_SORT_V1") != nullptr;   // A/B switch (development)
 #define FK_LAUNCH(KK)                                                                                      \
     do {                                                                                                   \
-        auto kfn = row_sort_fk_kernel<KK>;                                                                 \
+        auto kfn = v1 ? row_sort_fk_kernel<KK> : row_sort_v2_kernel<KK>;                                   \
         TG_CUDA_CHECK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem)); \
         kfn<<<grid, FK_T, pl.smem, st>>>(S, n, order, screen, pl); tg_count_launch(1);                      \
     } while (0)
         if (K <= 2) FK_LAUNCH(2);
         else if (K <= 4) FK_LAUNCH(4);
         else if (K <= 8) FK_LAUNCH(8);
+        else if (K <= 10) FK_LAUNCH(10);
         else if (K <= 12) FK_LAUNCH(12);
         else if (K <= 16) FK_LAUNCH(16);
         else FK_LAUNCH(24);

@@ -28,6 +28,8 @@ def pytest_configure(config):
     p._native.load()
     _SAVED.update(p.install(tmfgclust))
     config._tg_installed = sorted(f"{m}.{n}" for (m, n) in _SAVED)
+    print(f"paper_2408_09399_b200.install(): {len(_SAVED)} reference attributes rebound to the B200 path",
+          file=sys.stderr)
 
 
 def pytest_report_header(config):
