@@ -110,6 +110,19 @@ int tg_tmfg_heap(const double *S, const int32_t *order, int64_t n, const int32_t
                  int32_t *host_fid_out, int32_t *edges_out, int32_t *faces_out, int64_t *stats_out, int32_t check,
                  void *ws, size_t ws_bytes, void *stream);
 
+/* tmfg.py:208-263 build_tmfg_exact and tmfg.py:280-341 build_tmfg_corr, with the
+ * prefix rule of tmfg.py:185-205 _select_round (prefix_size >= 1).  S validated by the
+ * caller; clique from tg_initial_clique*; order (corr only) from tg_row_sort_f64.
+ * Outputs trace (n-4, 4), edges (3n-6, 2), faces (2n-4, 3) int32 exactly as the
+ * reference's _GraphAccum (tmfg.py:94-144).  One persistent CTA; the workspace holds
+ * the face table and the scan state (~40 n bytes). */
+size_t tg_tmfg_variant_workspace_bytes(int64_t n);
+int tg_tmfg_exact(const double *S, int64_t n, const int32_t *clique, int64_t prefix_size, int32_t *trace_out,
+                  int32_t *edges_out, int32_t *faces_out, void *ws, size_t ws_bytes, void *stream);
+int tg_tmfg_corr(const double *S, const int32_t *order, int64_t n, const int32_t *clique, int64_t prefix_size,
+                 int32_t *trace_out, int32_t *edges_out, int32_t *faces_out, void *ws, size_t ws_bytes,
+                 void *stream);
+
 /* tmfg.py:137-143 finalize weights: w[i] = S[edges[i,0], edges[i,1]]. */
 int tg_edge_weights(const double *S, int64_t n, const int32_t *edges, int64_t m, double *w_out, void *stream);
 

@@ -36,25 +36,57 @@ from .dbht import (
     converging_bubbles,
     orient_edges,
 )
-from .linkage import Dendrogram, cut, dendrogram_from_merges, nn_chain_merges, serialize_dendrogram
-from .pipeline import PipelineConfig, RunReport, StageError, run_series, run_stages
+from .linkage import (
+    Dendrogram,
+    complete_linkage,
+    cut,
+    dendrogram_from_merges,
+    load_dendrogram,
+    nn_chain_merges,
+    save_dendrogram,
+    serialize_dendrogram,
+)
+from .metrics import ari, edge_sum_delta
+from .pipeline import (
+    PipelineConfig,
+    RunReport,
+    StageError,
+    compare_variants,
+    load_input,
+    parse_variant_token,
+    run_pipeline,
+    run_series,
+    run_stages,
+)
 from .simmatrix import (
     DataError,
     Dataset,
     SortedNeighborLists,
+    load_matrix,
+    load_ucr_dataset,
     pearson_similarity,
+    read_matrix_binary,
+    save_matrix,
     sort_neighbor_lists,
     validate_similarity,
+    write_matrix_binary,
 )
 from .tmfg import (
     GAIN_EPS,
     BuildConfig,
     TmfgGraph,
+    TmfgState,
     TraceError,
     build_tmfg,
+    build_tmfg_corr,
+    build_tmfg_exact,
     build_tmfg_heap,
     edge_sum,
     gain,
+    load_tmfg,
+    refresh_max_corr,
+    replay_trace,
+    save_tmfg,
     select_initial_clique,
 )
 
@@ -63,7 +95,7 @@ __version__ = "0.1.0"
 # reference module -> names this package replaces in it
 _INSTALL_MAP = {
     "simmatrix": ["pearson_similarity", "sort_neighbor_lists"],
-    "tmfg": ["select_initial_clique", "build_tmfg_heap"],
+    "tmfg": ["select_initial_clique", "build_tmfg_exact", "build_tmfg_corr", "build_tmfg_heap"],
     "apsp": ["to_weighted", "apsp_exact", "apsp_hub", "select_hubs"],
     "dbht": ["build_bubble_tree", "orient_edges", "bubble_sinks", "assign_vertices", "build_hierarchy"],
     "linkage": ["nn_chain_merges"],

@@ -75,6 +75,9 @@ _PROTOS = {
     "tg_initial_clique_screened": (ctypes.c_int, [c_p, c_i64, c_p, c_p, c_p, c_sz, c_p]),
     "tg_tmfg_workspace_bytes": (c_sz, [c_i64]),
     "tg_tmfg_heap": (ctypes.c_int, [c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, ctypes.c_int32, c_p, c_sz, c_p]),
+    "tg_tmfg_variant_workspace_bytes": (c_sz, [c_i64]),
+    "tg_tmfg_exact": (ctypes.c_int, [c_p, c_i64, c_p, c_i64, c_p, c_p, c_p, c_p, c_sz, c_p]),
+    "tg_tmfg_corr": (ctypes.c_int, [c_p, c_p, c_i64, c_p, c_i64, c_p, c_p, c_p, c_p, c_sz, c_p]),
     "tg_edge_weights": (ctypes.c_int, [c_p, c_i64, c_p, c_i64, c_p, c_p]),
     "tg_weighted_workspace_bytes": (c_sz, [c_i64, c_i64]),
     "tg_to_weighted": (ctypes.c_int, [c_p, c_i64, c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_sz, c_p]),

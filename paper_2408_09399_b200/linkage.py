@@ -205,3 +205,41 @@ def serialize_dendrogram(d: Dendrogram) -> str:
         rc = lib.tg_serialize_dendrogram(*ptrs, k, buf, need.value, ctypes.byref(need))
     N.check("tg_serialize_dendrogram", rc)
     return buf.raw[: need.value].decode()
+
+
+def save_dendrogram(d: Dendrogram, path) -> None:
+    """Write the dendrogram text of serialize_dendrogram (linkage.py:190-191)."""
+    from pathlib import Path
+
+    Path(path).write_text(serialize_dendrogram(d))
+
+
+def load_dendrogram(path) -> Dendrogram:
+    """Read "left right height size" rows back (linkage.py:194-208); blank lines ignored."""
+    from pathlib import Path
+
+    text = Path(path).read_text()
+    rows = [ln.split() for ln in text.splitlines() if ln.strip()]
+    k = len(rows)
+    lefts = np.fromiter((int(r[0]) for r in rows), dtype=np.int64, count=k)
+    rights = np.fromiter((int(r[1]) for r in rows), dtype=np.int64, count=k)
+    heights = np.fromiter((float(r[2]) for r in rows), dtype=np.float64, count=k)
+    sizes = np.fromiter((int(r[3]) for r in rows), dtype=np.int64, count=k)
+    return Dendrogram(n_leaves=k + 1, lefts=lefts, rights=rights, heights=heights, sizes=sizes)
+
+
+def complete_linkage(items, dist) -> Dendrogram:
+    """Complete-linkage HAC over ``items`` with a symmetric callable ``dist`` (linkage.py:119-133).
+
+    The pairwise matrix is filled on the host (dist is arbitrary Python); the NN-chain runs
+    on the GPU.  Leaves are item positions 0..len(items)-1.
+    """
+    items = list(items)
+    m = len(items)
+    if m < 1:
+        raise ValueError("need at least one item")
+    Dm = np.zeros((m, m))
+    iu, ju = np.triu_indices(m, 1)
+    for i, j in zip(iu.tolist(), ju.tolist()):
+        Dm[i, j] = Dm[j, i] = float(dist(items[i], items[j]))
+    return dendrogram_from_merges(m, nn_chain_merges(Dm))

@@ -201,3 +201,121 @@ def sort_neighbor_lists(S, workers: int | None = None) -> SortedNeighborLists:
     Sd = D.device_matrix(S)
     order, screen = sort_rows_device(Sd, with_screen=True)
     return SortedNeighborLists(S, order, S_device=Sd, screen_device=screen)
+
+
+# ------------------------------------------------------------------ on-disk formats (simmatrix.py:55-202)
+SYMMETRY_TOL = 1e-9
+
+
+def _label_codes(raw: list) -> np.ndarray:
+    """Map a label alphabet onto 0..k-1: numeric-looking alphabets numerically, else lexicographically."""
+    alphabet = sorted(set(raw))
+    try:
+        alphabet.sort(key=float)
+    except ValueError:
+        pass
+    code = {lab: i for i, lab in enumerate(alphabet)}
+    return np.fromiter((code[lab] for lab in raw), dtype=np.int64, count=len(raw))
+
+
+def load_ucr_dataset(path) -> Dataset:
+    """UCR-style text: a label then L values per line, tab / comma (or space) separated (simmatrix.py:72-102)."""
+    import re
+    from pathlib import Path
+
+    sep = re.compile(r"[\t, ]+")
+    labels: list = []
+    rows: list = []
+    width = None
+    path = Path(path)
+    with path.open() as fh:
+        for lineno, line in enumerate(fh, start=1):
+            line = line.strip()
+            if not line:
+                continue
+            fields = [f for f in sep.split(line) if f]
+            if len(fields) < 3:
+                raise DataError(f"{path}:{lineno}: expected a label and at least 2 values")
+            if width is None:
+                width = len(fields)
+            elif len(fields) != width:
+                raise DataError(f"{path}:{lineno}: ragged row, expected {width} fields, got {len(fields)}")
+            try:
+                vals = [float(f) for f in fields[1:]]
+            except ValueError as exc:
+                raise DataError(f"{path}:{lineno}: non-numeric value") from exc
+            if any(v != v for v in vals):
+                raise DataError(f"{path}:{lineno}: NaN value in series")
+            labels.append(fields[0])
+            rows.append(vals)
+    if len(rows) < 4:
+        raise DataError(f"dataset too small: need at least 4 objects, got {len(rows)}")
+    return Dataset(labels=_label_codes(labels), series=np.array(rows, dtype=np.float64))
+
+
+def write_matrix_binary(path, M) -> None:
+    """Square matrix as 8-byte little-endian n, then n*n row-major little-endian float64."""
+    if D.is_device(M):
+        M = M.cpu().numpy()
+    M = np.ascontiguousarray(M, dtype="<f8")
+    with open(path, "wb") as fh:
+        fh.write(np.uint64(M.shape[0]).astype("<u8").tobytes())
+        fh.write(memoryview(M).cast("B"))
+
+
+def read_matrix_binary(path) -> np.ndarray:
+    """Inverse of write_matrix_binary; DataError on a truncated or mis-sized file."""
+    from pathlib import Path
+
+    raw = Path(path).read_bytes()
+    if len(raw) < 8:
+        raise DataError(f"{path}: truncated binary matrix")
+    n = int(np.frombuffer(raw, dtype="<u8", count=1)[0])
+    want = 8 + 8 * n * n
+    if len(raw) != want:
+        raise DataError(f"{path}: size mismatch, expected {want} bytes for n={n}")
+    return np.frombuffer(raw, dtype="<f8", offset=8).reshape(n, n).astype(np.float64)
+
+
+def save_matrix(path, S) -> None:
+    """Validate (on the device) and persist a similarity matrix in the binary format."""
+    write_matrix_binary(path, validate_similarity(S))
+
+
+def _is_binary_matrix(path) -> bool:
+    import os
+
+    size = os.path.getsize(path)
+    if size < 8:
+        return False
+    with open(path, "rb") as fh:
+        n = int(np.frombuffer(fh.read(8), dtype="<u8")[0])
+    return n > 0 and size == 8 + 8 * n * n
+
+
+def load_matrix(path) -> np.ndarray:
+    """Binary or text similarity matrix (simmatrix.py:173-202).
+
+    Asymmetry or a diagonal off 1 by more than SYMMETRY_TOL is a DataError; smaller
+    deviations are symmetrised exactly ((S + S.T) / 2, unit diagonal).
+    """
+    if _is_binary_matrix(path):
+        S = read_matrix_binary(path)
+    else:
+        try:
+            S = np.loadtxt(path, delimiter=None)
+        except ValueError:
+            S = np.loadtxt(path, delimiter=",")
+        S = np.atleast_2d(np.asarray(S, dtype=np.float64))
+    if S.ndim != 2 or S.shape[0] != S.shape[1]:
+        raise DataError(f"{path}: matrix must be square, got shape {S.shape}")
+    if np.isnan(S).any():
+        raise DataError(f"{path}: matrix contains NaN")
+    asym = float(np.abs(S - S.T).max())
+    if asym > SYMMETRY_TOL:
+        raise DataError(f"{path}: matrix asymmetry {asym:.3e} exceeds {SYMMETRY_TOL}")
+    S = (S + S.T) / 2.0
+    if np.abs(np.diag(S) - 1.0).max() > SYMMETRY_TOL:
+        raise DataError(f"{path}: diagonal entries must equal 1")
+    np.fill_diagonal(S, 1.0)
+    return validate_similarity(S)

@@ -1,10 +1,10 @@
 """TMFG construction on the B200 (drop-in for the heap builder of tmfgclust.tmfg).
 
 Mirrors tmfg.py:34-68 (BuildConfig, TmfgGraph, TraceError), 71-91 (clique,
-gain, edge_sum) and 344-451 (build_tmfg_heap, build_tmfg).  The insertion loop
-runs as one persistent CTA (csrc/tmfg.cu); S and the sorted rows never leave
-HBM.  The exact / corr builders of the reference are outside this tier's hot
-path and are not provided here.
+gain, edge_sum), 208-341 (build_tmfg_exact, build_tmfg_corr) and 344-451
+(build_tmfg_heap, build_tmfg).  The heap insertion loop runs as one persistent
+CTA cluster (csrc/tmfg.cu), the exact / corr builders as one persistent CTA
+(csrc/tmfg_variants.cu); S and the sorted rows never leave HBM.
 """
 
 from __future__ import annotations
@@ -225,12 +225,152 @@ def build_tmfg_heap(S, lists: SortedNeighborLists | None = None, config: BuildCo
     return g
 
 
+def _variant_device(variant: str, Sd, order_dev, clique_dev, prefix: int):
+    """tg_tmfg_exact / tg_tmfg_corr: device trace, edges, faces."""
+    t = D.torch()
+    n = int(Sd.shape[0])
+    trace = D.empty((max(n - 4, 0), 4), t.int32)
+    edges = D.empty((3 * n - 6, 2), t.int32)
+    faces = D.empty((2 * n - 4, 3), t.int32)
+    ws = D.Workspace.get(N.size("tg_tmfg_variant_workspace_bytes", n))
+    if variant == "exact":
+        N.call("tg_tmfg_exact", N.ptr(Sd), n, N.ptr(clique_dev), int(prefix), N.ptr(trace), N.ptr(edges),
+               N.ptr(faces), N.ptr(ws), ws.numel(), N.stream_ptr())
+    else:
+        N.call("tg_tmfg_corr", N.ptr(Sd), N.ptr(order_dev), n, N.ptr(clique_dev), int(prefix), N.ptr(trace),
+               N.ptr(edges), N.ptr(faces), N.ptr(ws), ws.numel(), N.stream_ptr())
+    return trace, edges, faces
+
+
+def _variant_graph(variant: str, S, Sd, order_dev, prefix: int) -> TmfgGraph:
+    n = int(Sd.shape[0])
+    clique = initial_clique_device(Sd)
+    trace, edges, faces = _variant_device(variant, Sd, order_dev, clique, prefix)
+    g = TmfgGraph(n=n, edges=edges, weights=edge_weights_device(Sd, edges), initial_clique=clique, trace=trace,
+                  faces=faces, variant=variant, S_device=Sd)
+    g._S_host = S
+    return g
+
+
+def build_tmfg_exact(S, config: BuildConfig | None = None) -> TmfgGraph:
+    """Prefix-based baseline: every live face tracks its true best vertex (tmfg.py:208-263), on the B200.
+
+    Bit-identical trace / edges / faces to the reference for every prefix_size.
+    """
+    config = config or BuildConfig(variant="exact")
+    shape = tuple(S.shape)
+    if len(shape) != 2 or shape[0] != shape[1]:
+        raise DataError(f"similarity matrix must be square, got shape {shape}")
+    if not D.is_device(S):
+        S = np.asarray(S, dtype=np.float64)
+    Sd = D.device_matrix(S)
+    validate_device(Sd)
+    return _variant_graph("exact", S, Sd, None, config.prefix_size)
+
+
+def build_tmfg_corr(S, lists: SortedNeighborLists, config: BuildConfig | None = None) -> TmfgGraph:
+    """Correlation-based builder with eager per-round refresh (tmfg.py:280-341), on the B200."""
+    config = config or BuildConfig(variant="corr")
+    shape = tuple(S.shape)
+    if len(shape) != 2 or shape[0] != shape[1]:
+        raise DataError(f"similarity matrix must be square, got shape {shape}")
+    if not D.is_device(S):
+        S = np.asarray(S, dtype=np.float64)
+    Sd = D.chained_device(lists, S)
+    validate_device(Sd)
+    if isinstance(lists, SortedNeighborLists):
+        order_dev = lists.order_device
+    else:
+        order_dev = D.to_device(np.asarray(lists.order, dtype=np.int32), D.torch().int32)
+    return _variant_graph("corr", S, Sd, order_dev, config.prefix_size)
+
+
 def build_tmfg(S, lists: SortedNeighborLists | None, config: BuildConfig) -> TmfgGraph:
-    """Dispatch (tmfg.py:439-451).  Only the heap variant is B200-accelerated."""
-    if config.variant != "heap":
-        raise NotImplementedError(
-            f"the {config.variant!r} builder is outside the accelerated path; "
-            "use the reference implementation (install() leaves it in place)")
+    """Dispatch to the configured builder; the exact variant ignores lists (tmfg.py:439-451)."""
+    if config.variant == "exact":
+        return build_tmfg_exact(S, config)
     if lists is None:
         raise ValueError(f"the {config.variant} builder needs sorted neighbor lists")
+    if config.variant == "corr":
+        return build_tmfg_corr(S, lists, config)
     return build_tmfg_heap(S, lists, config)
+
+
+# ------------------------------------------------------------------ trace replay and on-disk format (tmfg.py:454-516)
+def replay_trace(graph) -> tuple[set, set]:
+    """Re-run the insertion trace: (edge set, final live-face set); TraceError on a non-live host face."""
+    clique = [int(x) for x in np.asarray(graph.initial_clique)]
+    a, b, c, d = clique
+    edges = {(a, b), (a, c), (a, d), (b, c), (b, d), (c, d)}
+    live = {(a, b, c), (a, b, d), (a, c, d), (b, c, d)}
+    for row in np.asarray(graph.trace).reshape(-1, 4).tolist():
+        v, x, y, z = row
+        host = tuple(sorted((x, y, z)))
+        if host not in live:
+            raise TraceError(f"trace inserts {v} into non-live face {host}")
+        live.discard(host)
+        edges.update((min(q, v), max(q, v)) for q in host)
+        live.update(tuple(sorted(t)) for t in ((v, x, y), (v, x, z), (v, y, z)))
+    return edges, live
+
+
+def save_tmfg(graph, edges_path, trace_path) -> None:
+    """Edge list ("i j weight", weight as %.17g) and trace file (clique line, then "v a b c" lines)."""
+    e = np.asarray(graph.edges).reshape(-1, 2)
+    w = np.asarray(graph.weights, dtype=np.float64)
+    with open(edges_path, "w") as fh:
+        fh.writelines(f"{int(i)} {int(j)} {x:.17g}\n" for (i, j), x in zip(e.tolist(), w.tolist()))
+    with open(trace_path, "w") as fh:
+        fh.write(" ".join(str(int(v)) for v in np.asarray(graph.initial_clique)) + "\n")
+        fh.writelines(" ".join(str(v) for v in row) + "\n" for row in np.asarray(graph.trace).reshape(-1, 4).tolist())
+
+
+def load_tmfg(edges_path, trace_path) -> TmfgGraph:
+    """Rebuild a TmfgGraph from the two files; faces are the replayed live faces, sorted."""
+    from pathlib import Path
+
+    erows = [ln.split() for ln in Path(edges_path).read_text().splitlines() if ln.strip()]
+    tlines = [ln for ln in Path(trace_path).read_text().splitlines() if ln.strip()]
+    clique = np.array([int(x) for x in tlines[0].split()], dtype=np.int32)
+    trace = np.array([[int(x) for x in ln.split()] for ln in tlines[1:]], dtype=np.int32).reshape(-1, 4)
+    g = TmfgGraph(n=4 + trace.shape[0],
+                  edges=np.array([[int(r[0]), int(r[1])] for r in erows], dtype=np.int32).reshape(-1, 2),
+                  weights=np.array([float(r[2]) for r in erows], dtype=np.float64),
+                  initial_clique=clique, trace=trace, faces=np.zeros((0, 3), dtype=np.int32))
+    _, live = replay_trace(g)
+    g.faces = np.array(sorted(live), dtype=np.int32).reshape(-1, 3)
+    return g
+
+
+class TmfgState:
+    """Scan state of the list-based builders (tmfg.py:147-166): inserted flags, per-vertex
+    cursors into the sorted neighbour lists, cached best uninserted neighbours.
+
+    A host-side inspection object with the reference's fields (its tests drive it
+    directly); the GPU builders keep the same state in device memory.
+    """
+
+    def __init__(self, S, lists):
+        self.S = S
+        self.n = int(S.shape[0])
+        self.order = lists.order
+        self.cursors = [0] * self.n
+        self.inserted = bytearray(self.n)
+        self.max_corrs = [-1] * self.n
+        self.rem_count = self.n
+
+    def mark_inserted(self, v: int) -> None:
+        self.inserted[v] = 1
+        self.rem_count -= 1
+
+
+def refresh_max_corr(state: TmfgState, v: int) -> int:
+    """Advance v's cursor past inserted ids; cache and return the first uninserted one (tmfg.py:169-182)."""
+    row = state.order[v]
+    ins = state.inserted
+    cur = state.cursors[v]
+    while ins[int(row[cur])]:
+        cur += 1
+    state.cursors[v] = cur
+    state.max_corrs[v] = int(row[cur])
+    return state.max_corrs[v]

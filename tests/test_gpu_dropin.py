@@ -145,3 +145,21 @@ def test_in_place_edit_between_stage_calls_is_seen(oracle):
     w = p.to_weighted(g, S)
     wref = oracle.to_weighted(ref1, S)
     assert np.array_equal(w.lengths, wref["lengths"])
+
+
+def test_reference_compare_variants_under_install(ref, oracle, tmp_path):
+    """compare_variants (pipeline.py:295-315) through the reference's own driver: every builder,
+    including exact:3 and corr, runs on the B200 after install()."""
+    import json as _json
+    from paper_2408_09399_b200 import synth
+    var = _json.loads((REPO / "tests" / "golden" / "variants.json").read_text())["config1_pipeline"]
+    x, labels = synth.generate(1)
+    S = oracle.pearson_similarity(x)
+    path = tmp_path / "S.bin"
+    ref.simmatrix.write_matrix_binary(path, S)
+    cfg = ref.pipeline.PipelineConfig(input_path=str(path), input_format="matrix", k=5)
+    rows = ref.pipeline.compare_variants(cfg, ["exact:3", "corr", "heap"])
+    for row in rows:
+        name, p = ref.pipeline.parse_variant_token(row["variant"])
+        assert row["report"].digest == var[f"{name}_p{p}"]["digest"]
+        assert row["edge_sum_delta"] == var[f"{name}_p{p}"]["edge_sum_delta"]

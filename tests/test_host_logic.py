@@ -78,7 +78,10 @@ def test_pipeline_config_validation():
     with pytest.raises(ValueError):
         PipelineConfig(apsp_mode="exact", hub_count=3)
     with pytest.raises(ValueError):
-        PipelineConfig(variant="exact")
+        PipelineConfig(variant="nope")
+    with pytest.raises(ValueError):
+        PipelineConfig(prefix_size=0)
+    PipelineConfig(variant="exact", prefix_size=7)
     PipelineConfig(apsp_mode="hub", hub_count=3, radius_factor=1.5, k=4)
 
 
