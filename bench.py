@@ -314,7 +314,7 @@ def run_b200(args, world, rank, local):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(cfg, n, L, mode, k),
             "stage_ms": {kk: round(float(np.mean(vv)), 3) for kk, vv in stage.items()},
-            "roofline": {"bound": "hbm", "kernel": "row_sort_fk_kernel (per-row neighbour sort)",
+            "roofline": {"bound": "hbm", "kernel": "row_sort_v2_kernel (per-row neighbour sort)",
                          "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                          "frac": round(achieved / hbm_peak, 4), "traffic": traffic, "traffic_kernel": traffic_src,
                          "algorithmic_bytes": sort_bytes, "kernel_ms": round(sort_avg, 4),

@@ -163,7 +163,6 @@ tmfg_variant_kernel(const double *__restrict__ S, const int32_t *__restrict__ or
     __syncthreads();
     int rem = n - 4, ntrace = 0, nedge = 6;
     int round = 0;
-    bool first = true;
     while (rem > 0) {
         // ---- update the listed faces (round 0: the four clique faces)
         const int nlist = s_nlist;
@@ -232,10 +231,6 @@ tmfg_variant_kernel(const double *__restrict__ S, const int32_t *__restrict__ or
             }
             __syncthreads();
         }
-        if (!first) {
-            // (nothing: the round's insertions happened before the update)
-        }
-        first = false;
         // ---- select (tmfg.py:185-205)
         const int nf = s_nf;
         const int want = prefix < rem ? prefix : rem;
@@ -383,7 +378,7 @@ size_t carve_bytes(int64_t n) {
 template <int V>
 int launch(const double *S, const int32_t *order, int64_t n, const int32_t *clique, int64_t prefix, int32_t *trace,
            int32_t *edges, int32_t *faces, void *ws, size_t ws_bytes, void *stream) {
-    if (!S || !clique || !trace || !edges || !faces || n < 4 || prefix < 1) return TG_ERR_ARG;
+    if (!S || !clique || (n > 4 && !trace) || !edges || !faces || n < 4 || prefix < 1) return TG_ERR_ARG;
     if (V == 1 && !order) return TG_ERR_ARG;
     if (n > (int64_t)INT_MAX / 3) return TG_ERR_ARG;
     if (!ws || ws_bytes < carve_bytes(n)) return TG_ERR_WORKSPACE;
