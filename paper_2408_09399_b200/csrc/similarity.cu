@@ -16,6 +16,10 @@
 //     clamp to [-1, 1].
 #include "common.cuh"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cstdlib>
+
 namespace {
 
 constexpr int PBM = 128;          // tile rows / cols
@@ -189,6 +193,168 @@ syrk_dmma_kernel(const double *__restrict__ Xc, const double *__restrict__ inv, 
     }
 }
 
+
+// ---------------------------------------------------------------- TMA-fed SYRK
+// Same tiling and fused epilogue as syrk_dmma_kernel; the operand panels arrive by TMA
+// (cp.async.bulk.tensor.2d over a tensor map of Xc, 128 rows x 16 doubles = one 128-byte
+// swizzled row per Xc row) into a 4-stage mbarrier ring instead of 4,096 cp.async per
+// panel.  The 128-byte swizzle (16-byte chunk c of row r at c ^ (r & 7)) lets a lane read
+// its fragment pair for two k-steps with one conflict-free 16-byte load: lane (fr, fc)
+// takes k = 4 fc + s in k-step s (A and B alike), so steps 2h and 2h+1 need chunk 2 fc + h.
+// Out-of-range rows (n not a multiple of 128) are zero-filled by the TMA unit.
+constexpr int TS_STAGES = 4;
+constexpr int TS_PANEL = PBM * PBK;   // doubles per operand panel (16 KB)
+
+__device__ __forceinline__ unsigned ts_smem(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__global__ void __launch_bounds__(PTHREADS, 1)
+syrk_tma_kernel(const __grid_constant__ CUtensorMap tmX, const double *__restrict__ inv, int64_t n, int64_t Lp,
+                double *__restrict__ S) {
+    extern __shared__ __align__(16) unsigned char ts_raw[];
+    __shared__ __align__(8) uint64_t bar[TS_STAGES];
+    // the swizzled boxes need 1024-byte aligned destinations
+    double *base = reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(ts_raw) + 1023) & ~(uintptr_t)1023);
+    const int64_t nb = (n + PBM - 1) / PBM;
+    int64_t I, J;
+    tile_of(blockIdx.x, nb, I, J);
+    const int64_t i0 = I * PBM, j0 = J * PBM;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp >> 2, wn = warp & 3;
+    const int nk = (int)(Lp / PBK);
+    if (tid == 0) {
+        for (int s = 0; s < TS_STAGES; s++)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(ts_smem(&bar[s])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int kt) {   // thread 0: both operand panels of k-tile kt
+        const int s = kt % TS_STAGES;
+        double *as = base + (size_t)s * 2 * TS_PANEL, *bs = as + TS_PANEL;
+        const unsigned b = ts_smem(&bar[s]);
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(2u * TS_PANEL * 8u)
+                     : "memory");
+        const int k0 = kt * PBK;
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+                ts_smem(as)),
+            "l"(&tmX), "r"(k0), "r"((int)i0), "r"(b)
+            : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+                ts_smem(bs)),
+            "l"(&tmX), "r"(k0), "r"((int)j0), "r"(b)
+            : "memory");
+    };
+    if (tid == 0)
+        for (int kt = 0; kt < TS_STAGES - 1 && kt < nk; kt++) issue(kt);
+
+    double acc[8][4][2];
+#pragma unroll
+    for (int a = 0; a < 8; a++)
+#pragma unroll
+        for (int b = 0; b < 4; b++) acc[a][b][0] = acc[a][b][1] = 0.0;
+    const int fr = lane >> 2, fc = lane & 3;
+    for (int kt = 0; kt < nk; kt++) {
+        __syncthreads();   // k-tile kt-1 is consumed: its stage may be refilled
+        if (tid == 0 && kt + TS_STAGES - 1 < nk) issue(kt + TS_STAGES - 1);
+        const int s = kt % TS_STAGES;
+        {
+            const unsigned b = ts_smem(&bar[s]), par = (unsigned)((kt / TS_STAGES) & 1);
+            asm volatile(
+                "{\n .reg .pred p;\n TS_W_%=:\n"
+                " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                " @!p bra TS_W_%=;\n}\n" ::"r"(b),
+                "r"(par)
+                : "memory");
+        }
+        const double *as = base + (size_t)s * 2 * TS_PANEL + (wm * 64) * PBK;
+        const double *bs = base + (size_t)s * 2 * TS_PANEL + TS_PANEL + (wn * 32) * PBK;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int ch = ((2 * fc + h) ^ fr) * 2;   // swizzled 16-byte chunk of rows 8q + fr
+            double2 af[8], bf[4];
+#pragma unroll
+            for (int a = 0; a < 8; a++) af[a] = *reinterpret_cast<const double2 *>(as + (a * 8 + fr) * PBK + ch);
+#pragma unroll
+            for (int b = 0; b < 4; b++) bf[b] = *reinterpret_cast<const double2 *>(bs + (b * 8 + fr) * PBK + ch);
+#pragma unroll
+            for (int a = 0; a < 8; a++)
+#pragma unroll
+                for (int b = 0; b < 4; b++) dmma(acc[a][b][0], acc[a][b][1], af[a].x, bf[b].x);
+#pragma unroll
+            for (int a = 0; a < 8; a++)
+#pragma unroll
+                for (int b = 0; b < 4; b++) dmma(acc[a][b][0], acc[a][b][1], af[a].y, bf[b].y);
+        }
+    }
+    __syncthreads();   // every panel consumed: the ring becomes the epilogue tile
+
+    // ---- epilogue: scale, zero-norm, clamp into the smem tile T[128][129]
+    double *T = base;
+#pragma unroll
+    for (int a = 0; a < 8; a++) {
+        const int r = wm * 64 + a * 8 + fr;
+        const int64_t gi = i0 + r;
+        const double ii = gi < n ? inv[gi] : 0.0;
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int c = wn * 32 + b * 8 + fc * 2 + h;
+                const int64_t gj = j0 + c;
+                const double jj = gj < n ? inv[gj] : 0.0;
+                double v;
+                if (ii == 0.0 || jj == 0.0) {
+                    v = 0.0;
+                } else {
+                    v = acc[a][b][h] * ii * jj;
+                    v = v > 1.0 ? 1.0 : (v < -1.0 ? -1.0 : v);
+                }
+                T[r * TSTR + c] = v;
+            }
+        }
+    }
+    __syncthreads();
+    const bool diag = (I == J);
+    // rows of the I block, two columns per store when the row start is 16-byte aligned
+    const bool vec = ((n & 1) == 0);
+    for (int e = tid; e < PBM * PBM / 2; e += PTHREADS) {
+        const int r = e / (PBM / 2), c = 2 * (e % (PBM / 2));
+        const int64_t gi = i0 + r, gj = j0 + c;
+        if (gi >= n || gj >= n) continue;
+        double v0, v1;
+        if (!diag) {
+            v0 = T[r * TSTR + c];
+            v1 = T[r * TSTR + c + 1];
+        } else {
+            v0 = r < c ? T[r * TSTR + c] : (r == c ? 1.0 : T[c * TSTR + r]);
+            v1 = r < c + 1 ? T[r * TSTR + c + 1] : (r == c + 1 ? 1.0 : T[(c + 1) * TSTR + r]);
+        }
+        if (vec && gj + 1 < n) {
+            *reinterpret_cast<double2 *>(S + gi * n + gj) = make_double2(v0, v1);
+        } else {
+            S[gi * n + gj] = v0;
+            if (gj + 1 < n) S[gi * n + gj + 1] = v1;
+        }
+    }
+    if (!diag) {
+        // mirrored rows of the J block: S[j0 + c][i0 + r] = T[r][c], two rows r per store
+        for (int e = tid; e < PBM * PBM / 2; e += PTHREADS) {
+            const int c = e / (PBM / 2), r = 2 * (e % (PBM / 2));
+            const int64_t gi = i0 + r, gj = j0 + c;
+            if (gi >= n || gj >= n) continue;
+            const double v0 = T[r * TSTR + c], v1 = T[(r + 1) * TSTR + c];
+            if (vec && gi + 1 < n) {
+                *reinterpret_cast<double2 *>(S + gj * n + gi) = make_double2(v0, v1);
+            } else {
+                S[gj * n + gi] = v0;
+                if (gi + 1 < n) S[gj * n + gi + 1] = v1;
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------- validation
 __global__ void validate_kernel(const double *__restrict__ S, int64_t n, int32_t *flags) {
     __shared__ double A[32][33];
@@ -307,6 +473,29 @@ __global__ void __launch_bounds__(256) pearson_refexact_kernel(const double *__r
 
 }  // namespace
 
+// Tensor map of the centred, padded series Xc (n rows of Lp doubles): 128 x 16 boxes, 128-byte
+// swizzle, zero fill past row n.  cuTensorMapEncodeTiled comes from the driver through the
+// runtime's entry-point query (no libcuda link).  Returns 0 on success.
+static int tg_tensor_map_xc(CUtensorMap *tm, const double *Xc, int64_t n, int64_t Lp) {
+    static PFN_cuTensorMapEncodeTiled encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void *fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return 1;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+    }
+    const cuuint64_t dims[2] = {(cuuint64_t)Lp, (cuuint64_t)n};
+    const cuuint64_t strides[1] = {(cuuint64_t)Lp * sizeof(double)};
+    const cuuint32_t box[2] = {(cuuint32_t)PBK, (cuuint32_t)PBM};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(Xc), dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : 2;
+}
+
 TG_API size_t tg_pearson_workspace_bytes(int64_t n, int64_t L) {
     int64_t Lp = (L + PBK - 1) / PBK * PBK;
     return tg_align_up((size_t)n * Lp * sizeof(double), 256) + tg_align_up((size_t)n * sizeof(double), 256) + 512;
@@ -328,6 +517,17 @@ TG_API int tg_pearson_f64(const double *X, int64_t n, int64_t L, double *S, void
     size_t smem = (size_t)2 * PSTAGES * PBM * PSTR * sizeof(double);
     size_t smem_epi = (size_t)PBM * TSTR * sizeof(double);
     if (smem_epi > smem) smem = smem_epi;
+    static const bool use_cp_async = std::getenv("TG_SYRK_CPASYNC") != nullptr;   // A/B switch (development)
+    CUtensorMap tm;
+    if (!use_cp_async && n <= INT_MAX && tg_tensor_map_xc(&tm, Xc, n, Lp) == 0) {
+        size_t tsm = (size_t)TS_STAGES * 2 * TS_PANEL * sizeof(double);
+        if (smem_epi > tsm) tsm = smem_epi;
+        tsm += 1024;   // alignment slack for the swizzled boxes
+        TG_CUDA_CHECK(cudaFuncSetAttribute(syrk_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+        syrk_tma_kernel<<<(unsigned)tiles, PTHREADS, tsm, st>>>(tm, inv, n, Lp, S); tg_count_launch(1);
+        TG_LAUNCH_CHECK();
+        return TG_OK;
+    }
     // per call: the attribute is per device, and a cached flag would skip a second device
     TG_CUDA_CHECK(cudaFuncSetAttribute(syrk_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     syrk_dmma_kernel<<<(unsigned)tiles, PTHREADS, smem, st>>>(Xc, inv, n, Lp, S); tg_count_launch(1);
