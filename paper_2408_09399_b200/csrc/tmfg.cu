@@ -713,7 +713,8 @@ __device__ __forceinline__ bool kgt(double g1, int f1, double g2, int f2) {
 // the first i where L[i] is fresh or is beaten by the running max of the
 // refreshed entries or by the best new entry: a prefix max + a ballot.
 __device__ void replay_warp(const TmArgs &A, Ctl &ctl, const Ent *L, const Ent *Lref, const int *Lstale,
-                            const Ent *NE, Ent *batch, Ent *tobuf, double *kg, int *kf, int *ksrc) {
+                            const Ent *NE, Ent *batch, Ent *tobuf, double *kg, int *kf, int *ksrc, double *tkg,
+                            int *tkf) {
     const int lane = threadIdx.x & 31;
     const int Lc = ctl.L_count, nec = ctl.ne_count;
     // best new entry (<= 4, every lane)
@@ -848,6 +849,8 @@ __device__ void replay_warp(const TmArgs &A, Ctl &ctl, const Ent *L, const Ent *
         for (int j = 0; j < nbuf; j++) r += kgt(kg[j], kf[j], g, f);
         const int sidx = ksrc[k];
         tobuf[r] = sidx >= 0 ? Lref[sidx] : NE[~sidx];
+        tkg[r] = g;   // compact sorted keys for the merge's searches
+        tkf[r] = f;
     }
     __syncwarp();
 }
@@ -1101,6 +1104,8 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
     __shared__ Ent red_e[TM_WARPS];
     __shared__ double rk_g[TM_BATCH];
     __shared__ int rk_f[TM_BATCH], rk_src[TM_BATCH];
+    __shared__ double tk_g[TM_BATCH];   // tobuf's keys (gain, fid), sorted
+    __shared__ int tk_f[TM_BATCH];
     __shared__ int red_ok[TM_WARPS];
     __shared__ RcEnt rcache[TM_RC];
     __shared__ int rc_claim[TM_RC];   // round that last wrote the slot: one writer per slot per round
@@ -1112,6 +1117,8 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
     uint32_t *bits = reinterpret_cast<uint32_t *>(buf1 + QB);
     const int nwords = (n + 31) >> 5;
     unsigned long long *vst = reinterpret_cast<unsigned long long *>(bits + ((nwords + 1) & ~1));
+    // merge scratch: # re-pushed entries popping before each old queue entry (QB shorts)
+    short *mlo = reinterpret_cast<short *>(reinterpret_cast<unsigned char *>(vst) + (SMEM_ST ? (size_t)n * 8 : 0));
 
     namespace cg = cooperative_groups;
     const unsigned ncl = cg::this_cluster().num_blocks(), crank = cg::this_cluster().block_rank();
@@ -1313,7 +1320,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
         // it, so the first to claim a slot writes it.  The winner's bit is set while
         // the speculative refreshes run: they stay exact (every fact they use is
         // monotone) and the cache's candidate check rejects what the winner voids.
-        if (warp == 0) replay_warp(A, ctl, L, Lref, Lstale, NE, batch, tobuf, rk_g, rk_f, rk_src);
+        if (warp == 0) replay_warp(A, ctl, L, Lref, Lstale, NE, batch, tobuf, rk_g, rk_f, rk_src, tk_g, tk_f);
         else if (!A.check && (warp == 1 || warp >= MW)) {
             const int round = (int)ctl.rounds;
             if (warp == 1) {
@@ -1391,8 +1398,8 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
         // while thread 0 inserts the winner and settles the queue size: both only
         // depend on the replay's results, so one barrier closes the round
         {
-            const int r = ctl.removed, sz = ctl.size, nb = ctl.nbuf_new;
-            // thread 0 rewrites ctl.size / sel / L_count below: every merge warp has its copy first
+            const int r = ctl.removed, sz = ctl.size, nb = ctl.nbuf_new, pc0 = ctl.pool_count;
+            // thread 0 rewrites ctl.size / sel / L_count / pool_count below: every merge warp has its copy first
             asm volatile("bar.sync 2, %0;" ::"r"(MW * 32) : "memory");
             if (warp > 0) {
                 Ent *cur = sel ? buf1 : buf0;
@@ -1400,39 +1407,64 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
                 const int old = sz - r;
                 const int mt = tid - 32;
                 constexpr int MT = MW * 32 - 32;
+                // Positions >= QB spill to the pool.  They are the merged sequence's tail, so
+                // the spill at position p takes pool slot pc0 + (p - QB): no atomics here
+                // (thread 0 settles pool_count and the pool's minimum key, the key of the
+                // sequence's last entry); the entry at exactly QB becomes the pool maximum.
+                auto place = [&](const Ent &x, int pos) {
+                    if (pos < QB) {
+                        nxt[pos] = x;
+                    } else {
+                        const int idx = pc0 + (pos - QB);
+                        A.pool_g[idx] = x.g;
+                        A.pool_fc[idx] = make_int2(x.fid, x.cand);
+                        if (pos == QB) { ctl.pool_max = x; ctl.pool_has_max = 1; }
+                    }
+                };
+                // old entry i -> i + lo_i (lo_i = # re-pushed entries popping before it); the
+                // re-pushed entries k in [lo_{i-1}, lo_i) sit right before it, at k + i, and the
+                // ones after the last old entry at k + old: one short search per old entry, the
+                // lo_i exchanged through shared memory (no search of the long old run)
                 for (int i = mt; i < old; i += MT) {
                     Ent x = cur[r + i];
                     int lo = 0, hi = nb;  // # of tobuf entries popping before x
                     while (lo < hi) {
                         int mid = (lo + hi) >> 1;
-                        if (ent_gt(tobuf[mid], x)) lo = mid + 1;
+                        if (kgt(tk_g[mid], tk_f[mid], x.g, x.fid)) lo = mid + 1;
                         else hi = mid;
                     }
-                    int pos = i + lo;
-                    if (pos < QB) nxt[pos] = x;
-                    else {
-                        pool_put(A, &ctl.pool_minkey, atomicAdd(&ctl.pool_count, 1), x);
-                        if (pos == QB) { ctl.pool_max = x; ctl.pool_has_max = 1; }
-                    }
+                    place(x, i + lo);
+                    mlo[i] = (short)lo;
                 }
-                for (int k = mt; k < nb; k += MT) {
-                    Ent x = tobuf[k];
-                    int lo = 0, hi = old;  // # of old entries popping before x
-                    while (lo < hi) {
-                        int mid = (lo + hi) >> 1;
-                        if (ent_gt(cur[r + mid], x)) lo = mid + 1;
-                        else hi = mid;
+                if (nb > 0) {
+                    asm volatile("bar.sync 3, %0;" ::"r"(MT) : "memory");
+                    for (int i = mt; i < old; i += MT) {
+                        const int lo = mlo[i], lp = i > 0 ? mlo[i - 1] : 0;
+                        for (int k = lp; k < lo; k++) place(tobuf[k], k + i);
+                        if (i == old - 1)
+                            for (int k = lo; k < nb; k++) place(tobuf[k], k + old);
                     }
-                    int pos = k + lo;
-                    if (pos < QB) nxt[pos] = x;
-                    else {
-                        pool_put(A, &ctl.pool_minkey, atomicAdd(&ctl.pool_count, 1), x);
-                        if (pos == QB) { ctl.pool_max = x; ctl.pool_has_max = 1; }
-                    }
+                    if (old == 0)
+                        for (int k = mt; k < nb; k += MT) place(tobuf[k], k);
                 }
             } else if (lane == 0) {
+#if TM_PROFILE
+                long long tin0 = clock64();
+#endif
                 // spilled entries (total > B) are the smallest of the buffer; then no refill
                 const int total = min(sz - r + nb, QB);
+                const int spill = sz - r + nb - total;
+                if (spill > 0) {
+                    // the merged sequence's last entry: the later-popping of the two runs' tails
+                    const Ent *curq = sel ? buf1 : buf0;
+                    double lg;
+                    if (nb == 0) lg = curq[sz - 1].g;
+                    else if (sz - r == 0) lg = tobuf[nb - 1].g;
+                    else lg = ent_gt(curq[sz - 1], tobuf[nb - 1]) ? tobuf[nb - 1].g : curq[sz - 1].g;
+                    const unsigned long long lk = tg_order_key(lg);
+                    if (lk < ctl.pool_minkey) ctl.pool_minkey = lk;
+                    ctl.pool_count += spill;
+                }
                 ctl.size = total;
                 ctl.sel = sel ^ 1;
                 ctl.need_refill = total < TM_K && ctl.pool_count > 0;
@@ -1475,6 +1507,9 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
                     else ctl.ne_count = 3;
                 }
                 if (ctl.bad) ctl.done = 1;
+#if TM_PROFILE
+                ctl.t_insert += clock64() - tin0;
+#endif
             }
         }
         }
@@ -1573,6 +1608,7 @@ size_t tm_smem_bytes(int64_t n, bool smem_st) {
     size_t b = (size_t)2 * (smem_st ? tm_qb<true>() : tm_qb<false>()) * sizeof(Ent);
     b += (size_t)(((n + 31) / 32 + 1) & ~1LL) * 4;
     if (smem_st) b += (size_t)n * 8;
+    b += (size_t)(smem_st ? tm_qb<true>() : tm_qb<false>()) * sizeof(short);   // merge scratch
     return tg_align_up(b, 16) + 64;
 }
 
