@@ -134,3 +134,34 @@ def test_pipeline_config5_50k(pkg):
     assert report.digest == rec["hub_digest"]
     assert orc.sha(np.asarray(flat, dtype=np.int64)) == rec["hub_labels"]
     assert report.num_converging == rec["hub_num_converging"]
+
+
+def test_nan_is_stage_error_tmfg_insertion(pkg):
+    """pipeline.py:149-153 + test_pipeline.py:116-120: a NaN in S surfaces as
+    StageError('tmfg_insertion') (the sort accepts it; validation inside the TMFG stage raises)."""
+    rng = np.random.default_rng(12)
+    A = rng.random((60, 60))
+    S = (A + A.T) / 2
+    np.fill_diagonal(S, 1.0)
+    S[5, 9] = S[9, 5] = np.nan
+    with pytest.raises(pkg.StageError) as ei:
+        pkg.run_stages(pkg.PipelineConfig(k=3), S)
+    assert ei.value.stage == "tmfg_insertion"
+    assert isinstance(ei.value.cause, pkg.DataError)
+    assert str(ei.value.cause) == "similarity matrix contains NaN"
+
+
+@pytest.mark.parametrize("n", [4, 5, 6])
+def test_degenerate_sizes_through_the_pipeline(n, pkg):
+    """n = 4 (no insertion), 5, 6 through every stage of both APSP modes, against the
+    exhaustive-free structural invariants: 3n-6 edges, 2n-4 faces, n-1 merges."""
+    rng = np.random.default_rng(n)
+    A = rng.random((n, n))
+    S = (A + A.T) / 2
+    np.fill_diagonal(S, 1.0)
+    for mode in ("exact", "hub"):
+        report, g, d, flat = pkg.run_stages(pkg.PipelineConfig(apsp_mode=mode, k=2), S)
+        assert g.edges.shape == (3 * n - 6, 2) and g.faces.shape == (2 * n - 4, 3)
+        assert d.n_merges == n - 1
+        d.validate()
+        assert flat.shape == (n,) and flat.max() == 1
