@@ -13,6 +13,9 @@
 // by max into the (group x group) matrix.  Tiles of 64x64 pairs, hub columns
 // staged in shared memory 32 hubs at a time, 4x4 register micro-tiles.
 #include "common.cuh"
+
+#include <cooperative_groups.h>
+#include <cstdlib>
 #include <cstdlib>
 
 namespace {
@@ -718,6 +721,10 @@ __global__ void oracle_block_kernel(tg_oracle_t o, const int32_t *rows, int64_t 
 // and two barriers.  The value at the chain's second-to-last entry -- needed by
 // the tie rule -- is captured during the scan instead of re-read.
 constexpr int NN_SMEM_MAX = 7168;
+constexpr int NN_CL = 8;          // cluster NN-chain (below): CTAs per cluster
+constexpr int NN_CL_T = 256;      //   threads per CTA
+constexpr int NN_CL_MIN = 2048;   //   matrices with NN_CL_MIN <= m <= NN_SMEM_MAX (HBM-resident rows;
+                                  //   L2-resident smaller ones step faster in one CTA)
 constexpr int NN_BIG = 2048;   // larger matrices: 1024 threads, 8 row entries in flight per thread
 #ifndef NN_SMALL_T_DEF
 #define NN_SMALL_T_DEF 512
@@ -729,7 +736,8 @@ template <int NN_CTA_T, int NN_U>
 __global__ void __launch_bounds__(NN_CTA_T)
 nn_chain_cta_kernel(double *mats, const int64_t *mat_off, const int64_t *sizes, int64_t count,
                     const int64_t *merge_off, int64_t *lefts, int64_t *rights, double *heights,
-                    uint8_t *active_all, int64_t *slot_all, int64_t *chain_all, const int64_t *aux_off) {
+                    uint8_t *active_all, int64_t *slot_all, int64_t *chain_all, const int64_t *aux_off,
+                    int cl_min) {
     extern __shared__ __align__(16) unsigned char nn_smem[];
     __shared__ double rv[NN_CTA_T / 32];
     __shared__ int ri[NN_CTA_T / 32];
@@ -743,6 +751,7 @@ nn_chain_cta_kernel(double *mats, const int64_t *mat_off, const int64_t *sizes, 
     for (int64_t b = blockIdx.x; b < count; b += gridDim.x) {
         const int64_t m64 = sizes[b];
         if (m64 <= NN_WARP_MAX || (NN_CTA_T == 1024) != (m64 > NN_BIG)) continue;
+        if (cl_min > 0 && m64 >= cl_min && m64 <= NN_SMEM_MAX) continue;   // the cluster kernel's
         const int m = (int)m64;
         double *W = mats + mat_off[b];
         int64_t *L = lefts + merge_off[b], *R = rights + merge_off[b];
@@ -877,6 +886,164 @@ nn_chain_cta_kernel(double *mats, const int64_t *mat_off, const int64_t *sizes, 
             }
         }
         __syncthreads();
+    }
+}
+
+
+// ------------------------------------------------------------ NN-chain over a thread-block cluster
+// For the large matrices (m >= NN_CL_MIN: layer 3 at n = 50k has m = 5906, layer 2 at n = 10k
+// up to ~1000) one chain step was one CTA reading a whole row (47 KB at m = 5906) through one
+// SM.  Here a cluster of NN_CL CTAs runs one chain: CTA c owns the columns [c m / NN_CL,
+// (c + 1) m / NN_CL) of every row.  Per step each CTA scans its slice of row x, reduces it,
+// and writes its partial (min value, first index, and W[x, chain[-2]] if it owns that
+// column) into every CTA's shared memory (DSMEM; double-buffered by step parity); after one
+// cluster barrier every CTA reduces the same partials in the same order, so all of them take
+// the same decision and keep identical chain / activity state (linkage.py:50-94 semantics:
+// first index on ties, chain[-2] preferred on an equal value, all-inf row -> index 0).  A merge
+// updates row lo and column lo slice by slice (each CTA its own columns and its own rows) and
+// ends with a second barrier; W is read through L2 (ld.global.cg) so no CTA sees a stale line.
+
+struct NnPart {
+    double v, rp;
+    int i, has_p;
+};
+
+__device__ __forceinline__ void nn_cl_barrier() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+__global__ void __launch_bounds__(NN_CL_T)
+nn_chain_cluster_kernel(double *mats, const int64_t *mat_off, const int64_t *sizes, int64_t count,
+                        const int64_t *merge_off, int64_t *lefts, int64_t *rights, double *heights, int cl_min) {
+    extern __shared__ __align__(16) unsigned char ncl_smem[];
+    __shared__ NnPart part[2][NN_CL];
+    __shared__ double rv[NN_CL_T / 32], rpv[NN_CL_T / 32];
+    __shared__ int ri[NN_CL_T / 32], rph[NN_CL_T / 32];
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    const int crank = (int)cl.block_rank();
+    const int64_t cid = blockIdx.x / NN_CL, ncl = gridDim.x / NN_CL;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = NN_CL_T / 32;
+    int32_t *chain = reinterpret_cast<int32_t *>(ncl_smem);
+    int32_t *slot = chain + NN_SMEM_MAX;
+    uint8_t *act = reinterpret_cast<uint8_t *>(slot + NN_SMEM_MAX);
+    for (int64_t b = cid; b < count; b += ncl) {
+        const int m = (int)sizes[b];
+        if (m < cl_min || m > NN_SMEM_MAX) continue;
+        double *W = mats + mat_off[b];
+        int64_t *L = lefts + merge_off[b], *R = rights + merge_off[b];
+        double *Hh = heights + merge_off[b];
+        const int c0 = (int)((int64_t)crank * m / NN_CL), c1 = (int)((int64_t)(crank + 1) * m / NN_CL);
+        for (int i = tid; i < m; i += NN_CL_T) {
+            act[i] = 1;
+            slot[i] = i;
+        }
+        for (int i = c0 + tid; i < c1; i += NN_CL_T) W[(int64_t)i * m + i] = INFINITY;   // linkage.py:61
+        __syncthreads();
+        nn_cl_barrier();
+        int nchain = 0, remaining = m, nm = 0, first = 0, step = 0;
+        int next_id = m;
+        bool cycled = false;
+        while (remaining > 1) {
+            if (nchain == 0) {
+                while (!act[first]) first++;   // the first active slot only moves forward
+                chain[0] = first;
+                nchain = 1;
+            }
+            const int x = chain[nchain - 1];
+            const int p = nchain > 1 ? chain[nchain - 2] : -1;
+            const double *row = W + (int64_t)x * m;
+            double bv = INFINITY, rp = INFINITY;
+            int bi = INT_MAX, hp = 0;
+            for (int j = c0 + tid; j < c1; j += NN_CL_T) {
+                const double r = (act[j] && j != x) ? __ldcg(row + j) : INFINITY;
+                if (r < bv || (r == bv && j < bi)) { bv = r; bi = j; }
+                if (j == p) { rp = r; hp = 1; }
+            }
+            for (int o = 16; o; o >>= 1) {
+                const double r2 = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (r2 < bv || (r2 == bv && i2 < bi)) { bv = r2; bi = i2; }
+                const double p2 = __shfl_xor_sync(0xffffffffu, rp, o);
+                const int h2 = __shfl_xor_sync(0xffffffffu, hp, o);
+                if (h2) { rp = p2; hp = 1; }
+            }
+            if (lane == 0) { rv[warp] = bv; ri[warp] = bi; rpv[warp] = rp; rph[warp] = hp; }
+            __syncthreads();
+            const int par = step & 1;
+            if (warp == 0) {
+                double v = lane < NW ? rv[lane] : INFINITY;
+                int i = lane < NW ? ri[lane] : INT_MAX;
+                double q = lane < NW ? rpv[lane] : INFINITY;
+                int h = lane < NW ? rph[lane] : 0;
+                for (int o = 16; o; o >>= 1) {
+                    const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+                    const int i2 = __shfl_xor_sync(0xffffffffu, i, o);
+                    if (v2 < v || (v2 == v && i2 < i)) { v = v2; i = i2; }
+                    const double q2 = __shfl_xor_sync(0xffffffffu, q, o);
+                    const int h2 = __shfl_xor_sync(0xffffffffu, h, o);
+                    if (h2) { q = q2; h = 1; }
+                }
+                if (lane < NN_CL) {   // this CTA's partial into CTA `lane`'s slot crank (DSMEM)
+                    NnPart *dst = cl.map_shared_rank(&part[par][crank], (unsigned)lane);
+                    dst->v = v;
+                    dst->i = i;
+                    dst->rp = q;
+                    dst->has_p = h;
+                }
+            }
+            nn_cl_barrier();
+            // every CTA reduces the same partials in the same order: identical decisions
+            double v = INFINITY, q = INFINITY;
+            int i = INT_MAX;
+            for (int c = 0; c < NN_CL; c++) {
+                const NnPart &pp = part[par][c];
+                if (pp.v < v || (pp.v == v && pp.i < i)) { v = pp.v; i = pp.i; }
+                if (pp.has_p) q = pp.rp;
+            }
+            step++;
+            int y = v == INFINITY ? 0 : i;   // np.argmin: first index of the minimum (an all-inf row: 0)
+            if (p >= 0 && q == v) y = p;   // linkage.py:76-77
+            if (p >= 0 && y == p) {
+                nchain -= 2;
+                const int lo = x < y ? x : y, hi = x < y ? y : x;
+                if (crank == 0 && tid == 0) {
+                    L[nm] = slot[x];
+                    R[nm] = slot[y];
+                    Hh[nm] = q;   // W[x, y] with y = chain[-2]
+                }
+                nm++;
+                double *Wlo = W + (int64_t)lo * m;
+                const double *Whi = W + (int64_t)hi * m;
+                for (int j = c0 + tid; j < c1; j += NN_CL_T) {
+                    const double a = __ldcg(Wlo + j), c = __ldcg(Whi + j);
+                    const double mg = a > c ? a : (c > a ? c : a);
+                    Wlo[j] = mg;                      // row lo, own columns
+                    W[(int64_t)j * m + lo] = mg;      // column lo, own rows
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    if (lo >= c0 && lo < c1) Wlo[lo] = INFINITY;
+                    act[hi] = 0;
+                    slot[lo] = next_id;
+                }
+                next_id++;
+                remaining--;
+                __syncthreads();
+                nn_cl_barrier();   // the merged row / column are visible to every CTA
+            } else {
+                if (nchain >= m) { cycled = true; break; }
+                __syncthreads();   // every thread has read chain[] before it grows
+                if (tid == 0) chain[nchain] = y;
+                nchain++;
+                __syncthreads();
+            }
+        }
+        if (cycled && crank == 0 && tid == 0) Hh[0] = __longlong_as_double(0x7ff8dead00000000ll);
+        __syncthreads();
+        nn_cl_barrier();   // the cluster's shared state is reused by its next matrix
     }
 }
 
@@ -1087,12 +1254,51 @@ TG_API int tg_nn_chain_batch(double *mats, const int64_t *mat_off, const int64_t
                                        (int)nn_smem));
     TG_CUDA_CHECK(cudaFuncSetAttribute(nn_chain_cta_kernel<1024, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)nn_smem));
+    // matrices with cl_min <= m <= NN_SMEM_MAX take the cluster chain (TG_NN_CLMIN: development knob, 0 = off)
+    static const int cl_min = std::getenv("TG_NN_CLMIN") ? std::atoi(std::getenv("TG_NN_CLMIN")) : NN_CL_MIN;
+    const int cl_on = cl_min > 0;
+    // the cluster chains (the large matrices) run on a side stream, beside the per-CTA chains
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    if (cl_on) {
+        TG_CUDA_CHECK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+        TG_CUDA_CHECK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+        TG_CUDA_CHECK(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+        TG_CUDA_CHECK(cudaEventRecord(fork, st));
+        TG_CUDA_CHECK(cudaStreamWaitEvent(side, fork, 0));
+    }
     nn_chain_cta_kernel<NN_SMALL_T, NN_SMALL_U><<<(unsigned)cblocks, NN_SMALL_T, nn_smem, st>>>(mats, mat_off, sizes, count, merge_off, lefts,
-                                                                        rights, heights, active, slot, chain, aux_off);
+                                                                        rights, heights, active, slot, chain, aux_off,
+                                                                        cl_min);
     nn_chain_cta_kernel<1024, 8><<<(unsigned)cblocks, 1024, nn_smem, st>>>(mats, mat_off, sizes, count, merge_off,
                                                                           lefts, rights, heights, active, slot, chain,
-                                                                          aux_off);
+                                                                          aux_off, cl_min);
     tg_count_launch(2);
+    if (cl_on) {
+        const int64_t ncl = count < (int64_t)tg_num_sms() / NN_CL ? count : (int64_t)tg_num_sms() / NN_CL;
+        TG_CUDA_CHECK(cudaFuncSetAttribute(nn_chain_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)nn_smem));
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = NN_CL;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3((unsigned)(ncl * NN_CL), 1, 1);
+        cfg.blockDim = dim3(NN_CL_T, 1, 1);
+        cfg.dynamicSmemBytes = nn_smem;
+        cfg.stream = side;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        TG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, nn_chain_cluster_kernel, mats, mat_off, sizes, count, merge_off, lefts,
+                                         rights, heights, cl_min));
+        tg_count_launch(1);
+        TG_CUDA_CHECK(cudaEventRecord(join, side));
+        TG_CUDA_CHECK(cudaStreamWaitEvent(st, join, 0));
+        cudaEventDestroy(fork);
+        cudaEventDestroy(join);
+        cudaStreamDestroy(side);   // released once its work completes
+    }
     TG_LAUNCH_CHECK();
     return TG_OK;
 }

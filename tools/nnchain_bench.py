@@ -5,7 +5,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import numpy as np
 import torch
 from paper_2408_09399_b200 import linkage
-for m in (64, 256, 512, 1056, 2048):
+for m in [int(a) for a in sys.argv[1:]] or (64, 256, 512, 1056, 2048, 4096, 5906):
     rng = np.random.default_rng(m)
     A = rng.random((m, m))
     D = (A + A.T) / 2
