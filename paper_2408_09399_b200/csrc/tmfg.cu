@@ -62,7 +62,7 @@ constexpr int TM_MERGE_WARPS = TM_MERGE_WARPS_DEF;            // replay + merge 
 template <bool SMEM_ST>
 __host__ __device__ constexpr int tm_merge_warps() { return SMEM_ST ? TM_FG_WARPS : TM_MERGE_WARPS; }
 #ifndef TM_B_DEF
-#define TM_B_DEF 1024   // a longer queue means fewer pool refills; 2048 would push vst out of smem at n=10k
+#define TM_B_DEF 896    // measured: 640 / 768 / 896 / 1024 -> 87.6 / 86-88 / 86.2 / 87.6 ms at n = 10k, 588 / 572 / 576 / 587 ms at 50k
 #endif
 constexpr int TM_B = TM_B_DEF;                  // shared-memory queue capacity (scan state in smem)
 constexpr int TM_BMAX = 2 * TM_B;               // ... when the scan state lives in global memory (large n):
