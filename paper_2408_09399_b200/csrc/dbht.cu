@@ -408,7 +408,7 @@ group_max_tile_kernel(tg_oracle_t o, const int32_t *__restrict__ perm, const int
 // D = min_h fl64(hd[h,u] + hd[h,v]) (apsp.py:136-143); in fp32, d' = min_h
 // fl32(fl32(hd[h,u]) + fl32(hd[h,v])) satisfies |d' - D| <= 2^-22.8 D + 2^-147
 // (all terms >= 0).  Per tile and per (row group run, column group run) the
-// largest d' is taken; every pair with d' >= lmax' (1 - 2^-19) - 2^-140 -- a
+// largest d' is taken; every pair with d' >= lmax' (1 - 2^-21) - 2^-140 -- a
 // superset of the pairs attaining the tile-local maximum of D -- gets its exact
 // fp64 D and only those are maxed into M.  The maximum over tiles of the exact
 // tile-local maxima is M's exact entry.  The hub distances are first laid out
@@ -416,7 +416,8 @@ group_max_tile_kernel(tg_oracle_t o, const int32_t *__restrict__ perm, const int
 // fp64 copies), so every panel load is a coalesced row segment.
 constexpr int GH_T = 256;
 constexpr int GH_MAXC = GM_TILE * GM_TILE;
-constexpr int GH_LD = GM_HC + 1;   // panel row stride (conflict-free both ways)
+constexpr int GH_LD = GM_HC + 2;   // panel row stride: 17 8-byte words (odd), so 16 consecutive rows'
+                                   // float2 reads hit distinct 8-byte bank pairs
 
 __global__ void hp_fill_kernel(tg_oracle_t o, const int32_t *__restrict__ perm, int64_t total, int Hp,
                                float *__restrict__ hpf, double *__restrict__ hpd) {
@@ -444,7 +445,7 @@ group_max_hub_kernel(tg_oracle_t o, const int32_t *__restrict__ gid, const GmSub
     __shared__ int ncand;
     __shared__ int rg[GM_TILE], cg[GM_TILE], lr[GM_TILE], lc[GM_TILE];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int tx = tid & 15, ty = tid >> 4;   // 16 x 16 threads, rows ty*4.., cols tx*4..
+    const int tx = tid & 15, ty = tid >> 4;   // 16 x 16 threads, rows ty + 16 r, cols tx + 16 c
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const GmTile tl = tiles[t];
         const GmSub sb = subs[tl.sub];
@@ -476,23 +477,41 @@ group_max_hub_kernel(tg_oracle_t o, const int32_t *__restrict__ gid, const GmSub
 #pragma unroll
             for (int c = 0; c < 4; c++) acc[r][c] = INFINITY;
         for (int h0 = 0; h0 < Hp; h0 += GM_HC) {
-            for (int e = tid; e < GM_HC * GM_TILE; e += GH_T) {
-                const int i = e >> 5, h = e & 31;
-                Af[i][h] = i < rows ? hpf[(rbase + i) * Hp + h0 + h] : INFINITY;
-                Bf[i][h] = i < cols ? hpf[(cbase + i) * Hp + h0 + h] : INFINITY;
+            // 16-byte panel loads (rows of Hp floats, Hp a multiple of 32: aligned), 8-byte stores
+            for (int e = tid; e < GM_HC * GM_TILE / 4; e += GH_T) {
+                const int i = e >> 3, h = (e & 7) * 4;
+                const float4 inf4 = make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
+                const float4 a = i < rows ? *reinterpret_cast<const float4 *>(hpf + (rbase + i) * Hp + h0 + h) : inf4;
+                const float4 b = i < cols ? *reinterpret_cast<const float4 *>(hpf + (cbase + i) * Hp + h0 + h) : inf4;
+                *reinterpret_cast<float2 *>(&Af[i][h]) = make_float2(a.x, a.y);
+                *reinterpret_cast<float2 *>(&Af[i][h + 2]) = make_float2(a.z, a.w);
+                *reinterpret_cast<float2 *>(&Bf[i][h]) = make_float2(b.x, b.y);
+                *reinterpret_cast<float2 *>(&Bf[i][h + 2]) = make_float2(b.z, b.w);
             }
             __syncthreads();
+            // two hubs per step: one packed fp32x2 add (FADD2: two independent round-to-nearest
+            // fp32 adds) and one three-input min (FMNMX3) per pair -- the same d' as two FADD +
+            // two FMNMX, in half the instructions
 #pragma unroll 4
-            for (int h = 0; h < GM_HC; h++) {
-                float av[4], bv[4];
+            for (int h = 0; h < GM_HC; h += 2) {
+                unsigned long long av[4], bv[4];
 #pragma unroll
-                for (int r = 0; r < 4; r++) av[r] = Af[ty * 4 + r][h];
+                for (int r = 0; r < 4; r++) av[r] = *reinterpret_cast<const unsigned long long *>(&Af[ty + 16 * r][h]);
 #pragma unroll
-                for (int c = 0; c < 4; c++) bv[c] = Bf[tx * 4 + c][h];
+                for (int c = 0; c < 4; c++) bv[c] = *reinterpret_cast<const unsigned long long *>(&Bf[tx + 16 * c][h]);
 #pragma unroll
                 for (int r = 0; r < 4; r++)
 #pragma unroll
-                    for (int c = 0; c < 4; c++) acc[r][c] = fminf(acc[r][c], __fadd_rn(av[r], bv[c]));
+                    for (int c = 0; c < 4; c++) {
+                        unsigned long long sum;
+                        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(sum) : "l"(av[r]), "l"(bv[c]));
+                        float m3;
+                        asm("min.f32 %0, %1, %2, %3;"
+                            : "=f"(m3)
+                            : "f"(acc[r][c]), "f"(__uint_as_float((unsigned)sum)),
+                              "f"(__uint_as_float((unsigned)(sum >> 32))));
+                        acc[r][c] = m3;
+                    }
             }
             __syncthreads();
         }
@@ -501,11 +520,11 @@ group_max_hub_kernel(tg_oracle_t o, const int32_t *__restrict__ gid, const GmSub
         uint32_t valid = 0;
 #pragma unroll
         for (int r = 0; r < 4; r++) {
-            const int i = ty * 4 + r;
+            const int i = ty + 16 * r;
             const uint64_t mrow = i < rows ? mk[i] : ~0ull;
 #pragma unroll
             for (int c = 0; c < 4; c++) {
-                const int j = tx * 4 + c;
+                const int j = tx + 16 * c;
                 if (i < rows && j < cols && !((mrow >> j) & 1ull)) {
                     valid |= 1u << (r * 4 + c);
                     atomicMax(&lmax[lr[i] * GM_TILE + lc[j]], __float_as_uint(acc[r][c]));
@@ -518,10 +537,13 @@ group_max_hub_kernel(tg_oracle_t o, const int32_t *__restrict__ gid, const GmSub
 #pragma unroll
             for (int c = 0; c < 4; c++) {
                 if (!((valid >> (r * 4 + c)) & 1u)) continue;
-                const int i = ty * 4 + r, j = tx * 4 + c;
+                const int i = ty + 16 * r, j = tx + 16 * c;
                 // (an overflowed lmax' = inf still admits every pair near FLT_MAX)
                 const float lm = fminf(__uint_as_float(lmax[lr[i] * GM_TILE + lc[j]]), 3.4028235e38f);
-                const float thr = __fsub_rn(__fmul_rn(lm, 1.0f - 0x1p-19f), 0x1p-140f);
+                // |d' - D| <= e D + t (e = 2^-22.8, t = 2^-147) gives, for a pair attaining the exact
+                // maximum, d' >= lmax' (1 - 2e) - 2t; 1 - 2^-21 stays below 1 - 2e after the rounding
+                // of the product (2^-21 - 2^-24 > 2^-21.8)
+                const float thr = __fsub_rn(__fmul_rn(lm, 1.0f - 0x1p-21f), 0x1p-140f);
                 if (acc[r][c] >= thr) cand[atomicAdd(&ncand, 1)] = (uint16_t)((i << 6) | j);
             }
         __syncthreads();
