@@ -113,6 +113,15 @@ struct Rec {
     int64_t l, r;
     double h;
 };
+// a vertex group: a run of a flat member array (ascending vertex ids)
+struct Span {
+    const int32_t *p;
+    int64_t len;
+    int64_t size() const { return len; }
+    const int32_t *begin() const { return p; }
+    const int32_t *end() const { return p + len; }
+    int32_t operator[](int64_t i) const { return p[i]; }
+};
 struct Row {
     int64_t handle;
     double h;
@@ -241,14 +250,14 @@ int collect_linkages(Ctx &cx, LinkJob &job, const std::vector<std::vector<int64_
 
 // dbht.py:217-230 group maxima for vertex-disjoint sub-problems (one launch) on job.st, then
 // the linkages (launched; collect_linkages finishes them)
-int launch_group_linkages(Ctx &cx, LinkJob &job, const std::vector<std::vector<const std::vector<int32_t> *>> &subproblems) {
+int launch_group_linkages(Ctx &cx, LinkJob &job, const std::vector<std::vector<Span>> &subproblems) {
     std::vector<int32_t> perm, gid;
     std::vector<tg_gm_sub_t> subs;
     std::vector<tg_gm_tile_t> tiles;
     int64_t out_off = 0, total_len = 0, total_tiles = 0;
     for (const auto &groups : subproblems) {
         int64_t len = 0;
-        for (const auto *g : groups) len += (int64_t)g->size();
+        for (const auto &g : groups) len += g.size();
         total_len += len;
         total_tiles += ((len + 63) / 64) * ((len + 63) / 64);
     }
@@ -260,8 +269,8 @@ int launch_group_linkages(Ctx &cx, LinkJob &job, const std::vector<std::vector<c
         const auto &groups = subproblems[p];
         const int64_t perm_off = (int64_t)perm.size();
         for (size_t g = 0; g < groups.size(); g++) {
-            perm.insert(perm.end(), groups[g]->begin(), groups[g]->end());
-            gid.insert(gid.end(), groups[g]->size(), (int32_t)g);
+            perm.insert(perm.end(), groups[g].begin(), groups[g].end());
+            gid.insert(gid.end(), (size_t)groups[g].size(), (int32_t)g);
         }
         const int32_t len = (int32_t)(perm.size() - perm_off), m = (int32_t)groups.size();
         tg_gm_sub_t sd;
@@ -320,12 +329,20 @@ int build(Ctx &cx, const int64_t *vb_dev, const int64_t *vc_dev, int64_t *lefts,
         if (vb[v] < 0) return TG_ERR_ARG;
         nb = std::max(nb, vb[v] + 1);
     }
-    // vertices by (bubble, id): members[b] ascending
-    std::vector<std::vector<int32_t>> members(nb);
-    for (int64_t v = 0; v < n; v++) members[vb[v]].push_back((int32_t)v);
+    // vertices by (bubble, id): a counting sort into one flat array, members[b] ascending
+    std::vector<int64_t> moff(nb + 1, 0);
+    for (int64_t v = 0; v < n; v++) moff[vb[v] + 1]++;
+    for (int64_t b = 0; b < nb; b++) moff[b + 1] += moff[b];
+    std::vector<int32_t> mflat(n);
+    {
+        std::vector<int64_t> fill(moff.begin(), moff.end() - 1);
+        for (int64_t v = 0; v < n; v++) mflat[fill[vb[v]]++] = (int32_t)v;
+    }
+    std::vector<Span> members(nb);
+    for (int64_t b = 0; b < nb; b++) members[b] = Span{mflat.data() + moff[b], moff[b + 1] - moff[b]};
     std::vector<int64_t> bubble_ids;
     for (int64_t b = 0; b < nb; b++)
-        if (!members[b].empty()) bubble_ids.push_back(b);
+        if (members[b].size() > 0) bubble_ids.push_back(b);
     std::vector<int64_t> group_root(nb, -1);
 
     // All three layers' device work is independent: layer 1 (bubble groups) reads oracle
@@ -353,42 +370,54 @@ int build(Ctx &cx, const int64_t *vb_dev, const int64_t *vc_dev, int64_t *lefts,
     std::vector<int64_t> conv_ids;
     std::vector<std::vector<int64_t>> conv_bubbles;   // parallel to conv_ids
     std::vector<int64_t> conv_root;
-    std::vector<std::vector<const std::vector<int32_t> *>> subproblems;
+    std::vector<std::vector<Span>> subproblems;
     std::vector<size_t> which;
     {
-        std::vector<std::pair<int64_t, int64_t>> cb;   // (conv id, bubble) in bubble order
-        for (int64_t b : bubble_ids) cb.push_back({vc[members[b][0]], b});
-        std::stable_sort(cb.begin(), cb.end(),
-                         [](const std::pair<int64_t, int64_t> &a, const std::pair<int64_t, int64_t> &b) {
-                             return a.first < b.first;
-                         });
-        for (const auto &x : cb) {
-            if (conv_ids.empty() || conv_ids.back() != x.first) {
-                conv_ids.push_back(x.first);
-                conv_bubbles.emplace_back();
+        // bubbles grouped by converging id (ascending), bubble order inside: a stable counting
+        // sort (converging ids are bubble indices)
+        int64_t ncv = 0;
+        for (int64_t b : bubble_ids) ncv = std::max(ncv, vc[members[b][0]] + 1);
+        std::vector<int64_t> cnt(ncv, 0);
+        for (int64_t b : bubble_ids) cnt[vc[members[b][0]]]++;
+        std::vector<int64_t> slot_of(ncv, -1);
+        for (int64_t c = 0; c < ncv; c++)
+            if (cnt[c] > 0) {
+                slot_of[c] = (int64_t)conv_ids.size();
+                conv_ids.push_back(c);
             }
-            conv_bubbles.back().push_back(x.second);
-        }
+        conv_bubbles.resize(conv_ids.size());
+        for (size_t c = 0; c < conv_ids.size(); c++) conv_bubbles[c].reserve((size_t)cnt[conv_ids[c]]);
+        for (int64_t b : bubble_ids) conv_bubbles[slot_of[vc[members[b][0]]]].push_back(b);
         conv_root.assign(conv_ids.size(), -1);
         for (size_t c = 0; c < conv_ids.size(); c++) {
             if (conv_bubbles[c].size() == 1) continue;
-            std::vector<const std::vector<int32_t> *> groups;
-            for (int64_t b : conv_bubbles[c]) groups.push_back(&members[b]);
+            std::vector<Span> groups;
+            groups.reserve(conv_bubbles[c].size());
+            for (int64_t b : conv_bubbles[c]) groups.push_back(members[b]);
             subproblems.push_back(std::move(groups));
             which.push_back(c);
         }
     }
     const bool layer3 = conv_ids.size() > 1;
-    std::vector<std::vector<int32_t>> cmem(layer3 ? conv_ids.size() : 0);
-    std::vector<const std::vector<int32_t> *> groups3;
+    std::vector<int32_t> cflat;
+    std::vector<Span> groups3;
     if (layer3) {
-        // cmem[c] = the union of group c's bubble members, ascending: one pass over the
-        // vertices in id order (every vertex is in exactly one bubble) instead of a sort
+        // group c's vertices = the union of its bubbles' members, ascending: a counting sort of
+        // the vertices (in id order) by group into one flat array
+        const size_t ng = conv_ids.size();
         std::vector<int32_t> conv_of_bubble(nb, -1);
-        for (size_t c = 0; c < conv_ids.size(); c++)
-            for (int64_t b : conv_bubbles[c]) conv_of_bubble[b] = (int32_t)c;
-        for (int64_t v = 0; v < n; v++) cmem[conv_of_bubble[vb[v]]].push_back((int32_t)v);
-        for (size_t c = 0; c < conv_ids.size(); c++) groups3.push_back(&cmem[c]);
+        std::vector<int64_t> coff(ng + 1, 0);
+        for (size_t c = 0; c < ng; c++)
+            for (int64_t b : conv_bubbles[c]) {
+                conv_of_bubble[b] = (int32_t)c;
+                coff[c + 1] += members[b].size();
+            }
+        for (size_t c = 0; c < ng; c++) coff[c + 1] += coff[c];
+        cflat.resize((size_t)n);
+        std::vector<int64_t> fill(coff.begin(), coff.end() - 1);
+        for (int64_t v = 0; v < n; v++) cflat[fill[conv_of_bubble[vb[v]]]++] = (int32_t)v;
+        groups3.reserve(ng);
+        for (size_t c = 0; c < ng; c++) groups3.push_back(Span{cflat.data() + coff[c], coff[c + 1] - coff[c]});
         HPROF("cmem");
         HC(side3.open(cx.st));
         HPROF("open3");
