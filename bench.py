@@ -270,7 +270,7 @@ def run_b200(args, world, rank, local):
     # ---- the top of the north star's n range: config 5 (n = 50,000, 20 GB S in HBM),
     # device-resident pass after one warm-up pass (reported beside, not the value)
     big = None
-    if rank == 0 and not args.no_50k and cfg == 3 and args.n is None:
+    if rank == 0 and world == 1 and not args.no_50k and cfg == 3 and args.n is None:   # side measurement, N = 1 only
         del S, order, S_buf, order_buf
         torch.cuda.empty_cache()
         x5, _ = synth.generate(5)
