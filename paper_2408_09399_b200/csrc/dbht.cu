@@ -448,6 +448,11 @@ group_max_hub_kernel(tg_oracle_t o, const int32_t *__restrict__ gid, const GmSub
     const int tx = tid & 15, ty = tid >> 4;   // 16 x 16 threads, rows ty + 16 r, cols tx + 16 c
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const GmTile tl = tiles[t];
+        // the hub estimate D(u, v) = min_h fl(hd[h,u] + hd[h,v]) is symmetric, and so is the
+        // override set (u in near(v) or v in near(u)): a tile below the diagonal repeats the
+        // transposed tile's pairs, whose maxima are written to both orientations instead
+        if (tl.i0 > tl.j0) continue;
+        const bool mirror = tl.i0 < tl.j0;
         const GmSub sb = subs[tl.sub];
         const int rows = min(GM_TILE, sb.len - tl.i0), cols = min(GM_TILE, sb.len - tl.j0);
         const int64_t rbase = sb.perm_off + tl.i0, cbase = sb.perm_off + tl.j0;
@@ -557,7 +562,10 @@ group_max_hub_kernel(tg_oracle_t o, const int32_t *__restrict__ gid, const GmSub
 #pragma unroll 4
             for (int h = lane; h < Hp; h += 32) ex = fmin(ex, __dadd_rn(ha[h], hb[h]));
             for (int o = 16; o; o >>= 1) ex = fmin(ex, __shfl_xor_sync(0xffffffffu, ex, o));
-            if (lane == 0) atomicMax(&out[sb.out_off + (int64_t)rg[ci] * sb.m + cg[cj]], tg_dbits(ex));
+            if (lane == 0) {
+                atomicMax(&out[sb.out_off + (int64_t)rg[ci] * sb.m + cg[cj]], tg_dbits(ex));
+                if (mirror) atomicMax(&out[sb.out_off + (int64_t)cg[cj] * sb.m + rg[ci]], tg_dbits(ex));
+            }
         }
         __syncthreads();
     }
