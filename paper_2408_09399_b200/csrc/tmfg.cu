@@ -263,20 +263,21 @@ __device__ void warp_entries(const TmArgs &A, const uint32_t *bits, unsigned lon
     const int nv = 3 * cnt;
     // a vertex whose certified max-corr (or the id after it) is still uninserted needs no scan
     unsigned pending = 0u;
+    // vertex k's word is read and decided by lane k (all of them at once, not one after the
+    // other on lane 0) and broadcast: background warps rewrite the word and the winner's bit
+    // may be set concurrently (speculative refreshes), and every lane must take the same scan
+    // decision (full-mask collectives follow)
+    int c_mine = 0, f_mine = -1;
+    if (lane < nv && lane < NV) {
+        const VSt r = vst_unpack(st[fverts[lane / 3][lane % 3]]);
+        c_mine = r.cur;
+        f_mine = vst_pick(bits, r);
+    }
 #pragma unroll
     for (int k = 0; k < NV; k++) {
         vv[k] = k < nv ? fverts[k / 3][k % 3] : 0;
-        // decided on lane 0 and broadcast: background warps rewrite the word and the
-        // winner's bit may be set concurrently (speculative refreshes), and every lane
-        // must take the same scan decision (full-mask collectives follow)
-        int c0 = 0, f0 = -1;
-        if (lane == 0 && k < nv) {
-            const VSt r = vst_unpack(st[vv[k]]);
-            c0 = r.cur;
-            f0 = vst_pick(bits, r);
-        }
-        cur[k] = __shfl_sync(0xffffffffu, c0, 0);
-        const int mcv = __shfl_sync(0xffffffffu, f0, 0);
+        cur[k] = __shfl_sync(0xffffffffu, c_mine, k);
+        const int mcv = __shfl_sync(0xffffffffu, f_mine, k);
         found[k] = -1;
         found2[k] = -1;
         if (k < nv) {
