@@ -1280,17 +1280,23 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
                     }
                 }
                 if (cnt) {
-                    warp_entries<SMEM_ST>(A, bits, vst, cnt, fvv, fids, Lout[warp - TM_NEW_WARPS], my_iters,
-                                          nullptr);
-                    const int *mcs = &g_went[threadIdx.x >> 5][3 * TM_EPW];   // the refreshed max-corrs
-                    if (lane == 0)
-                        for (int q = 0; q < cnt; q++) {
-                            Lref[idx[q]] = Lout[warp - TM_NEW_WARPS][q];
-                            Lmc[idx[q]][0] = mcs[3 * q];
-                            Lmc[idx[q]][1] = mcs[3 * q + 1];
-                            Lmc[idx[q]][2] = mcs[3 * q + 2];
-                            Lcomp[idx[q]] = 1;
-                        }
+                    if (TM_EPW == 1) {
+                        // the refreshed entry and its max-corrs straight into the window arrays
+                        warp_entries<SMEM_ST>(A, bits, vst, 1, fvv, fids, &Lref[idx[0]], my_iters, Lmc[idx[0]]);
+                        if (lane == 0) Lcomp[idx[0]] = 1;
+                    } else {
+                        warp_entries<SMEM_ST>(A, bits, vst, cnt, fvv, fids, Lout[warp - TM_NEW_WARPS], my_iters,
+                                              nullptr);
+                        const int *mcs = &g_went[threadIdx.x >> 5][3 * TM_EPW];   // the refreshed max-corrs
+                        if (lane == 0)
+                            for (int q = 0; q < cnt; q++) {
+                                Lref[idx[q]] = Lout[warp - TM_NEW_WARPS][q];
+                                Lmc[idx[q]][0] = mcs[3 * q];
+                                Lmc[idx[q]][1] = mcs[3 * q + 1];
+                                Lmc[idx[q]][2] = mcs[3 * q + 2];
+                                Lcomp[idx[q]] = 1;
+                            }
+                    }
                 }
             }
         }
