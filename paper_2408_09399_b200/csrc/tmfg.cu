@@ -1670,8 +1670,19 @@ TG_API int tg_tmfg_heap(const double *S, const int32_t *order, int64_t n, const 
     if (n >= (1 << 21)) return TG_ERR_ARG;   // scan-state word packs ids in 21 bits
     A.prefetch = 1;
     if (const char *e = std::getenv("TG_TMFG_PREFETCH")) A.prefetch = std::atoi(e);
-    const bool smem_st = tm_smem_bytes(n, true) <= 200 * 1024;
+    // dynamic shared memory budget: the per-block opt-in maximum minus the kernel's static arrays
+    // (a fixed 200 KB would overflow the block's 227 KB for n ~ 13k-17k with ~46 KB of static data)
+    int dev = 0, optin = 0;
+    TG_CUDA_CHECK(cudaGetDevice(&dev));
+    TG_CUDA_CHECK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa_st, fa_gl;
+    TG_CUDA_CHECK(cudaFuncGetAttributes(&fa_st, tmfg_heap_kernel<true>));
+    TG_CUDA_CHECK(cudaFuncGetAttributes(&fa_gl, tmfg_heap_kernel<false>));
+    const size_t budget_st = (size_t)optin - fa_st.sharedSizeBytes, budget_gl = (size_t)optin - fa_gl.sharedSizeBytes;
+    const bool smem_st = tm_smem_bytes(n, true) <= budget_st;
     const size_t smem_leader = tm_smem_bytes(n, smem_st);
+    const size_t budget = smem_st ? budget_st : budget_gl;
+    if (smem_leader > budget) return TG_ERR_ARG;
     // a cluster of 1 leader + helper CTAs (TG_TMFG_CLUSTER, default 8 = portable
     // maximum; 1 disables the helpers); falls back to a lone CTA if it cannot be placed
     int ncl = 8;
@@ -1683,7 +1694,7 @@ TG_API int tg_tmfg_heap(const double *S, const int32_t *order, int64_t n, const 
     for (; ncl > 1; ncl--) {
         const int vslots = ncl - 1 - ((A.prefetch && ncl > 2) ? 1 : 0);
         const size_t hs = (size_t)((((n + 31) / 32) + 1) & ~1LL) * 4 + (size_t)tm_helper_slice((int)n, vslots) * 8 + 64;
-        if (hs <= 200 * 1024) { smem = std::max(smem_leader, hs); break; }
+        if (hs <= budget) { smem = std::max(smem_leader, hs); break; }
     }
 #define TM_LAUNCH(M)                                                                                      \
     do {                                                                                                  \

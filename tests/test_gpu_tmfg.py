@@ -90,7 +90,7 @@ def test_tmfg_nan_raises(pkg):
         pkg.build_tmfg_heap(S, lists)
 
 
-@pytest.mark.parametrize("config,n", [(3, 10000), (4, 4000), (2, 2000), (1, 500), (5, 3000), (3, 6001)])
+@pytest.mark.parametrize("config,n", [(3, 10000), (4, 4000), (2, 2000), (1, 500), (5, 3000), (3, 6001), (3, 17000)])
 def test_tmfg_matches_oracle_larger(config, n, oracle, pkg):
     """Full-size heap TMFG vs the oracle on the reference's own S (reference-order Pearson on
     the GPU): trace, edges, faces and the debug counters, bit for bit.  Sizes where the
