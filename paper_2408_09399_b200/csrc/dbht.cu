@@ -769,10 +769,9 @@ nn_chain_cta_kernel(double *mats, const int64_t *mat_off, const int64_t *sizes, 
                     uint8_t *active_all, int64_t *slot_all, int64_t *chain_all, const int64_t *aux_off,
                     int cl_min) {
     extern __shared__ __align__(16) unsigned char nn_smem[];
-    __shared__ double rv[NN_CTA_T / 32];
-    __shared__ int ri[NN_CTA_T / 32];
-    __shared__ int sh_y, sh_first;
-    __shared__ double sh_rp;
+    __shared__ double rv[2][NN_CTA_T / 32];
+    __shared__ int ri[2][NN_CTA_T / 32];
+    __shared__ double sh_rp[2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = NN_CTA_T / 32;
     int32_t *s_chain = reinterpret_cast<int32_t *>(nn_smem);
@@ -801,8 +800,12 @@ nn_chain_cta_kernel(double *mats, const int64_t *mat_off, const int64_t *sizes, 
             W[(int64_t)i * m + i] = INFINITY;
         }
         __syncthreads();
-        int nchain = 0, remaining = m, nm = 0;
+        int nchain = 0, remaining = m, nm = 0, step = 0;
         int64_t next_id = m;
+        // every thread reduces the warps' partials itself and so takes the same decision: the
+        // chain's top two stay in registers, partials are double-buffered by step parity, and
+        // a chain step costs one barrier (a merge: one more after its row / column pass)
+        int x = 0, p = -1;
         while (remaining > 1) {
             if (nchain == 0) {
                 // chain start: the first active cluster
@@ -810,18 +813,17 @@ nn_chain_cta_kernel(double *mats, const int64_t *mat_off, const int64_t *sizes, 
                 for (int i = tid; i < m; i += NN_CTA_T)
                     if (act[i]) { f = i; break; }
                 f = __reduce_min_sync(0xffffffffu, (unsigned)f);
-                if (lane == 0) ri[warp] = f;
+                if (lane == 0) ri[0][warp] = f;
                 __syncthreads();
-                if (warp == 0) {
-                    int g = lane < NW ? ri[lane] : INT_MAX;
-                    g = (int)__reduce_min_sync(0xffffffffu, (unsigned)g);
-                    if (lane == 0) { chain_set(0, g); sh_first = g; }
-                }
-                __syncthreads();
+                int g = lane < NW ? ri[0][lane] : INT_MAX;
+                g = (int)__reduce_min_sync(0xffffffffu, (unsigned)g);
+                if (tid == 0) chain_set(0, g);
+                __syncthreads();   // ri[0] is rewritten by the next step
                 nchain = 1;
+                x = g;
+                p = -1;
             }
-            const int x = nchain > 0 ? (in_smem ? s_chain[nchain - 1] : chain_get(nchain - 1)) : 0;
-            const int p = nchain > 1 ? chain_get(nchain - 2) : -1;
+            const int par = step & 1;
             const double *row = W + (int64_t)x * m;
             double bv = INFINITY;
             int bi = INT_MAX;
@@ -838,7 +840,7 @@ nn_chain_cta_kernel(double *mats, const int64_t *mat_off, const int64_t *sizes, 
                     if (j < m) {
                         const double r = (act[j] && j != x) ? rr[u] : INFINITY;
                         if (r < bv || (r == bv && j < bi)) { bv = r; bi = j; }
-                        if (j == p) sh_rp = r;
+                        if (j == p) sh_rp[par] = r;
                     }
                 }
             }
@@ -847,33 +849,29 @@ nn_chain_cta_kernel(double *mats, const int64_t *mat_off, const int64_t *sizes, 
                 const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
                 if (r2 < bv || (r2 == bv && i2 < bi)) { bv = r2; bi = i2; }
             }
-            if (lane == 0) { rv[warp] = bv; ri[warp] = bi; }
+            if (lane == 0) { rv[par][warp] = bv; ri[par][warp] = bi; }
             __syncthreads();
-            if (warp == 0) {
-                double v = lane < NW ? rv[lane] : INFINITY;
-                int i = lane < NW ? ri[lane] : INT_MAX;
-                for (int o = 16; o; o >>= 1) {
-                    const double r2 = __shfl_xor_sync(0xffffffffu, v, o);
-                    const int i2 = __shfl_xor_sync(0xffffffffu, i, o);
-                    if (r2 < v || (r2 == v && i2 < i)) { v = r2; i = i2; }
-                }
-                if (lane == 0) {
-                    int y = (i == INT_MAX) ? 0 : i;  // all-inf row: np.argmin -> 0
-                    // linkage.py: prefer the previous chain element on ties (row[y] is the minimum v)
-                    if (p >= 0 && sh_rp == v) y = p;
-                    sh_y = y;
-                }
+            double v = lane < NW ? rv[par][lane] : INFINITY;
+            int i = lane < NW ? ri[par][lane] : INT_MAX;
+            for (int o = 16; o; o >>= 1) {
+                const double r2 = __shfl_xor_sync(0xffffffffu, v, o);
+                const int i2 = __shfl_xor_sync(0xffffffffu, i, o);
+                if (r2 < v || (r2 == v && i2 < i)) { v = r2; i = i2; }
             }
-            __syncthreads();
-            const int y = sh_y;
+            const double rp = p >= 0 ? sh_rp[par] : INFINITY;
+            step++;
+            int y = (i == INT_MAX) ? 0 : i;   // all-inf row: np.argmin -> 0
+            // linkage.py: prefer the previous chain element on ties (row[y] is the minimum v)
+            if (p >= 0 && rp == v) y = p;
             if (p >= 0 && y == p) {
                 nchain -= 2;
-                const double h = sh_rp;
                 const int lo = x < y ? x : y, hi = x < y ? y : x;
                 if (tid == 0) {
                     L[nm] = slot_get(x);
                     R[nm] = slot_get(y);
-                    Hh[nm] = h;
+                    Hh[nm] = rp;
+                    act[hi] = 0;          // read again only after the barrier below
+                    slot_set(lo, next_id);
                 }
                 nm++;
                 double *Wlo = W + (int64_t)lo * m;
@@ -889,30 +887,29 @@ nn_chain_cta_kernel(double *mats, const int64_t *mat_off, const int64_t *sizes, 
 #pragma unroll
                     for (int u = 0; u < NN_U; u++) {
                         const int j = j0 + u * NN_CTA_T;
-                        if (j < m) {
+                        if (j < m && j != lo) {   // W[lo, lo] stays inf (linkage.py:88)
                             const double mg = pv[u] > qv[u] ? pv[u] : (qv[u] > pv[u] ? qv[u] : pv[u]);
                             Wlo[j] = mg;
                             W[(int64_t)j * m + lo] = mg;
                         }
                     }
                 }
-                __syncthreads();
-                if (tid == 0) {
-                    Wlo[lo] = INFINITY;
-                    act[hi] = 0;
-                    slot_set(lo, next_id);
-                }
                 next_id++;
                 remaining--;
-                __syncthreads();
+                __syncthreads();   // the merged row / column and act[hi] are visible
+                if (nchain > 0) {
+                    x = in_smem ? s_chain[nchain - 1] : chain_get(nchain - 1);
+                    p = nchain > 1 ? chain_get(nchain - 2) : -1;
+                }
             } else {
                 if (nchain >= m) {  // a non-reducible (asymmetric) matrix made the chain cycle
                     if (tid == 0) Hh[0] = __longlong_as_double(0x7ff8dead00000000ll);
                     break;
                 }
-                if (tid == 0) chain_set(nchain, y);
+                if (tid == 0) chain_set(nchain, y);   // read back only after a later barrier
                 nchain++;
-                __syncthreads();
+                p = x;
+                x = y;
             }
         }
         __syncthreads();
