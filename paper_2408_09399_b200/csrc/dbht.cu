@@ -559,8 +559,17 @@ group_max_hub_kernel(tg_oracle_t o, const int32_t *__restrict__ gid, const GmSub
             const int ci = cand[k] >> 6, cj = cand[k] & 63;
             const double *ha = hpd + (rbase + ci) * Hp, *hb = hpd + (cbase + cj) * Hp;
             double ex = INFINITY;
-#pragma unroll 4
-            for (int h = lane; h < Hp; h += 32) ex = fmin(ex, __dadd_rn(ha[h], hb[h]));
+            for (int h0 = 0; h0 < Hp; h0 += 256) {   // every load of a 256-hub chunk in flight at once
+                double xa[8], xb[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const int h = h0 + u * 32 + lane;
+                    xa[u] = h < Hp ? ha[h] : INFINITY;
+                    xb[u] = h < Hp ? hb[h] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; u++) ex = fmin(ex, __dadd_rn(xa[u], xb[u]));
+            }
             for (int o = 16; o; o >>= 1) ex = fmin(ex, __shfl_xor_sync(0xffffffffu, ex, o));
             if (lane == 0) {
                 atomicMax(&out[sb.out_off + (int64_t)rg[ci] * sb.m + cg[cj]], tg_dbits(ex));
