@@ -176,6 +176,8 @@ __device__ __forceinline__ long long fg_sync_clock() {
 // with one atomicMax (cursor in the top bits: the furthest scan wins), so readers
 // never see a cursor from one scan with ids from another.  n <= 2^21 - 1.
 #if TM_PROFILE
+__device__ unsigned long long g_rp[4];
+__shared__ unsigned long long g_mw_round;   // slowest merge warp this round   // replay segments: prefix scan, winner, re-queue split, sort
 __device__ unsigned long long g_tm_prof[8];   // fg vertices looked up, scanned, tail batches; bg scans
 #endif
 struct VSt {
@@ -717,6 +719,9 @@ __device__ void replay_warp(const TmArgs &A, Ctl &ctl, const Ent *L, const Ent *
                             const Ent *NE, Ent *batch, Ent *tobuf, double *kg, int *kf, int *ksrc, double *tkg,
                             int *tkf) {
     const int lane = threadIdx.x & 31;
+#if TM_PROFILE
+    const long long rp0 = clock64();
+#endif
     const int Lc = ctl.L_count, nec = ctl.ne_count;
     // best new entry (<= 4, every lane)
     double ng = 0.0;
@@ -759,6 +764,9 @@ __device__ void replay_warp(const TmArgs &A, Ctl &ctl, const Ent *L, const Ent *
     const bool eok = (lane > 0) & (__shfl_up_sync(0xffffffffu, (int)iok, 1) != 0);
     const bool c = v & ((!st) | (eok & kgt(eg, ef, hg, hf)) | (have_ne & kgt(ng, nf, hg, hf)));
     const unsigned bc = __ballot_sync(0xffffffffu, c);
+#if TM_PROFILE
+    const long long rp1 = clock64() + (bc & 0u);
+#endif
     const int istar = bc ? __ffs(bc) - 1 : Lc;
     // tmfg.py:425-431 counters over the stale pops j < istar (+ the check_invariants assertion)
     const bool rose = st & (lane < istar) & (rg > __dadd_rn(hg, 1e-12));
@@ -816,6 +824,9 @@ __device__ void replay_warp(const TmArgs &A, Ctl &ctl, const Ent *L, const Ent *
     }
     // re-queue: refreshed entries of the stale pops (minus a refreshed winner) and
     // new entries (minus a new winner); above the pool max -> shared buffer, else pool
+#if TM_PROFILE
+    const long long rp2 = clock64() + (kind & 0);
+#endif
     const bool pm = ctl.pool_has_max;
     const double pg = ctl.pool_max.g;
     const int pf = ctl.pool_max.fid;
@@ -843,6 +854,9 @@ __device__ void replay_warp(const TmArgs &A, Ctl &ctl, const Ent *L, const Ent *
         ctl.pool_count = pc + npr + __popc(bpn);
         ctl.nbuf_new = nbuf;
     }
+#if TM_PROFILE
+    const long long rp3 = clock64() + (nbuf & 0);
+#endif
     for (int k = lane; k < nbuf; k += 32) {
         const double g = kg[k];
         const int f = kf[k];
@@ -854,6 +868,15 @@ __device__ void replay_warp(const TmArgs &A, Ctl &ctl, const Ent *L, const Ent *
         tkf[r] = f;
     }
     __syncwarp();
+#if TM_PROFILE
+    const long long rp4 = clock64();
+    if (lane == 0) {
+        g_rp[0] += rp1 - rp0;   // scan + winner
+        g_rp[0] += rp2 - rp1;
+        g_rp[1] += rp3 - rp2;
+        g_rp[2] += rp4 - rp3;
+    }
+#endif
 }
 
 // Background warp: sweep the vertices (32 per step, lane-parallel check), and for
@@ -1143,6 +1166,8 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
     for (int i = tid; i < nwords; i += TM_T) bits[i] = 0u;
 #if TM_PROFILE
     if (tid < 8) g_tm_prof[tid] = 0ull;
+    if (tid < 4) g_rp[tid] = 0ull;
+    if (tid == 0) g_mw_round = 0ull;
 #endif
     {
         unsigned long long *st0 = SMEM_ST ? vst : A.gvst;
@@ -1409,6 +1434,9 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
             // thread 0 rewrites ctl.size / sel / L_count / pool_count below: every merge warp has its copy first
             asm volatile("bar.sync 2, %0;" ::"r"(MW * 32) : "memory");
             if (warp > 0) {
+#if TM_PROFILE
+                const long long tm0 = clock64();
+#endif
                 Ent *cur = sel ? buf1 : buf0;
                 Ent *nxt = sel ? buf0 : buf1;
                 const int old = sz - r;
@@ -1454,6 +1482,9 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
                     if (old == 0)
                         for (int k = mt; k < nb; k += MT) place(tobuf[k], k);
                 }
+#if TM_PROFILE
+                if (lane == 0) atomicMax(&g_mw_round, (unsigned long long)(clock64() - tm0));
+#endif
             } else if (lane == 0) {
 #if TM_PROFILE
                 long long tin0 = clock64();
@@ -1523,7 +1554,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
         sel ^= 1;
 #if TM_PROFILE
         tc1 = fg_sync_clock();
-        if (tid == 0) { ctl.t_merge += tc1 - tc0; tc0 = tc1; }
+        if (tid == 0) { ctl.t_merge += tc1 - tc0; tc0 = tc1; g_rp[3] += g_mw_round; g_mw_round = 0; }
 #else
         fg_sync();
 #endif
@@ -1601,6 +1632,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
         A.stats[29] = (long long)g_tm_prof[3];
         A.stats[31] = (long long)(g_tm_prof[5] << 32 | g_tm_prof[6]);   // helper warp-phase vertices, batches
         A.stats[20] = (long long)g_tm_prof[7];
+        for (int q = 0; q < 4; q++) A.stats[4 + q] = (long long)g_rp[q];   // (slot 7: it_total overwritten)
 #endif
         A.stats[24] = ctl.rf_t[0];
         A.stats[25] = ctl.rf_t[1];

@@ -26,10 +26,12 @@ d["us_per_insert"] = dt * 1e6 / (n - 4)
 for kk in ("cyc_warp_max", "cyc_ne_max", "cyc_rf_max", "cyc_S_max", "cyc_refill", "cyc_par", "cyc_replay", "cyc_merge", "cyc_insert", "spec_refreshes"):
     d[kk + "_per_round"] = round(d[kk] / max(d["rounds"], 1))
 d["cyc_per_round_total"] = round(dt * 1.965e9 / max(d["rounds"], 1))
+for q, nm in enumerate(["rp_scan_winner", "rp_split", "rp_sort", "merge_warp_max"]):
+    d[nm] = round(int(st[4 + q]) / max(d["rounds"], 1))
 print(json.dumps(d))
 if "helper_wp" in d:
     d["helper_wp_vertices"] = d["helper_wp"] >> 32; d["helper_wp_batches"] = d["helper_wp"] & 0xffffffff
-keys = ["helper_wp_vertices", "helper_wp_batches", "ms", "rounds", "rc_hit", "spec_refreshes", "fg_scans", "fg_tail_batches", "bg_scans", "cyc_per_round_total",
+keys = ["rp_scan_winner", "rp_split", "rp_sort", "merge_warp_max", "cyc_insert_per_round", "helper_wp_vertices", "helper_wp_batches", "ms", "rounds", "rc_hit", "spec_refreshes", "fg_scans", "fg_tail_batches", "bg_scans", "cyc_per_round_total",
         "cyc_par_per_round", "cyc_ne_max_per_round", "cyc_rf_max_per_round", "cyc_S_max_per_round",
         "cyc_replay_per_round", "cyc_merge_per_round", "cyc_refill_per_round", "helper_passes"]
 print("SHORT", os.environ.get("TG_LIB", "").split("/")[-1], os.environ.get("TG_TMFG_CLUSTER", "8"),
