@@ -1124,7 +1124,9 @@ __device__ __forceinline__ void v2_row(const FkRow &R, const float (&fk)[KPT], u
                 }
             }
             if (tie > 1) {   // float ties (itself included): the doubles decide, then the id
-                const double xj = __ldg(row + j);
+                // (segments: slots map to column ids through R.sid)
+                const int idj = R.sid ? R.sid[j] : j;
+                const double xj = __ldg(row + idj);
                 rank = 0;
                 for (int q = s0[g]; q < s0[g] + c; q++) {
                     const uint2 o = P[q];
@@ -1135,7 +1137,8 @@ __device__ __forceinline__ void v2_row(const FkRow &R, const float (&fk)[KPT], u
                         if (!ODD) rank += fo > fj;
                         else rank += (fo > fj) | ((fj != fj) & (fo == fo));
                     } else {
-                        rank += rs_before(__ldg(row + o.y), (int)o.y, xj, j);
+                        const int ido = R.sid ? R.sid[o.y] : (int)o.y;
+                        rank += rs_before(__ldg(row + ido), ido, xj, idj);
                     }
                 }
             }
@@ -1146,7 +1149,7 @@ __device__ __forceinline__ void v2_row(const FkRow &R, const float (&fk)[KPT], u
     int32_t *out32 = reinterpret_cast<int32_t *>(buf) + (int)(((uintptr_t)R.out >> 2) & 3);
 #pragma unroll
     for (int e = 0; e < KPT; e++)
-        if (pk[e] != 0xffffffffu) out32[pk[e]] = tid + e * NT;
+        if (pk[e] != 0xffffffffu) out32[pk[e]] = R.sid ? R.sid[tid + e * NT] : tid + e * NT;
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic writes -> bulk-store reads
     __syncthreads();
 }
@@ -1573,8 +1576,13 @@ row_seg_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restrict__ 
         }
         const int Ci = rs_coarse_bins(cnt);
         const float hci = 0.5f * (float)Ci;
-        for (int i = tid; i < nw16; i += NT) f16[i] = 0u;
-        const int ns = (cnt + 3) / 4;   // slots s % 4 == 0 (fk_row samples threads 4k)
+        for (int i = tid; i < nw16 + 8; i += NT) f16[i] = 0u;   // + the 16-byte scan's overhang
+        int ns = 0;   // sampled slots: e % 4 == 0 (v2_row's histogram)
+#pragma unroll
+        for (int e = 0; e < KPT; e += 4) {
+            const int rr = cnt - e * NT;
+            ns += rr < 0 ? 0 : (rr < NT ? rr : NT);
+        }
         R.row = S + (int64_t)it.v * n64;
         R.out = out;
         R.n = cnt;
@@ -1583,9 +1591,12 @@ row_seg_kernel(const double *__restrict__ S, int64_t n64, int32_t *__restrict__ 
         R.hc = hci;
         R.nsamp = ns;
         __syncthreads();   // sid and the cleared counters are visible
-        // the segment's own float range (fk_row's general path): a fixed map over the
-        // segment window degrades badly when the keys crowd into part of it
-        fk_row<true, KPT>(R, fk);
+        // the segment's own float range (the general path): a fixed map over the segment
+        // window degrades badly when the keys crowd into part of it.  v2_row ranks the
+        // (key, slot) pairs and leaves the column ids (through sid) in the buffer
+        v2_row<true, KPT>(R, fk, fk_smem);
+        const int32_t *o32 = reinterpret_cast<const int32_t *>(fk_smem) + (int)(((uintptr_t)out >> 2) & 3);
+        for (int i = tid; i < cnt; i += NT) out[i] = o32[i];
     }
 }
 
