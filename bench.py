@@ -80,6 +80,19 @@ class ClockSampler:
             if len(parts) >= 6:
                 self.rows.append(parts)
 
+    def wait_first(self, timeout: float = 5.0):
+        """Block until nvidia-smi has produced a sample (its start-up queries the driver and can
+        stall CUDA calls for tens of ms: keep that out of the timed region)."""
+        t0 = time.perf_counter()
+        while self._proc is not None and not self.rows and time.perf_counter() - t0 < timeout:
+            time.sleep(0.01)
+        return self
+
+    def mark(self):
+        """Samples before this call are discarded: only the timed region's samples count."""
+        self._first = len(self.rows)
+        return self
+
     def stop(self) -> dict:
         if self._proc is not None:
             time.sleep(0.25)
@@ -88,6 +101,7 @@ class ClockSampler:
                 self._proc.wait(timeout=2)
             except Exception:
                 self._proc.kill()
+        self.rows = self.rows[getattr(self, "_first", 0):]
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
@@ -192,13 +206,16 @@ def run_b200(args, world, rank, local):
                 record.setdefault(nm, []).append(marks[i].elapsed_time(marks[i + 1]))
         return d, flat, S, order
 
+    # the clock sampler starts before the warm-up and has answered once before the timed region
+    sampler = ClockSampler(local).start() if rank == 0 else None
     # warm-up (also the sort-kernel timing source below)
     for _ in range(max(args.warmup, 0)):
         step(None)
     torch.cuda.synchronize()
+    if sampler:
+        sampler.wait_first().mark()
 
     # ---- timed region (device-resident)
-    sampler = ClockSampler(local).start() if rank == 0 else None
     stage = {}
     per_step = []
     launches0 = N.load().tg_launch_count()
@@ -326,7 +343,7 @@ def run_b200(args, world, rank, local):
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": launches // max(args.steps, 1),
             "gpu_launches_timed_total": launches,
-            "wall_s_timed": round(wall, 3),
+            "wall_s_timed": round(wall, 3), "step_ms": [round(x, 3) for x in per_step],
             "clocks": clocks,
             "cpu_baseline": cpu,
             "n50k": big,
