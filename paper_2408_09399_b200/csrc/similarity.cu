@@ -227,6 +227,10 @@ syrk_tma_kernel(const __grid_constant__ CUtensorMap tmX, const double *__restric
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
+    // Xc (n x Lp doubles, ~100 MB at n = 50k) stays in L2 while the 8 n^2 bytes of S stream past
+    // it: operand panels are loaded evict_last, S is stored evict_first (st.global.cs)
+    uint64_t pol = 0;
+    if (tid == 0) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
     auto issue = [&](int kt) {   // thread 0: both operand panels of k-tile kt
         const int s = kt % TS_STAGES;
         double *as = base + (size_t)s * 2 * TS_PANEL, *bs = as + TS_PANEL;
@@ -236,14 +240,14 @@ syrk_tma_kernel(const __grid_constant__ CUtensorMap tmX, const double *__restric
                      : "memory");
         const int k0 = kt * PBK;
         asm volatile(
-            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(
                 ts_smem(as)),
-            "l"(&tmX), "r"(k0), "r"((int)i0), "r"(b)
+            "l"(&tmX), "r"(k0), "r"((int)i0), "r"(b), "l"(pol)
             : "memory");
         asm volatile(
-            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(
                 ts_smem(bs)),
-            "l"(&tmX), "r"(k0), "r"((int)j0), "r"(b)
+            "l"(&tmX), "r"(k0), "r"((int)j0), "r"(b), "l"(pol)
             : "memory");
     };
     if (tid == 0)
@@ -332,7 +336,7 @@ syrk_tma_kernel(const __grid_constant__ CUtensorMap tmX, const double *__restric
             v1 = r < c + 1 ? T[r * TSTR + c + 1] : (r == c + 1 ? 1.0 : T[(c + 1) * TSTR + r]);
         }
         if (vec && gj + 1 < n) {
-            *reinterpret_cast<double2 *>(S + gi * n + gj) = make_double2(v0, v1);
+            __stcs(reinterpret_cast<double2 *>(S + gi * n + gj), make_double2(v0, v1));
         } else {
             S[gi * n + gj] = v0;
             if (gj + 1 < n) S[gi * n + gj + 1] = v1;
@@ -346,7 +350,7 @@ syrk_tma_kernel(const __grid_constant__ CUtensorMap tmX, const double *__restric
             if (gi >= n || gj >= n) continue;
             const double v0 = T[r * TSTR + c], v1 = T[(r + 1) * TSTR + c];
             if (vec && gi + 1 < n) {
-                *reinterpret_cast<double2 *>(S + gj * n + gi) = make_double2(v0, v1);
+                __stcs(reinterpret_cast<double2 *>(S + gj * n + gi), make_double2(v0, v1));
             } else {
                 S[gj * n + gi] = v0;
                 if (gi + 1 < n) S[gj * n + gi + 1] = v1;
