@@ -279,6 +279,12 @@ int tg_release_cached_memory(void);
 int tg_serialize_dendrogram(const int64_t *lefts, const int64_t *rights, const double *heights, const int64_t *sizes,
                             int64_t k, char *out, size_t cap, size_t *len_out);
 
+/* linkage.py:151-178 cut (HOST arrays): flat labels 0..k-1 after the first n - k merges (the
+ * reference's union-find; labels by ascending smallest member id).  scratch: 2 (2n - 1) int64.
+ * TG_ERR_ARG for k outside 1..n or a child id outside [0, 2n - 1). */
+int tg_cut_labels(const int64_t *lefts, const int64_t *rights, int64_t n, int64_t k, int64_t *labels,
+                  int64_t *scratch);
+
 #ifdef __cplusplus
 }
 #endif

@@ -572,6 +572,42 @@ TG_API int tg_serialize_dendrogram(const int64_t *lefts, const int64_t *rights, 
     return (out && used > cap) ? TG_ERR_CAPACITY : TG_OK;
 }
 
+// linkage.py:151-178 cut: flat labels after the first n - k merges, by the reference's own
+// union-find (path halving, parent[find(child)] = node), labels in order of first appearance
+// over the leaves (= ascending smallest member id).  Host arrays; `scratch` holds 2 (2n - 1)
+// int64.  TG_ERR_ARG when a child id is outside [0, 2n - 1) (the reference raises IndexError).
+TG_API int tg_cut_labels(const int64_t *lefts, const int64_t *rights, int64_t n, int64_t k, int64_t *labels,
+                         int64_t *scratch) {
+    if (n < 1 || k < 1 || k > n || !labels || !scratch || (n - k > 0 && (!lefts || !rights))) return TG_ERR_ARG;
+    const int64_t nn = 2 * n - 1;
+    int64_t *parent = scratch, *lab = scratch + nn;
+    for (int64_t x = 0; x < nn; x++) {
+        parent[x] = x;
+        lab[x] = -1;
+    }
+    auto find = [&](int64_t x) {
+        while (parent[x] != x) {
+            parent[x] = parent[parent[x]];
+            x = parent[x];
+        }
+        return x;
+    };
+    for (int64_t t = 0; t < n - k; t++) {
+        const int64_t node = n + t, c[2] = {lefts[t], rights[t]};
+        for (int q = 0; q < 2; q++) {
+            if (c[q] < 0 || c[q] >= nn) return TG_ERR_ARG;
+            parent[find(c[q])] = node;
+        }
+    }
+    int64_t next = 0;
+    for (int64_t leaf = 0; leaf < n; leaf++) {
+        const int64_t r = find(leaf);
+        if (lab[r] < 0) lab[r] = next++;
+        labels[leaf] = lab[r];
+    }
+    return TG_OK;
+}
+
 // Return the hierarchy pool's cached memory (kept between tg_build_hierarchy calls) to the device.
 TG_API int tg_release_cached_memory(void) {
     std::lock_guard<std::mutex> lk(g_pool_mu);

@@ -157,28 +157,29 @@ def dendrogram_from_merges(n_leaves: int, merges) -> Dendrogram:
 
 
 def cut(dendrogram: Dendrogram, k: int) -> np.ndarray:
-    """Flat labels from undoing the last k-1 merges (linkage.py:151-178)."""
+    """Flat labels from undoing the last k-1 merges (linkage.py:151-178).
+
+    The reference's union-find, run by the library's C++ side (``tg_cut_labels``, host
+    arrays, O(n)); labels 0..k-1 by ascending smallest member id.
+    """
+    import ctypes
+
     n = dendrogram.n_leaves
     if not 1 <= k <= n:
         raise ValueError(f"cluster count k={k} out of range 1..{n}")
-    # cluster of each node after the first n-k merges: propagate parent ids top-down
-    parent = np.arange(2 * n - 1, dtype=np.int64)
     kept = n - k
-    if kept:
-        nodes = n + np.arange(kept, dtype=np.int64)
-        parent[dendrogram.lefts[:kept]] = nodes
-        parent[dendrogram.rights[:kept]] = nodes
-    root = parent.copy()
-    for _ in range(64):
-        nxt = root[root]
-        if np.array_equal(nxt, root):
-            break
-        root = nxt
-    leaf_root = root[:n]
-    # labels by ascending smallest member id == order of first appearance
-    _, first, inv = np.unique(leaf_root, return_index=True, return_inverse=True)
-    label_of_unique = np.argsort(np.argsort(first, kind="stable"), kind="stable")
-    return label_of_unique[inv].astype(np.int64)
+    lefts = np.ascontiguousarray(np.asarray(dendrogram.lefts)[:kept], dtype=np.int64)
+    rights = np.ascontiguousarray(np.asarray(dendrogram.rights)[:kept], dtype=np.int64)
+    if lefts.shape[0] < kept or rights.shape[0] < kept:
+        raise IndexError("dendrogram has fewer merges than n - k")
+    labels = np.empty(n, dtype=np.int64)
+    scratch = np.empty(2 * (2 * n - 1), dtype=np.int64)
+    vp = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    rc = N.load(require_cuda=False).tg_cut_labels(vp(lefts), vp(rights), n, k, vp(labels), vp(scratch))
+    if rc == N.TG_ERR_ARG:
+        raise IndexError("dendrogram child id out of range")
+    N.check("tg_cut_labels", rc)
+    return labels
 
 
 def serialize_dendrogram(d: Dendrogram) -> str:

@@ -112,3 +112,33 @@ def test_serialize_dendrogram_matches_python_format():
     empty = linkage.Dendrogram(n_leaves=1, lefts=np.zeros(0, np.int64), rights=np.zeros(0, np.int64),
                                heights=np.zeros(0), sizes=np.zeros(0, np.int64))
     assert linkage.serialize_dendrogram(empty) == ""
+
+
+def test_cut_matches_oracle_every_k():
+    """tg_cut_labels (C++ union-find) against the oracle's restatement of linkage.py:151-178 on
+    a random n = 700 dendrogram for every k, and an out-of-range child id -> IndexError."""
+    import random
+
+    from oracle import oracle as orc
+    from paper_2408_09399_b200.linkage import Dendrogram, cut
+
+    n = 700
+    rnd = random.Random(11)
+    active, L, R, nxt = list(range(n)), [], [], n
+    for _ in range(n - 1):
+        a = active.pop(rnd.randrange(len(active)))
+        b = active.pop(rnd.randrange(len(active)))
+        L.append(min(a, b))
+        R.append(max(a, b))
+        active.append(nxt)
+        nxt += 1
+    lefts, rights = np.array(L, dtype=np.int64), np.array(R, dtype=np.int64)
+    d = Dendrogram(n_leaves=n, lefts=lefts, rights=rights, heights=np.arange(n - 1, dtype=np.float64),
+                   sizes=np.ones(n - 1, dtype=np.int64))
+    od = {"n_leaves": n, "lefts": lefts, "rights": rights}
+    for k in range(1, n + 1):
+        assert np.array_equal(cut(d, k), orc.cut(od, k)), k
+    bad = Dendrogram(n_leaves=n, lefts=np.where(np.arange(n - 1) == 3, 5 * n, lefts), rights=rights,
+                     heights=d.heights, sizes=d.sizes)
+    with pytest.raises(IndexError):
+        cut(bad, 1)
