@@ -19,6 +19,9 @@
 #include <cstring>
 #include <mutex>
 #include <vector>
+#include <thread>
+#include <string>
+#include <functional>
 
 // The hierarchy's per-layer buffers come from a pool owned by this library (one per device),
 // not from the process-wide default pool: it keeps up to 16 GiB cached between calls (the
@@ -551,22 +554,43 @@ TG_API int tg_build_hierarchy(const tg_oracle_t *oracle, const int64_t *vertex_b
 TG_API int tg_serialize_dendrogram(const int64_t *lefts, const int64_t *rights, const double *heights,
                                    const int64_t *sizes, int64_t k, char *out, size_t cap, size_t *len_out) {
     if (k < 0 || !len_out || (k > 0 && (!lefts || !rights || !heights || !sizes))) return TG_ERR_ARG;
+    // rows formatted in parallel chunks (std::to_chars(general, 17) is printf's "%.17g",
+    // correctly rounded, ~0.2 us per row: 1.8 ms for a 10k-leaf dendrogram on one thread)
+    auto fmt = [&](int64_t t0, int64_t t1, std::string &dst) {
+        dst.clear();
+        dst.reserve((size_t)(t1 - t0) * 40);
+        char line[128];
+        for (int64_t t = t0; t < t1; t++) {
+            char *p = line, *end = line + sizeof(line);
+            p = std::to_chars(p, end, (long long)lefts[t]).ptr;
+            *p++ = ' ';
+            p = std::to_chars(p, end, (long long)rights[t]).ptr;
+            *p++ = ' ';
+            p = std::to_chars(p, end, heights[t], std::chars_format::general, 17).ptr;
+            *p++ = ' ';
+            p = std::to_chars(p, end, (long long)sizes[t]).ptr;
+            *p++ = '\n';
+            dst.append(line, (size_t)(p - line));
+        }
+    };
+    int nt = (int)std::min<int64_t>(16, std::max<int64_t>(1, k / 640));
+    const unsigned hw = std::thread::hardware_concurrency();
+    if (hw > 0 && (unsigned)nt > hw) nt = (int)hw;
+    std::vector<std::string> parts((size_t)nt);
+    if (nt == 1) {
+        fmt(0, k, parts[0]);
+    } else {
+        std::vector<std::thread> th;
+        th.reserve((size_t)nt - 1);
+        for (int i = 1; i < nt; i++)
+            th.emplace_back(fmt, k * i / nt, k * (i + 1) / nt, std::ref(parts[(size_t)i]));
+        fmt(0, k / nt, parts[0]);
+        for (auto &t : th) t.join();
+    }
     size_t used = 0;
-    char line[128];
-    for (int64_t t = 0; t < k; t++) {
-        // std::to_chars(general, 17) is printf's "%.17g" (correctly rounded), much faster
-        char *p = line, *end = line + sizeof(line);
-        p = std::to_chars(p, end, (long long)lefts[t]).ptr;
-        *p++ = ' ';
-        p = std::to_chars(p, end, (long long)rights[t]).ptr;
-        *p++ = ' ';
-        p = std::to_chars(p, end, heights[t], std::chars_format::general, 17).ptr;
-        *p++ = ' ';
-        p = std::to_chars(p, end, (long long)sizes[t]).ptr;
-        *p++ = '\n';
-        const int w = (int)(p - line);
-        if (out && used + (size_t)w <= cap) std::memcpy(out + used, line, (size_t)w);
-        used += (size_t)w;
+    for (const auto &pt : parts) {
+        if (out && used + pt.size() <= cap) std::memcpy(out + used, pt.data(), pt.size());
+        used += pt.size();
     }
     *len_out = used;
     return (out && used > cap) ? TG_ERR_CAPACITY : TG_OK;

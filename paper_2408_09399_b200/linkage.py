@@ -196,16 +196,16 @@ def serialize_dendrogram(d: Dendrogram) -> str:
     cols = [np.ascontiguousarray(d.lefts, dtype=np.int64), np.ascontiguousarray(d.rights, dtype=np.int64),
             np.ascontiguousarray(d.heights, dtype=np.float64), np.ascontiguousarray(d.sizes, dtype=np.int64)]
     ptrs = [c.ctypes.data_as(ctypes.c_void_p) for c in cols]
-    cap = 80 * k
-    buf = ctypes.create_string_buffer(cap)
+    buf = np.empty(80 * k, dtype=np.uint8)   # no zero fill
     need = ctypes.c_size_t(0)
     lib = N.load(require_cuda=False)
-    rc = lib.tg_serialize_dendrogram(*ptrs, k, buf, cap, ctypes.byref(need))
+    vp = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    rc = lib.tg_serialize_dendrogram(*ptrs, k, vp(buf), buf.size, ctypes.byref(need))
     if rc == N.TG_ERR_CAPACITY:
-        buf = ctypes.create_string_buffer(need.value)
-        rc = lib.tg_serialize_dendrogram(*ptrs, k, buf, need.value, ctypes.byref(need))
+        buf = np.empty(need.value, dtype=np.uint8)
+        rc = lib.tg_serialize_dendrogram(*ptrs, k, vp(buf), buf.size, ctypes.byref(need))
     N.check("tg_serialize_dendrogram", rc)
-    return buf.raw[: need.value].decode()
+    return buf[: need.value].tobytes().decode()
 
 
 def save_dendrogram(d: Dendrogram, path) -> None:
