@@ -1281,8 +1281,6 @@ TG_API int tg_nn_chain_batch(double *mats, const int64_t *mat_off, const int64_t
     int64_t blocks = (warps * 32 + threads - 1) / threads;
     if (blocks > (int64_t)tg_num_sms() * 32) blocks = (int64_t)tg_num_sms() * 32;
     cudaStream_t st = tg_stream(stream);
-    nn_chain_kernel<<<(unsigned)blocks, threads, 0, st>>>(mats, mat_off, sizes, count, merge_off, lefts, rights, heights,
-                                                        active, slot, chain, aux_off); tg_count_launch(1);
     int64_t cblocks = count < (int64_t)tg_num_sms() * 2 ? count : (int64_t)tg_num_sms() * 2;
     const size_t nn_smem = (size_t)NN_SMEM_MAX * 9;
     // m <= NN_BIG: 512 threads (two CTAs per SM); larger: 1024 threads, one row read in flight
@@ -1310,6 +1308,10 @@ TG_API int tg_nn_chain_batch(double *mats, const int64_t *mat_off, const int64_t
                                                                           lefts, rights, heights, active, slot, chain,
                                                                           aux_off, cl_min);
     tg_count_launch(2);
+    // the warp-per-matrix chains (m <= NN_WARP_MAX) last: the large matrices' chains are the
+    // batch's critical path and should not queue behind them
+    nn_chain_kernel<<<(unsigned)blocks, threads, 0, st>>>(mats, mat_off, sizes, count, merge_off, lefts, rights, heights,
+                                                        active, slot, chain, aux_off); tg_count_launch(1);
     if (cl_on) {
         const int64_t ncl = count < (int64_t)tg_num_sms() / NN_CL ? count : (int64_t)tg_num_sms() / NN_CL;
         TG_CUDA_CHECK(cudaFuncSetAttribute(nn_chain_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
