@@ -243,6 +243,10 @@ typedef struct {
 /* H: the hub count of a hub-mode oracle (0 in exact mode); the workspace holds the
  * permuted vertex-major fp32/fp64 copies of hub_dist used by the hub-mode tiles. */
 size_t tg_group_max_workspace_bytes(int64_t n, int64_t ntiles, int64_t H);
+/* The tile list of tg_group_max_batch built on the device: tile t of sub-problem p (row-major
+ * over its nt x nt grid) = {p, 64 (t / nt), 64 (t % nt)} at tiles[subs[p].tile_off + t]
+ * (dbht.py:217-230 sub-problem layout; the host no longer builds and uploads it). */
+int tg_group_tiles_fill(const void *subs, int64_t nsub, void *tiles, int64_t ntiles, void *stream);
 /* total_len: the number of perm / gid entries (the sub-problems lie back to back). */
 int tg_group_max_batch(const tg_oracle_t *oracle, const int32_t *perm, const int32_t *gid, int64_t total_len,
                        const void *subs, int64_t nsub, const void *tiles, int64_t ntiles, double *out, int64_t out_len,

@@ -105,6 +105,7 @@ _PROTOS = {
     "tg_nn_chain_batch": (ctypes.c_int, [c_p, c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p]),
     "tg_serialize_dendrogram": (ctypes.c_int, [c_p, c_p, c_p, c_p, c_i64, c_p, c_sz, ctypes.POINTER(c_sz)]),
     "tg_cut_labels": (ctypes.c_int, [c_p, c_p, c_i64, c_i64, c_p, c_p]),
+    "tg_group_tiles_fill": (ctypes.c_int, [c_p, c_i64, c_p, c_i64, c_p]),
     "tg_release_cached_memory": (ctypes.c_int, []),
     "tg_build_hierarchy": (ctypes.c_int, [ctypes.POINTER(TgOracle), c_p, c_p, c_i64, c_p, c_p, c_p, c_p, c_p, c_p]),
 }

@@ -1212,6 +1212,33 @@ TG_API int tg_group_blocks(const tg_oracle_t *o, const int32_t *perm, const int6
     return TG_OK;
 }
 
+namespace {
+__global__ void group_tiles_fill_kernel(const GmSub *__restrict__ subs, int64_t nsub, GmTile *__restrict__ tiles,
+                                        int64_t ntiles) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = 0, hi = nsub;   // the last sub-problem with tile_off <= t
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (subs[mid].tile_off <= t) lo = mid;
+            else hi = mid;
+        }
+        const int64_t nt = (subs[lo].len + GM_TILE - 1) / GM_TILE, q = t - subs[lo].tile_off;
+        tiles[t] = GmTile{(int)lo, (int)(q / nt) * GM_TILE, (int)(q % nt) * GM_TILE};
+    }
+}
+}  // namespace
+
+TG_API int tg_group_tiles_fill(const void *subs_v, int64_t nsub, void *tiles_v, int64_t ntiles, void *stream) {
+    if (nsub < 0 || ntiles < 0 || (ntiles > 0 && (!subs_v || !tiles_v || nsub == 0))) return TG_ERR_ARG;
+    if (ntiles == 0) return TG_OK;
+    const int64_t blocks = std::min<int64_t>((ntiles + 255) / 256, (int64_t)tg_num_sms() * 8);
+    group_tiles_fill_kernel<<<(unsigned)blocks, 256, 0, tg_stream(stream)>>>(
+        reinterpret_cast<const GmSub *>(subs_v), nsub, reinterpret_cast<GmTile *>(tiles_v), ntiles);
+    tg_count_launch(1);
+    TG_LAUNCH_CHECK();
+    return TG_OK;
+}
+
 TG_API size_t tg_group_max_workspace_bytes(int64_t n, int64_t ntiles, int64_t H) {
     const size_t Hp = (size_t)((H + GM_HC - 1) / GM_HC * GM_HC);
     return tg_align_up((size_t)n * 4, 256) * 2 + tg_align_up((size_t)ntiles * GM_TILE * 8 + 8, 256) +

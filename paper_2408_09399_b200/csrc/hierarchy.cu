@@ -84,8 +84,11 @@ struct DevBuf {
 struct SideStream {
     cudaStream_t st = nullptr;
     cudaEvent_t ev = nullptr;
-    cudaError_t open(cudaStream_t main) {
-        cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    // priority: 0 = default; the stream's blocks are scheduled first when SMs free up
+    cudaError_t open(cudaStream_t main, bool high_priority = false) {
+        int lo = 0, hi = 0;
+        if (high_priority) cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        cudaError_t e = cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, high_priority ? hi : 0);
         if (e != cudaSuccess) return e;
         if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return e;
         if ((e = cudaEventRecord(ev, main)) != cudaSuccess) return e;
@@ -256,7 +259,6 @@ int collect_linkages(Ctx &cx, LinkJob &job, const std::vector<std::vector<int64_
 int launch_group_linkages(Ctx &cx, LinkJob &job, const std::vector<std::vector<Span>> &subproblems) {
     std::vector<int32_t> perm, gid;
     std::vector<tg_gm_sub_t> subs;
-    std::vector<tg_gm_tile_t> tiles;
     int64_t out_off = 0, total_len = 0, total_tiles = 0;
     for (const auto &groups : subproblems) {
         int64_t len = 0;
@@ -266,8 +268,8 @@ int launch_group_linkages(Ctx &cx, LinkJob &job, const std::vector<std::vector<S
     }
     perm.reserve(total_len);
     gid.reserve(total_len);
-    tiles.resize(total_tiles);   // filled in place below (n = 50k layer 3: 611k tiles)
-    tg_gm_tile_t *tp = tiles.data();
+    // the tile list (n = 50k layer 3: 611k tiles, 7 MB) is built on the device from subs
+    int64_t tile_off = 0;
     for (size_t p = 0; p < subproblems.size(); p++) {
         const auto &groups = subproblems[p];
         const int64_t perm_off = (int64_t)perm.size();
@@ -281,16 +283,15 @@ int launch_group_linkages(Ctx &cx, LinkJob &job, const std::vector<std::vector<S
         sd.len = len;
         sd.m = m;
         sd.out_off = out_off;
-        sd.tile_off = (int64_t)(tp - tiles.data());
+        sd.tile_off = tile_off;
         subs.push_back(sd);
-        for (int32_t i0 = 0; i0 < len; i0 += 64)
-            for (int32_t j0 = 0; j0 < len; j0 += 64) *tp++ = {(int32_t)p, i0, j0};
+        tile_off += (int64_t)((len + 63) / 64) * ((len + 63) / 64);
         job.sizes.push_back(m);
         job.mat_off.push_back(out_off);
         out_off += (int64_t)m * m;
     }
     HPROF("gl_host");
-    const int64_t ntiles = (int64_t)tiles.size();
+    const int64_t ntiles = total_tiles;
     const size_t ws_bytes = tg_group_max_workspace_bytes(cx.n, ntiles, cx.oracle->mode == 1 ? cx.oracle->H : 0);
     const size_t b_perm = tg_align_up(perm.size() * 4, 256), b_sub = tg_align_up(subs.size() * sizeof(tg_gm_sub_t), 256);
     const size_t b_tile = tg_align_up((size_t)ntiles * sizeof(tg_gm_tile_t), 256);
@@ -307,7 +308,7 @@ int launch_group_linkages(Ctx &cx, LinkJob &job, const std::vector<std::vector<S
     HC(cudaMemcpyAsync(d_perm, perm.data(), perm.size() * 4, cudaMemcpyHostToDevice, job.st));
     HC(cudaMemcpyAsync(d_gid, gid.data(), gid.size() * 4, cudaMemcpyHostToDevice, job.st));
     HC(cudaMemcpyAsync(d_sub, subs.data(), subs.size() * sizeof(tg_gm_sub_t), cudaMemcpyHostToDevice, job.st));
-    HC(cudaMemcpyAsync(d_tile, tiles.data(), (size_t)ntiles * sizeof(tg_gm_tile_t), cudaMemcpyHostToDevice, job.st));
+    HR(tg_group_tiles_fill(d_sub, (int64_t)subs.size(), d_tile, ntiles, job.st));
     HPROF("gl_h2d");
     HR(tg_group_max_batch(cx.oracle, d_perm, d_gid, (int64_t)perm.size(), d_sub, (int64_t)subs.size(), d_tile, ntiles,
                           d_out, out_off, d_ws, ws_bytes, job.st));
@@ -422,7 +423,8 @@ int build(Ctx &cx, const int64_t *vb_dev, const int64_t *vc_dev, int64_t *lefts,
         groups3.reserve(ng);
         for (size_t c = 0; c < ng; c++) groups3.push_back(Span{cflat.data() + coff[c], coff[c + 1] - coff[c]});
         HPROF("cmem");
-        HC(side3.open(cx.st));
+        // layer 3 (the n = 50k critical path: one large group max + NN-chain) ahead of layers 1-2
+        HC(side3.open(cx.st, true));
         HPROF("open3");
         j3.st = side3.st;
         HR(launch_group_linkages(cx, j3, {groups3}));
