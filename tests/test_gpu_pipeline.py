@@ -75,6 +75,23 @@ def test_pipeline_digest_configs(config, mode, digests, oracle, pkg):
     assert report.num_converging == rec[f"{mode}_num_converging"]
 
 
+@pytest.mark.parametrize("n", [13000, 26000])
+def test_pipeline_mid_size_vs_oracle(n, oracle, pkg):
+    """Sizes between the BASELINE configs (n = 13,000: one row buffer in the sort, the TMFG scan
+    state still in shared memory; n = 26,000: the partitioned long-row sort, the scan state in
+    global memory, the cluster NN-chain): the whole device pipeline on the reference-order S
+    against the oracle run in the test."""
+    from paper_2408_09399_b200 import simmatrix, synth
+    x, labels = synth.generate(3, n=n)
+    Sd = simmatrix.pearson_similarity_refexact_device(x)
+    S = Sd.cpu().numpy()
+    ref = oracle.run_stages(S, 20, "hub")
+    report, graph, dend, flat = pkg.run_stages(pkg.PipelineConfig(apsp_mode="hub", k=20), Sd, labels)
+    assert report.digest == ref["digest"]
+    assert np.array_equal(flat, ref["labels"])
+    assert report.num_converging == ref["num_converging"]
+
+
 def test_hub_query_and_block_semantics(small_cases, pkg):
     c = small_cases["n200_s"]
     S = c["S"]
