@@ -771,7 +771,7 @@ constexpr int NN_BIG = 2048;   // larger matrices: 1024 threads, 8 row entries i
 #endif
 constexpr int NN_SMALL_T = NN_SMALL_T_DEF, NN_SMALL_U = NN_SMALL_U_DEF;
 
-template <int NN_CTA_T, int NN_U>
+template <int NN_CTA_T, int NN_U, bool BIG>
 __global__ void __launch_bounds__(NN_CTA_T)
 nn_chain_cta_kernel(double *mats, const int64_t *mat_off, const int64_t *sizes, int64_t count,
                     const int64_t *merge_off, int64_t *lefts, int64_t *rights, double *heights,
@@ -788,7 +788,7 @@ nn_chain_cta_kernel(double *mats, const int64_t *mat_off, const int64_t *sizes, 
     uint8_t *s_act = reinterpret_cast<uint8_t *>(s_slot + NN_SMEM_MAX);
     for (int64_t b = blockIdx.x; b < count; b += gridDim.x) {
         const int64_t m64 = sizes[b];
-        if (m64 <= NN_WARP_MAX || (NN_CTA_T == 1024) != (m64 > NN_BIG)) continue;
+        if (m64 <= NN_WARP_MAX || BIG != (m64 > NN_BIG)) continue;
         if (cl_min > 0 && m64 >= cl_min && m64 <= NN_SMEM_MAX) continue;   // the cluster kernel's
         const int m = (int)m64;
         double *W = mats + mat_off[b];
@@ -1311,9 +1311,9 @@ TG_API int tg_nn_chain_batch(double *mats, const int64_t *mat_off, const int64_t
     int64_t cblocks = count < (int64_t)tg_num_sms() * 2 ? count : (int64_t)tg_num_sms() * 2;
     const size_t nn_smem = (size_t)NN_SMEM_MAX * 9;
     // m <= NN_BIG: 512 threads (two CTAs per SM); larger: 1024 threads, one row read in flight
-    TG_CUDA_CHECK(cudaFuncSetAttribute(nn_chain_cta_kernel<NN_SMALL_T, NN_SMALL_U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    TG_CUDA_CHECK(cudaFuncSetAttribute(nn_chain_cta_kernel<NN_SMALL_T, NN_SMALL_U, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)nn_smem));
-    TG_CUDA_CHECK(cudaFuncSetAttribute(nn_chain_cta_kernel<1024, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    TG_CUDA_CHECK(cudaFuncSetAttribute(nn_chain_cta_kernel<1024, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)nn_smem));
     // matrices with cl_min <= m <= NN_SMEM_MAX take the cluster chain (TG_NN_CLMIN: development knob, 0 = off)
     static const int cl_min = std::getenv("TG_NN_CLMIN") ? std::atoi(std::getenv("TG_NN_CLMIN")) : NN_CL_MIN;
@@ -1328,10 +1328,10 @@ TG_API int tg_nn_chain_batch(double *mats, const int64_t *mat_off, const int64_t
         TG_CUDA_CHECK(cudaEventRecord(fork, st));
         TG_CUDA_CHECK(cudaStreamWaitEvent(side, fork, 0));
     }
-    nn_chain_cta_kernel<NN_SMALL_T, NN_SMALL_U><<<(unsigned)cblocks, NN_SMALL_T, nn_smem, st>>>(mats, mat_off, sizes, count, merge_off, lefts,
+    nn_chain_cta_kernel<NN_SMALL_T, NN_SMALL_U, false><<<(unsigned)cblocks, NN_SMALL_T, nn_smem, st>>>(mats, mat_off, sizes, count, merge_off, lefts,
                                                                         rights, heights, active, slot, chain, aux_off,
                                                                         cl_min);
-    nn_chain_cta_kernel<1024, 8><<<(unsigned)cblocks, 1024, nn_smem, st>>>(mats, mat_off, sizes, count, merge_off,
+    nn_chain_cta_kernel<1024, 8, true><<<(unsigned)cblocks, 1024, nn_smem, st>>>(mats, mat_off, sizes, count, merge_off,
                                                                           lefts, rights, heights, active, slot, chain,
                                                                           aux_off, cl_min);
     tg_count_launch(2);
