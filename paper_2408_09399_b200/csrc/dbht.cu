@@ -1162,17 +1162,17 @@ TG_API int tg_bubble_sinks(const double *S, int64_t n, const int32_t *bubbles, i
         hop_pick_kernel<<<(unsigned)((L + T - 1) / T), T, 0, st>>>(src, dst, L, g, best, hops); tg_count_launch(1);
     }
     sink_init_kernel<<<(unsigned)((m + T - 1) / T), T, 0, st>>>(m, hops, sinks); tg_count_launch(1);
+    // pointer jumping: the hops follow the oriented tree (acyclic), so after ceil(log2 m) + 1
+    // doublings every bubble points at its sink (dbht.py:161-175) -- launched back to back, no
+    // host round trip per doubling
     int64_t *a = sinks, *b = tmp;
-    for (int it = 0; it < 64; it++) {
-        TG_CUDA_CHECK(cudaMemsetAsync(changed, 0, 4, st));
+    int iters = 1;
+    while (((int64_t)1 << (iters - 1)) < m) iters++;
+    for (int it = 0; it < iters; it++) {
         sink_jump_kernel<<<(unsigned)((m + T - 1) / T), T, 0, st>>>(m, a, b, changed); tg_count_launch(1);
-        int h = 0;
-        TG_CUDA_CHECK(cudaMemcpyAsync(&h, changed, 4, cudaMemcpyDeviceToHost, st));
-        TG_CUDA_CHECK(cudaStreamSynchronize(st));
         int64_t *t = a;
         a = b;
         b = t;
-        if (!h) break;
     }
     if (a != sinks) TG_CUDA_CHECK(cudaMemcpyAsync(sinks, a, m * 8, cudaMemcpyDeviceToDevice, st));
     TG_LAUNCH_CHECK();
