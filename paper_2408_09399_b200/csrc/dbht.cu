@@ -762,6 +762,7 @@ __global__ void oracle_block_kernel(tg_oracle_t o, const int32_t *rows, int64_t 
 constexpr int NN_SMEM_MAX = 7168;
 constexpr int NN_CL = 8;          // cluster NN-chain (below): CTAs per cluster
 constexpr int NN_CL_T = 256;      //   threads per CTA
+constexpr int NN_CL_U = 4;        //   row entries in flight per thread (one pass covers 1024 columns)
 constexpr int NN_CL_MIN = 2048;   //   matrices with NN_CL_MIN <= m <= NN_SMEM_MAX (HBM-resident rows;
                                   //   L2-resident smaller ones step faster in one CTA)
 constexpr int NN_BIG = 2048;   // larger matrices: 1024 threads, 8 row entries in flight per thread
@@ -993,10 +994,22 @@ nn_chain_cluster_kernel(double *mats, const int64_t *mat_off, const int64_t *siz
             const double *row = W + (int64_t)x * m;
             double bv = INFINITY, rp = INFINITY;
             int bi = INT_MAX, hp = 0;
-            for (int j = c0 + tid; j < c1; j += NN_CL_T) {
-                const double r = (act[j] && j != x) ? __ldcg(row + j) : INFINITY;
-                if (r < bv || (r == bv && j < bi)) { bv = r; bi = j; }
-                if (j == p) { rp = r; hp = 1; }
+            for (int j0 = c0 + tid; j0 < c1; j0 += NN_CL_U * NN_CL_T) {
+                double rr[NN_CL_U];
+#pragma unroll
+                for (int u = 0; u < NN_CL_U; u++) {   // the slice's loads all in flight before any use
+                    const int j = j0 + u * NN_CL_T;
+                    rr[u] = j < c1 ? __ldcg(row + j) : INFINITY;
+                }
+#pragma unroll
+                for (int u = 0; u < NN_CL_U; u++) {
+                    const int j = j0 + u * NN_CL_T;
+                    if (j < c1) {
+                        const double r = (act[j] && j != x) ? rr[u] : INFINITY;
+                        if (r < bv || (r == bv && j < bi)) { bv = r; bi = j; }
+                        if (j == p) { rp = r; hp = 1; }
+                    }
+                }
             }
             for (int o = 16; o; o >>= 1) {
                 const double r2 = __shfl_xor_sync(0xffffffffu, bv, o);
@@ -1053,11 +1066,23 @@ nn_chain_cluster_kernel(double *mats, const int64_t *mat_off, const int64_t *siz
                 nm++;
                 double *Wlo = W + (int64_t)lo * m;
                 const double *Whi = W + (int64_t)hi * m;
-                for (int j = c0 + tid; j < c1; j += NN_CL_T) {
-                    const double a = __ldcg(Wlo + j), c = __ldcg(Whi + j);
-                    const double mg = a > c ? a : (c > a ? c : a);
-                    Wlo[j] = mg;                      // row lo, own columns
-                    W[(int64_t)j * m + lo] = mg;      // column lo, own rows
+                for (int j0 = c0 + tid; j0 < c1; j0 += NN_CL_U * NN_CL_T) {
+                    double a[NN_CL_U], c[NN_CL_U];
+#pragma unroll
+                    for (int u = 0; u < NN_CL_U; u++) {
+                        const int j = j0 + u * NN_CL_T;
+                        a[u] = j < c1 ? __ldcg(Wlo + j) : 0.0;
+                        c[u] = j < c1 ? __ldcg(Whi + j) : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < NN_CL_U; u++) {
+                        const int j = j0 + u * NN_CL_T;
+                        if (j < c1) {
+                            const double mg = a[u] > c[u] ? a[u] : (c[u] > a[u] ? c[u] : a[u]);
+                            Wlo[j] = mg;                      // row lo, own columns
+                            W[(int64_t)j * m + lo] = mg;      // column lo, own rows
+                        }
+                    }
                 }
                 __syncthreads();
                 if (tid == 0) {
