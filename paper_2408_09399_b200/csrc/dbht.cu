@@ -772,6 +772,23 @@ constexpr int NN_BIG = 2048;   // larger matrices: 1024 threads, 8 row entries i
 #endif
 constexpr int NN_SMALL_T = NN_SMALL_T_DEF, NN_SMALL_U = NN_SMALL_U_DEF;
 
+// Order key of a row entry for the argmin: unsigned order = double order for every non-NaN
+// value (-0.0 keyed as +0.0: np.argmin compares them equal); NaN keys above +inf, so a NaN is
+// never the minimum (as the compare-based scans treat it).
+__device__ __forceinline__ unsigned long long nn_key(double r) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(r == 0.0 ? 0.0 : r);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// (minimum key, first index attaining it) over the warp: three REDUX steps, no shuffle tree
+__device__ __forceinline__ void nn_warp_argmin(unsigned long long k, unsigned i, unsigned &kh, unsigned &kl,
+                                               unsigned &ki) {
+    const unsigned h = (unsigned)(k >> 32), l = (unsigned)k;
+    kh = __reduce_min_sync(0xffffffffu, h);
+    kl = __reduce_min_sync(0xffffffffu, h == kh ? l : 0xffffffffu);
+    ki = __reduce_min_sync(0xffffffffu, (h == kh && l == kl) ? i : 0xffffffffu);
+}
+
 template <int NN_CTA_T, int NN_U, bool BIG>
 __global__ void __launch_bounds__(NN_CTA_T)
 nn_chain_cta_kernel(double *mats, const int64_t *mat_off, const int64_t *sizes, int64_t count,
@@ -779,11 +796,13 @@ nn_chain_cta_kernel(double *mats, const int64_t *mat_off, const int64_t *sizes, 
                     uint8_t *active_all, int64_t *slot_all, int64_t *chain_all, const int64_t *aux_off,
                     int cl_min) {
     extern __shared__ __align__(16) unsigned char nn_smem[];
-    __shared__ double rv[2][NN_CTA_T / 32];
-    __shared__ int ri[2][NN_CTA_T / 32];
-    __shared__ double sh_rp[2];
+    __shared__ uint4 part[2][NN_CTA_T / 32];   // per warp: (key hi, key lo, first index)
+    __shared__ double sh_rp[2], sh_patch;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = NN_CTA_T / 32;
+    // the next chain top's row is read together with the merged rows (one L2 round trip per
+    // merge instead of two); the big variant has no registers for a third row
+    constexpr bool PREF = !BIG;
     int32_t *s_chain = reinterpret_cast<int32_t *>(nn_smem);
     int32_t *s_slot = s_chain + NN_SMEM_MAX;
     uint8_t *s_act = reinterpret_cast<uint8_t *>(s_slot + NN_SMEM_MAX);
@@ -816,6 +835,9 @@ nn_chain_cta_kernel(double *mats, const int64_t *mat_off, const int64_t *sizes, 
         // chain's top two stay in registers, partials are double-buffered by step parity, and
         // a chain step costs one barrier (a merge: one more after its row / column pass)
         int x = 0, p = -1;
+        double rr[NN_U];
+        bool have = false;   // rr holds row x (read during the last merge; column `plo` patched)
+        int plo = -1;
         while (remaining > 1) {
             if (nchain == 0) {
                 // chain start: the first active cluster
@@ -823,56 +845,57 @@ nn_chain_cta_kernel(double *mats, const int64_t *mat_off, const int64_t *sizes, 
                 for (int i = tid; i < m; i += NN_CTA_T)
                     if (act[i]) { f = i; break; }
                 f = __reduce_min_sync(0xffffffffu, (unsigned)f);
-                if (lane == 0) ri[0][warp] = f;
+                if (lane == 0) part[0][warp].x = (unsigned)f;
                 __syncthreads();
-                int g = lane < NW ? ri[0][lane] : INT_MAX;
-                g = (int)__reduce_min_sync(0xffffffffu, (unsigned)g);
-                if (tid == 0) chain_set(0, g);
-                __syncthreads();   // ri[0] is rewritten by the next step
+                unsigned g = lane < NW ? part[0][lane].x : 0xffffffffu;
+                g = __reduce_min_sync(0xffffffffu, g);
+                if (tid == 0) chain_set(0, (int)g);
+                __syncthreads();   // part[0] is rewritten by the next step
                 nchain = 1;
-                x = g;
+                x = (int)g;
                 p = -1;
+                have = false;
             }
             const int par = step & 1;
             const double *row = W + (int64_t)x * m;
-            double bv = INFINITY;
-            int bi = INT_MAX;
+            unsigned long long bk = ~0ull;
+            unsigned bi = 0xffffffffu;
             for (int j0 = tid; j0 < m; j0 += NN_U * NN_CTA_T) {
-                double rr[NN_U];
+                if (!(PREF && have && j0 == tid)) {
 #pragma unroll
-                for (int u = 0; u < NN_U; u++) {   // all loads in flight before any use
-                    const int j = j0 + u * NN_CTA_T;
-                    rr[u] = j < m ? row[j] : INFINITY;
+                    for (int u = 0; u < NN_U; u++) {   // all loads in flight before any use
+                        const int j = j0 + u * NN_CTA_T;
+                        rr[u] = j < m ? row[j] : INFINITY;
+                    }
                 }
 #pragma unroll
                 for (int u = 0; u < NN_U; u++) {
                     const int j = j0 + u * NN_CTA_T;
                     if (j < m) {
-                        const double r = (act[j] && j != x) ? rr[u] : INFINITY;
-                        if (r < bv || (r == bv && j < bi)) { bv = r; bi = j; }
+                        double r = (act[j] && j != x) ? rr[u] : INFINITY;
+                        if (PREF && j == plo) r = sh_patch;   // W[x, lo] of the last merge
+                        const unsigned long long k = nn_key(r);
+                        if (k < bk) { bk = k; bi = (unsigned)j; }   // j ascends: first index on ties
                         if (j == p) sh_rp[par] = r;
                     }
                 }
             }
-            for (int o = 16; o; o >>= 1) {
-                const double r2 = __shfl_xor_sync(0xffffffffu, bv, o);
-                const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-                if (r2 < bv || (r2 == bv && i2 < bi)) { bv = r2; bi = i2; }
-            }
-            if (lane == 0) { rv[par][warp] = bv; ri[par][warp] = bi; }
+            have = false;
+            plo = -1;
+            unsigned kh, kl, ki;
+            nn_warp_argmin(bk, bi, kh, kl, ki);
+            if (lane == 0) part[par][warp] = make_uint4(kh, kl, ki, 0u);
             __syncthreads();
-            double v = lane < NW ? rv[par][lane] : INFINITY;
-            int i = lane < NW ? ri[par][lane] : INT_MAX;
-            for (int o = 16; o; o >>= 1) {
-                const double r2 = __shfl_xor_sync(0xffffffffu, v, o);
-                const int i2 = __shfl_xor_sync(0xffffffffu, i, o);
-                if (r2 < v || (r2 == v && i2 < i)) { v = r2; i = i2; }
+            {
+                const uint4 q = lane < NW ? part[par][lane] : make_uint4(~0u, ~0u, ~0u, 0u);
+                nn_warp_argmin(((unsigned long long)q.x << 32) | q.y, q.z, kh, kl, ki);
             }
+            const unsigned long long vk = ((unsigned long long)kh << 32) | kl;
             const double rp = p >= 0 ? sh_rp[par] : INFINITY;
             step++;
-            int y = (i == INT_MAX) ? 0 : i;   // all-inf row: np.argmin -> 0
+            int y = (int)ki;   // every column takes part (masked ones as +inf): np.argmin's index
             // linkage.py: prefer the previous chain element on ties (row[y] is the minimum v)
-            if (p >= 0 && rp == v) y = p;
+            if (p >= 0 && nn_key(rp) == vk) y = p;
             if (p >= 0 && y == p) {
                 nchain -= 2;
                 const int lo = x < y ? x : y, hi = x < y ? y : x;
@@ -884,8 +907,11 @@ nn_chain_cta_kernel(double *mats, const int64_t *mat_off, const int64_t *sizes, 
                     slot_set(lo, next_id);
                 }
                 nm++;
+                const int xn = nchain > 0 ? chain_get(nchain - 1) : -1;   // the next chain top
                 double *Wlo = W + (int64_t)lo * m;
                 const double *Whi = W + (int64_t)hi * m;
+                const double *Wxn = W + (int64_t)(xn >= 0 ? xn : 0) * m;
+                const bool pref = PREF && xn >= 0 && m <= NN_U * NN_CTA_T;
                 for (int j0 = tid; j0 < m; j0 += NN_U * NN_CTA_T) {
                     double pv[NN_U], qv[NN_U];
 #pragma unroll
@@ -893,6 +919,7 @@ nn_chain_cta_kernel(double *mats, const int64_t *mat_off, const int64_t *sizes, 
                         const int j = j0 + u * NN_CTA_T;
                         pv[u] = j < m ? Wlo[j] : 0.0;
                         qv[u] = j < m ? Whi[j] : 0.0;
+                        if (PREF && pref) rr[u] = j < m ? Wxn[j] : INFINITY;
                     }
 #pragma unroll
                     for (int u = 0; u < NN_U; u++) {
@@ -901,15 +928,18 @@ nn_chain_cta_kernel(double *mats, const int64_t *mat_off, const int64_t *sizes, 
                             const double mg = pv[u] > qv[u] ? pv[u] : (qv[u] > pv[u] ? qv[u] : pv[u]);
                             Wlo[j] = mg;
                             W[(int64_t)j * m + lo] = mg;
+                            if (PREF && j == xn) sh_patch = mg;   // = the new W[xn, lo]
                         }
                     }
                 }
                 next_id++;
                 remaining--;
-                __syncthreads();   // the merged row / column and act[hi] are visible
+                __syncthreads();   // the merged row / column, act[hi] and sh_patch are visible
                 if (nchain > 0) {
-                    x = in_smem ? s_chain[nchain - 1] : chain_get(nchain - 1);
+                    x = xn;
                     p = nchain > 1 ? chain_get(nchain - 2) : -1;
+                    have = pref;
+                    plo = pref ? lo : -1;
                 }
             } else {
                 if (nchain >= m) {  // a non-reducible (asymmetric) matrix made the chain cycle

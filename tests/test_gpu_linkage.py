@@ -32,6 +32,23 @@ def test_nn_chain_matches_oracle(m, oracle, pkg):
     assert pkg.nn_chain_merges(B) == oracle.nn_chain_merges(B)
 
 
+@pytest.mark.parametrize("m", [60, 400, 1056, 2100])
+def test_nn_chain_inf_and_signed_zero(m, oracle, pkg):
+    """+inf entries (np.argmin over an all-inf row: index 0) and -0.0 == +0.0 ties (first index)."""
+    rng = np.random.default_rng(100 + m)
+    A = rng.random((m, m))
+    D = (A + A.T) / 2
+    I = rng.random((m, m)) < 0.3
+    D[I | I.T] = np.inf
+    Z = rng.random((m, m)) < 0.01
+    D[Z] = 0.0
+    D[Z.T & ~Z] = -0.0
+    np.fill_diagonal(D, 0.0)
+    D[: m // 10, :] = np.inf              # whole rows at +inf
+    D[:, : m // 10] = np.inf
+    assert pkg.nn_chain_merges(D) == oracle.nn_chain_merges(D)
+
+
 def test_nn_chain_batch_mixed_sizes(oracle, pkg):
     import torch
     from paper_2408_09399_b200 import linkage
