@@ -304,6 +304,8 @@ def run_b200(args, world, rank, local):
         st5 = {}
         passes = []
         for rep_i in range(3):   # pass 1 warms up
+            gc.collect()   # between passes, outside the timed region: with collection paused, cycles
+            torch.cuda.empty_cache()   # kept the previous pass's 10-20 GB buffers alive (cudaMalloc inside a stage)
             flush.zero_()
             torch.cuda.synchronize()
             a, b = ev(), ev()
@@ -327,6 +329,7 @@ def run_b200(args, world, rank, local):
                "ms": round(float(np.mean([p[0] for p in passes])), 1),
                "ms_passes": [p[0] for p in passes],
                "stage_ms": {kk: round(float(np.mean([p[1][kk] for p in passes])), 2) for kk in stage_names},
+               "stage_ms_passes": [p[1] for p in passes],
                "passes": "mean of passes 2-3 (pass 1 = warm-up)"}
 
     cpu = None
@@ -354,6 +357,7 @@ def run_b200(args, world, rank, local):
             "gc": "collected before, paused through the timed measurements",
             "gpu_launches_timed_total": launches,
             "wall_s_timed": round(wall, 3), "step_ms": [round(x, 3) for x in per_step],
+            "stage_ms_steps": {kk: [round(float(x), 2) for x in vv] for kk, vv in stage.items()},
             "clocks": clocks,
             "cpu_baseline": cpu,
             "n50k": big,

@@ -429,6 +429,157 @@ __device__ void warp_entries(const TmArgs &A, const uint32_t *bits, unsigned lon
     }
 }
 
+// Fast path of one entry refresh.  When all three vertices' scan-state words certify an
+// uninserted max-corr (the common case: the cluster helpers keep the words two deep), lanes
+// 0..8 each read the word of "their" candidate's vertex (lanes of one candidate read the same
+// address in the same instruction, so they agree), load their S value and reduce -- no
+// shuffle broadcast of the words, no per-warp staging slot, no local-memory face arrays.
+
+// lane (ci, vi) = (lane / 3, lane % 3), lane < 9, holds candidate u = mc[face vertex ci] and
+// w = face vertex vi: 9 loads of S, g = (S[a,u] + S[b,u]) + S[c,u] per candidate (tmfg.py:273,
+// left to right), best of the three in (mc[a], mc[b], mc[c]) order: g desc, u asc (tmfg.py:272-276)
+__device__ __forceinline__ void entry_from_cands(const TmArgs &A, int a, int b, int c, int fid, int u, int w, Ent *out,
+                                                 int *mc_out, int *iters) {
+    const int lane = threadIdx.x & 31;
+#if TM_PROFILE
+    const long long tf1 = clock64();
+#endif
+    const double sv = lane < 9 ? __ldg(A.S + (int64_t)w * A.n + u) : 0.0;
+    const double s1 = __shfl_down_sync(0xffffffffu, sv, 1);
+#if TM_PROFILE
+    const long long tf2 = clock64() + (long long)(s1 != s1);
+    if (iters && lane == 0) iters[3] = (int)(tf2 - tf1);
+#endif
+    const double s2 = __shfl_down_sync(0xffffffffu, sv, 2);
+    const double g = __dadd_rn(__dadd_rn(sv, s1), s2);
+    const double g1 = __shfl_down_sync(0xffffffffu, g, 3), g2 = __shfl_down_sync(0xffffffffu, g, 6);
+    const int u1 = __shfl_down_sync(0xffffffffu, u, 3), u2 = __shfl_down_sync(0xffffffffu, u, 6);
+    if (mc_out && (lane == 0 || lane == 3 || lane == 6)) mc_out[lane / 3] = u;
+    if (lane == 0) {
+        double best_g = g;
+        int best_v = u;
+        if (g1 > best_g || (g1 == best_g && u1 < best_v)) { best_g = g1; best_v = u1; }
+        if (g2 > best_g || (g2 == best_g && u2 < best_v)) { best_g = g2; best_v = u2; }
+        Ent x;
+        x.g = best_g;
+        x.fid = fid;
+        x.cand = best_v;
+        x.a = a;
+        x.b = b;
+        x.c = c;
+        x.opt = 0;
+        *out = x;
+    }
+    __syncwarp();
+}
+
+// Returns false (nothing written) when a vertex needs a scan: the caller runs warp_entries.
+template <bool SMEM_ST>
+__device__ __forceinline__ bool warp_entry_fast(const TmArgs &A, const uint32_t *bits, unsigned long long *vst,
+                                                int a, int b, int c, int fid, Ent *out, int *mc_out,
+                                                int *iters = nullptr) {
+    const int lane = threadIdx.x & 31;
+    const unsigned long long *st = SMEM_ST ? vst : A.gvst;
+    const int l9 = lane < 9 ? lane : 0;
+    const int ci = l9 / 3, vi = l9 - 3 * ci;
+    const int xc = ci == 0 ? a : (ci == 1 ? b : c);
+    const int w = vi == 0 ? a : (vi == 1 ? b : c);
+    const VSt r = vst_unpack(st[xc]);
+    // both certificates' bitmap words in flight at once
+    const bool i1 = r.mc < 0 || is_ins(bits, max(r.mc, 0));
+    const bool i2 = r.mc2 < 0 || is_ins(bits, max(r.mc2, 0));
+    const int u = !i1 ? r.mc : (!i2 ? r.mc2 : -1);
+    if (__any_sync(0xffffffffu, u < 0)) return false;
+#if TM_PROFILE
+    if (lane == 0) atomicAdd(&g_tm_prof[0], 3ull);
+#endif
+    entry_from_cands(A, a, b, c, fid, u, w, out, mc_out, iters);
+    return true;
+}
+
+// One window position (queue entry *hp at position i) of the parallel phase, one warp:
+// fresh -> flags only; stale -> the refresh cache's entry if its three max-corr candidates
+// are still uninserted (a refreshed entry stays exact while they are: each is a monotone
+// fact; the cache is written only between rounds, so this read is stable), else the fast
+// refresh.  With the scan state in shared memory the cache's candidates (lanes 9..11) and
+// the scan-state words' (lanes 0..8) go through the inserted bitmap in one instruction
+// stream, so the cache check is not a dependent step before the refresh.  Returns false
+// (nothing written) when a vertex needs a scan.
+template <bool SMEM_ST>
+__device__ __forceinline__ bool window_refresh(const TmArgs &A, const uint32_t *bits, unsigned long long *vst,
+                                               const RcEnt *rcache, const Ent *hp, int i, Ent *Lref, int *Lstale,
+                                               int *Lcomp, int (*Lmc)[3], int *iters, unsigned *rc_hits) {
+    const int lane = threadIdx.x & 31;
+    const int2 fc = *reinterpret_cast<const int2 *>(&hp->fid);   // (fid, cand)
+    if (!is_ins(bits, fc.y)) {
+        if (lane == 0) { Lstale[i] = 0; Lcomp[i] = 0; }
+        return true;
+    }
+    const int4 fa = *reinterpret_cast<const int4 *>(&hp->a);     // (a, b, c, opt)
+    const int a = fa.x, b = fa.y, c = fa.z, fid = fc.x;
+    const RcEnt &rc = rcache[fid & (TM_RC - 1)];
+    const int l9 = lane < 9 ? lane : 0;
+    const int ci = l9 / 3, vi = l9 - 3 * ci;
+    const int xc = ci == 0 ? a : (ci == 1 ? b : c);
+    const int w = vi == 0 ? a : (vi == 1 ? b : c);
+    const bool rcl = lane >= 9 && lane < 12;
+    int id1, id2 = -1;
+    bool rc_ok;
+    int u;
+    if (SMEM_ST) {
+        if (rcl) {
+            id1 = rc.fid == fid ? rc.m[lane - 9] : -1;
+        } else {
+            const VSt r = vst_unpack(vst[xc]);
+            id1 = r.mc;
+            id2 = r.mc2;
+        }
+        const bool i1 = id1 < 0 || is_ins(bits, max(id1, 0));
+        const bool i2 = id2 < 0 || is_ins(bits, max(id2, 0));
+        u = !i1 ? id1 : (!i2 ? id2 : -1);
+        const unsigned okb = __ballot_sync(0xffffffffu, u >= 0);
+        rc_ok = (okb & 0xe00u) == 0xe00u;
+        if (!rc_ok && (okb & 0x1ffu) != 0x1ffu) return false;
+    } else {
+        id1 = (lane < 3 && rc.fid == fid) ? rc.m[lane] : -1;
+        const bool okc = id1 >= 0 && !is_ins(bits, id1);
+        rc_ok = (__ballot_sync(0xffffffffu, okc) & 7u) == 7u;
+        u = -1;
+        if (!rc_ok) {
+            const VSt r = vst_unpack(A.gvst[xc]);
+            const bool i1 = r.mc < 0 || is_ins(bits, max(r.mc, 0));
+            const bool i2 = r.mc2 < 0 || is_ins(bits, max(r.mc2, 0));
+            u = !i1 ? r.mc : (!i2 ? r.mc2 : -1);
+            if (__any_sync(0xffffffffu, u < 0)) return false;
+        }
+    }
+    if (rc_ok) {
+        if (lane == 0) {
+            Ent x;
+            x.g = rc.g;
+            x.fid = fid;
+            x.cand = rc.cand;
+            x.a = a;
+            x.b = b;
+            x.c = c;
+            x.opt = 0;
+            Lref[i] = x;
+            Lstale[i] = 1;
+            Lcomp[i] = 0;
+#if TM_PROFILE
+            atomicAdd(rc_hits, 1u);
+#endif
+        }
+        return true;
+    }
+#if TM_PROFILE
+    if (lane == 0) atomicAdd(&g_tm_prof[0], 3ull);
+#endif
+    if (lane == 0) { Lstale[i] = 1; Lcomp[i] = 1; }
+    entry_from_cands(A, a, b, c, fid, u, w, &Lref[i], Lmc[i], iters);
+    return true;
+}
+
 __device__ __forceinline__ void sort3(int &x, int &y, int &z) {
     int t;
     if (y < x) { t = x; x = y; y = t; }
@@ -1118,7 +1269,6 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
     const int n = A.n;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     __shared__ Ctl ctl;
-    __shared__ Ent L[TM_K];
     __shared__ Ent Lref[TM_K];
     __shared__ Ent Lout[TM_WARPS - TM_NEW_WARPS][TM_EPW];
     __shared__ int Lstale[TM_K];
@@ -1249,13 +1399,21 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
             Ent *cur = sel ? buf1 : buf0;
             if (warp < TM_NEW_WARPS) {
                 if (warp < ctl.ne_count) {
-                    int fids[1] = {ctl.ne_fid[warp]};
-                    int fvv[1][3] = {{ctl.ne_v[warp][0], ctl.ne_v[warp][1], ctl.ne_v[warp][2]}};
-                    warp_entries<SMEM_ST>(A, bits, vst, 1, fvv, fids, &NE[warp], my_iters, nullptr);
+                    const int na = ctl.ne_v[warp][0], nb_ = ctl.ne_v[warp][1], nc = ctl.ne_v[warp][2], nfid = ctl.ne_fid[warp];
+                    if (A.check || !warp_entry_fast<SMEM_ST>(A, bits, vst, na, nb_, nc, nfid, &NE[warp], nullptr)) {
+                        int fids[1] = {nfid};
+                        int fvv[1][3] = {{na, nb_, nc}};
+                        warp_entries<SMEM_ST>(A, bits, vst, 1, fvv, fids, &NE[warp], my_iters, nullptr);
+                    }
                 }
             } else {
                 int base = TM_EPW * (warp - TM_NEW_WARPS);
                 int cntL = ctl.L_count;
+                // one entry per warp: flags, refresh cache and the scan-free refresh in one lean pass
+                if (TM_EPW == 1 && !A.check && base < cntL &&
+                    window_refresh<SMEM_ST>(A, bits, vst, rcache, cur + base, base, Lref, Lstale, Lcomp, Lmc, my_iters,
+                                            &ctl.rc_hit))
+                    cntL = 0;   // handled
                 int idx[TM_EPW];
                 int cnt = 0;
                 int fids[TM_EPW];
@@ -1271,7 +1429,6 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
                         // are still uninserted (each is a monotone fact).  Decided on lane 0.
                         int hit = 0;
                         if (lane == 0) {
-                            L[i] = h;
                             Lstale[i] = stale;
                             Lcomp[i] = 0;
                             if (stale && !A.check) {
@@ -1352,7 +1509,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
         // it, so the first to claim a slot writes it.  The winner's bit is set while
         // the speculative refreshes run: they stay exact (every fact they use is
         // monotone) and the cache's candidate check rejects what the winner voids.
-        if (warp == 0) replay_warp(A, ctl, L, Lref, Lstale, NE, batch, tobuf, rk_g, rk_f, rk_src, tk_g, tk_f);
+        if (warp == 0) replay_warp(A, ctl, sel ? buf1 : buf0, Lref, Lstale, NE, batch, tobuf, rk_g, rk_f, rk_src, tk_g, tk_f);
         else if (!A.check && (warp == 1 || warp >= MW)) {
             const int round = (int)ctl.rounds;
             if (warp == 1) {
@@ -1518,7 +1675,12 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
                     A.trace[4 * t + 1] = a;
                     A.trace[4 * t + 2] = b;
                     A.trace[4 * t + 3] = c;
+#if TM_PROFILE && defined(TM_TS)
+                    // per-insertion timeline for tools/tmfg_timeline.py: clock (64-cycle units) / rounds / refills / pops
+                    A.host_fid[t] = TM_TS == 1 ? (int)(clock64() >> 6) : TM_TS == 2 ? (int)ctl.rounds : TM_TS == 3 ? (int)ctl.refills : (int)ctl.pops;
+#else
                     A.host_fid[t] = fid;
+#endif
                     int e = 6 + 3 * t;
                     int wv[3] = {a, b, c};
                     for (int q = 0; q < 3; q++) {
