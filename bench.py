@@ -53,8 +53,85 @@ def _peaks():
     return 6650.0, "fallback"
 
 
+class NvmlSampler:
+    """SM clock / throttle reasons sampled in-process through NVML (nvidia_ml_py) every 50 ms.
+
+    Preferred over the nvidia-smi subprocess below: one `nvidia-smi --query-gpu` pass holds driver
+    locks for tens of ms, and a CUDA call of the step's host phase (the hierarchy stage makes
+    hundreds) that lands behind it stalls -- two rounds of measurements read 36-50 ms outliers in
+    single steps with the subprocess sampler and none without it."""
+
+    def __init__(self, index: int):
+        import pynvml
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        # NVML enumerates physical devices: honour CUDA_VISIBLE_DEVICES when it is a plain index list
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        ids = [v.strip() for v in vis.split(",") if v.strip()]
+        phys = int(ids[index]) if ids and index < len(ids) and ids[index].isdigit() else index
+        self.h = pynvml.nvmlDeviceGetHandleByIndex(phys)
+        self.rows = []
+        self._first = 0
+        self._stop = threading.Event()
+        self._thr = None
+
+    def _sample(self):
+        nv = self.nv
+        sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        try:
+            rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:
+            rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+        self.rows.append((float(sm), float(mx), int(rs)))
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self._sample()
+            except Exception:
+                pass
+            self._stop.wait(0.05)
+
+    def start(self):
+        self._sample()   # fails here (caught by the caller) rather than silently in the thread
+        self._thr = threading.Thread(target=self._run, daemon=True)
+        self._thr.start()
+        return self
+
+    def wait_first(self, timeout: float = 5.0):
+        return self
+
+    def mark(self):
+        self._first = len(self.rows)
+        return self
+
+    def stop(self) -> dict:
+        self._stop.set()
+        if self._thr is not None:
+            self._thr.join(timeout=1.0)
+        rows = self.rows[self._first:]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        nv = self.nv
+        bits = {"hw_slowdown": getattr(nv, "nvmlClocksThrottleReasonHwSlowdown", 0x8),
+                "hw_thermal_slowdown": getattr(nv, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
+                "sw_thermal_slowdown": getattr(nv, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
+                "sw_power_cap": getattr(nv, "nvmlClocksThrottleReasonSwPowerCap", 0x4)}
+        reasons = sorted({k for r in rows for k, b in bits.items() if r[2] & b})
+        return {"sm_mhz": statistics.median([r[0] for r in rows]), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows), "sampler": "nvml"}
+
+
+def make_sampler(index: int):
+    try:
+        return NvmlSampler(index).start()
+    except Exception:
+        return ClockSampler(index).start()
+
+
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled during the timed region (fallback without NVML)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -208,7 +285,7 @@ def run_b200(args, world, rank, local):
         return d, flat, S, order
 
     # the clock sampler starts before the warm-up and has answered once before the timed region
-    sampler = ClockSampler(local).start() if rank == 0 else None
+    sampler = make_sampler(local) if rank == 0 else None
     # warm-up (also the sort-kernel timing source below)
     for _ in range(max(args.warmup, 0)):
         step(None)
@@ -301,16 +378,21 @@ def run_b200(args, world, rank, local):
         torch.cuda.empty_cache()
         x5, _ = synth.generate(5)
         X5 = torch.from_numpy(x5).to(device)
+        # S (20 GB) is an output buffer allocated once, as in the timed loop above, and the caching
+        # allocator keeps the other buffers (order: 10 GB) between passes: a pass that has to
+        # cudaMalloc tens of GB right after they were freed waits for the driver inside whichever
+        # stage allocates next (passes of 670 and 1009 ms in one run, apsp stage 12 vs 271 ms)
+        S5_buf = torch.empty((x5.shape[0], x5.shape[0]), dtype=torch.float64, device=device)
         st5 = {}
         passes = []
-        for rep_i in range(3):   # pass 1 warms up
-            gc.collect()   # between passes, outside the timed region: with collection paused, cycles
-            torch.cuda.empty_cache()   # kept the previous pass's 10-20 GB buffers alive (cudaMalloc inside a stage)
+        for rep_i in range(4):   # pass 1 warms up
+            gc.collect()   # between passes, outside the timed region (collection is paused): cycles
+            # would keep the previous pass's buffers away from the allocator's cache
             flush.zero_()
             torch.cuda.synchronize()
             a, b = ev(), ev()
             a.record()
-            S5 = simmatrix.pearson_similarity_device(X5)
+            S5 = simmatrix.pearson_similarity_device(X5, out=S5_buf)
             a2 = ev()
             a2.record()
             rep5, _, _, _ = P.run_stages(P.PipelineConfig(apsp_mode="hub", k=synth.num_clusters(5)), S5, None,
@@ -322,15 +404,14 @@ def run_b200(args, world, rank, local):
             ms5 = round(a.elapsed_time(b), 1)
             if rep_i > 0:
                 passes.append((ms5, st5))
-            del S5
-            torch.cuda.empty_cache()
+            del S5, rep5
         stage_names = passes[0][1].keys()
         big = {"workload": "BASELINE config 5: n=50000, L=256, hub APSP, heap TMFG",
                "ms": round(float(np.mean([p[0] for p in passes])), 1),
                "ms_passes": [p[0] for p in passes],
                "stage_ms": {kk: round(float(np.mean([p[1][kk] for p in passes])), 2) for kk in stage_names},
                "stage_ms_passes": [p[1] for p in passes],
-               "passes": "mean of passes 2-3 (pass 1 = warm-up)"}
+               "passes": "mean of passes 2-4 (pass 1 = warm-up)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

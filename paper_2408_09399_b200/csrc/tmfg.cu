@@ -603,8 +603,10 @@ __device__ __forceinline__ void pool_put(const TmArgs &A, unsigned long long *mi
 // Taken entries leave holes that are refilled from the pool's tail (O(taken)).
 constexpr int RF_U = 8;   // pool loads in flight per thread in the selection passes
 constexpr int RF_LOG = 11, RF_BINS = 1 << RF_LOG;   // selection histogram bins
-static_assert(RF_BINS * 4 + TM_B / 2 * 20 <= TM_B * (int)sizeof(Ent), "refill scratch overflows the spare buffer");
-static_assert(RF_BINS * 4 + TM_BMAX / 2 * 20 <= TM_BMAX * (int)sizeof(Ent), "refill scratch overflows the spare buffer");
+constexpr int RF_RB = 1024;   // bins of the counting sort that ranks the taken entries
+static_assert(2 * RF_RB <= RF_BINS, "the rank bins reuse the selection histogram");
+static_assert(RF_BINS * 4 + TM_B / 2 * 24 <= TM_B * (int)sizeof(Ent), "refill scratch overflows the spare buffer");
+static_assert(RF_BINS * 4 + TM_BMAX / 2 * 24 <= TM_BMAX * (int)sizeof(Ent), "refill scratch overflows the spare buffer");
 
 template <int NT, int QB>
 __device__ void refill(const TmArgs &A, Ctl &ctl, Ent *cur, Ent *scratch, Ent *red_e, int *red_ok, int tid) {
@@ -618,6 +620,7 @@ __device__ void refill(const TmArgs &A, Ctl &ctl, Ent *cur, Ent *scratch, Ent *r
     int *holes = takeidx + QB / 2;                         // room entries
     double *tgv = reinterpret_cast<double *>(holes + QB / 2);
     int *tfv = reinterpret_cast<int *>(tgv + QB / 2);
+    int *binned = tfv + QB / 2;                            // room entries: taken entries grouped by rank bin
     unsigned long long thr_hi = 0ull, thr_lo = 0ull;
     const bool take_all = P <= room;
     if (!take_all) {
@@ -700,6 +703,9 @@ __device__ void refill(const TmArgs &A, Ctl &ctl, Ent *cur, Ent *scratch, Ent *r
                 hi = nhi < hi ? nhi : hi;
             }
             fg_sync();
+#if TM_PROFILE
+            if (tid == 0) atomicAdd(&g_tm_prof[7], 1ull);   // selection passes over the pool (reported as spec_refreshes)
+#endif
         }
         if (need_fid) {
             // all remaining candidates share one gain: select on ~fid bytes
@@ -791,15 +797,78 @@ __device__ void refill(const TmArgs &A, Ctl &ctl, Ent *cur, Ent *scratch, Ent *r
     const int nt = ctl.refill_take;
     const int sz = ctl.size;
     const int keep = P - nt;
+    // Pop-order rank of each taken entry by a counting sort over RF_RB linear bins of the taken
+    // keys' range [threshold (or pool min), pool max] (bin 0 = largest keys), then an exact
+    // (gain desc, fid asc) rank among the few entries of its own bin -- instead of comparing
+    // every taken entry with every other (nt^2 / NT compares per thread: 15k cycles of a 38k-cycle
+    // refill at n = 10k, 38k of 128k at n = 50k).
+    int *bcnt = reinterpret_cast<int *>(scratch);   // the selection histogram is dead by now
+    int *bstart = bcnt + RF_RB;
+    const unsigned long long kmin = take_all ? ctl.pool_minkey : thr_hi;
+    const unsigned long long kspan = tg_order_key(ctl.pool_max.g) - kmin;
+    const int knb = 64 - __clzll(kspan);
+    const int kshift = knb > 10 ? knb - 10 : 0;
+    for (int i = tid; i < 2 * RF_RB; i += NT) bcnt[i] = 0;
+    // the entries' (fid, cand) and face vertices: two dependent global round trips, under the ranking
+    static_assert(QB / 2 <= NT, "one taken entry per thread");
+    int2 my_fc = make_int2(0, 0);
+    int4 my_fv = make_int4(0, 0, 0, 0);
+    if (tid < nt) {
+        my_fc = A.pool_fc[takeidx[tid]];
+        my_fv = A.fv[my_fc.x];
+    }
+    fg_sync();
+    int mybin[(QB / 2 + NT - 1) / NT];
+#pragma unroll
+    for (int q = 0; q < (QB / 2 + NT - 1) / NT; q++) {
+        const int s = tid + q * NT;
+        if (s < nt) {
+            const unsigned long long d = (tg_order_key(tgv[s]) - kmin) >> kshift;
+            mybin[q] = RF_RB - 1 - (int)(d < (unsigned long long)(RF_RB - 1) ? d : (unsigned long long)(RF_RB - 1));
+            atomicAdd(&bcnt[mybin[q]], 1);
+        }
+    }
+    fg_sync();
+    if (warp == 0) {
+        // exclusive prefix sums of the bin counts: lane l owns bins [32 l, 32 l + 32)
+        constexpr int PB = RF_RB / 32;
+        int sum = 0;
+        for (int q = 0; q < PB; q++) sum += bcnt[lane * PB + q];
+        int incl = sum;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        int acc = incl - sum;
+        for (int q = 0; q < PB; q++) {
+            bstart[lane * PB + q] = acc;
+            acc += bcnt[lane * PB + q];
+            bcnt[lane * PB + q] = 0;   // becomes the bin's fill cursor
+        }
+    }
+    fg_sync();
+#pragma unroll
+    for (int q = 0; q < (QB / 2 + NT - 1) / NT; q++) {
+        const int s = tid + q * NT;
+        if (s < nt) binned[bstart[mybin[q]] + atomicAdd(&bcnt[mybin[q]], 1)] = s;
+    }
+    fg_sync();
     // selected entries -> sorted tail of the buffer; holes below `keep` listed
-    for (int s = tid; s < nt; s += NT) {
+#pragma unroll
+    for (int q = 0; q < (QB / 2 + NT - 1) / NT; q++) {
+        const int s = tid + q * NT;
+        if (s >= nt) continue;
         const double g = tgv[s];
         const int f = tfv[s];
-        int rank = 0;
-        for (int j = 0; j < nt; j++) rank += (tgv[j] > g) | ((tgv[j] == g) & (tfv[j] < f));
+        const int b0 = bstart[mybin[q]], b1 = b0 + bcnt[mybin[q]];
+        int rank = b0;
+        for (int pj = b0; pj < b1; pj++) {
+            const int j = binned[pj];
+            rank += (tgv[j] > g) | ((tgv[j] == g) & (tfv[j] < f));
+        }
         const int i = takeidx[s];
-        const int2 fc = A.pool_fc[i];
-        const int4 fvv = A.fv[fc.x];
+        const int2 fc = my_fc;
+        const int4 fvv = my_fv;
         Ent x;
         x.g = g;
         x.fid = fc.x;
