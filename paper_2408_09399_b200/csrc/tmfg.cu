@@ -604,23 +604,31 @@ __device__ __forceinline__ void pool_put(const TmArgs &A, unsigned long long *mi
 constexpr int RF_U = 8;   // pool loads in flight per thread in the selection passes
 constexpr int RF_LOG = 11, RF_BINS = 1 << RF_LOG;   // selection histogram bins
 constexpr int RF_RB = 1024;   // bins of the counting sort that ranks the taken entries
+// Entries one refill may take: 3/4 of the queue (a refill costs about the same whatever it takes
+// -- its passes over the whole pool dominate -- so fewer, larger refills; 1/2 before)
+#ifndef TM_RF_NUM
+#define TM_RF_NUM 3
+#define TM_RF_DEN 4
+#endif
+constexpr int rf_room(int qb) { return qb * TM_RF_NUM / TM_RF_DEN; }
 static_assert(2 * RF_RB <= RF_BINS, "the rank bins reuse the selection histogram");
-static_assert(RF_BINS * 4 + TM_B / 2 * 24 <= TM_B * (int)sizeof(Ent), "refill scratch overflows the spare buffer");
-static_assert(RF_BINS * 4 + TM_BMAX / 2 * 24 <= TM_BMAX * (int)sizeof(Ent), "refill scratch overflows the spare buffer");
+static_assert(RF_BINS * 4 + rf_room(TM_B) * 24 <= TM_B * (int)sizeof(Ent), "refill scratch overflows the spare buffer");
+static_assert(RF_BINS * 4 + rf_room(TM_BMAX) * 24 <= TM_BMAX * (int)sizeof(Ent), "refill scratch overflows the spare buffer");
 
 template <int NT, int QB>
 __device__ void refill(const TmArgs &A, Ctl &ctl, Ent *cur, Ent *scratch, Ent *red_e, int *red_ok, int tid) {
     const int lane = tid & 31, warp = tid >> 5;
     const int P = ctl.pool_count;
-    const int room = min(QB - ctl.size, QB / 2);
+    constexpr int RM = rf_room(QB);
+    const int room = min(QB - ctl.size, RM);
 #if TM_PROFILE
     long long rc0 = fg_sync_clock(), rc1;
 #endif
     int *takeidx = reinterpret_cast<int *>(scratch) + RF_BINS;   // room entries (after the histogram)
-    int *holes = takeidx + QB / 2;                         // room entries
-    double *tgv = reinterpret_cast<double *>(holes + QB / 2);
-    int *tfv = reinterpret_cast<int *>(tgv + QB / 2);
-    int *binned = tfv + QB / 2;                            // room entries: taken entries grouped by rank bin
+    int *holes = takeidx + RM;                         // room entries
+    double *tgv = reinterpret_cast<double *>(holes + RM);
+    int *tfv = reinterpret_cast<int *>(tgv + RM);
+    int *binned = tfv + RM;                            // room entries: taken entries grouped by rank bin
     unsigned long long thr_hi = 0ull, thr_lo = 0ull;
     const bool take_all = P <= room;
     if (!take_all) {
@@ -810,17 +818,23 @@ __device__ void refill(const TmArgs &A, Ctl &ctl, Ent *cur, Ent *scratch, Ent *r
     const int kshift = knb > 10 ? knb - 10 : 0;
     for (int i = tid; i < 2 * RF_RB; i += NT) bcnt[i] = 0;
     // the entries' (fid, cand) and face vertices: two dependent global round trips, under the ranking
-    static_assert(QB / 2 <= NT, "one taken entry per thread");
-    int2 my_fc = make_int2(0, 0);
-    int4 my_fv = make_int4(0, 0, 0, 0);
-    if (tid < nt) {
-        my_fc = A.pool_fc[takeidx[tid]];
-        my_fv = A.fv[my_fc.x];
+    constexpr int PT = (RM + NT - 1) / NT;   // taken entries per thread
+    int2 my_fc[PT];
+    int4 my_fv[PT];
+#pragma unroll
+    for (int q = 0; q < PT; q++) {
+        my_fc[q] = make_int2(0, 0);
+        if (tid + q * NT < nt) my_fc[q] = A.pool_fc[takeidx[tid + q * NT]];
+    }
+#pragma unroll
+    for (int q = 0; q < PT; q++) {
+        my_fv[q] = make_int4(0, 0, 0, 0);
+        if (tid + q * NT < nt) my_fv[q] = A.fv[my_fc[q].x];
     }
     fg_sync();
-    int mybin[(QB / 2 + NT - 1) / NT];
+    int mybin[PT];
 #pragma unroll
-    for (int q = 0; q < (QB / 2 + NT - 1) / NT; q++) {
+    for (int q = 0; q < PT; q++) {
         const int s = tid + q * NT;
         if (s < nt) {
             const unsigned long long d = (tg_order_key(tgv[s]) - kmin) >> kshift;
@@ -848,14 +862,14 @@ __device__ void refill(const TmArgs &A, Ctl &ctl, Ent *cur, Ent *scratch, Ent *r
     }
     fg_sync();
 #pragma unroll
-    for (int q = 0; q < (QB / 2 + NT - 1) / NT; q++) {
+    for (int q = 0; q < PT; q++) {
         const int s = tid + q * NT;
         if (s < nt) binned[bstart[mybin[q]] + atomicAdd(&bcnt[mybin[q]], 1)] = s;
     }
     fg_sync();
     // selected entries -> sorted tail of the buffer; holes below `keep` listed
 #pragma unroll
-    for (int q = 0; q < (QB / 2 + NT - 1) / NT; q++) {
+    for (int q = 0; q < PT; q++) {
         const int s = tid + q * NT;
         if (s >= nt) continue;
         const double g = tgv[s];
@@ -867,8 +881,8 @@ __device__ void refill(const TmArgs &A, Ctl &ctl, Ent *cur, Ent *scratch, Ent *r
             rank += (tgv[j] > g) | ((tgv[j] == g) & (tfv[j] < f));
         }
         const int i = takeidx[s];
-        const int2 fc = my_fc;
-        const int4 fvv = my_fv;
+        const int2 fc = my_fc[q];
+        const int4 fvv = my_fv[q];
         Ent x;
         x.g = g;
         x.fid = fc.x;
