@@ -62,7 +62,11 @@ constexpr int TM_MERGE_WARPS = TM_MERGE_WARPS_DEF;            // replay + merge 
 template <bool SMEM_ST>
 __host__ __device__ constexpr int tm_merge_warps() { return SMEM_ST ? TM_FG_WARPS : TM_MERGE_WARPS; }
 #ifndef TM_B_DEF
-#define TM_B_DEF 896    // measured: 640 / 768 / 896 / 1024 -> 87.6 / 86-88 / 86.2 / 87.6 ms at n = 10k, 588 / 572 / 576 / 587 ms at 50k
+// measured after the refill's counting-sort ranking and 3/4 take (refills got ~2x cheaper, so a shorter queue -- a
+// shorter merge -- pays): 512 (1/2 take) / 608 / 640 / 704 / 768 / 896 / 1024 -> 75.4 / 69.4 / 69.3 / 69.3 / 69.4 /
+// 70.1 / 71.8 ms at n = 10k, 503 / 511 / 449-452 / 455 / 455 / 463 / 469 ms at n = 50k (queue 2x these there);
+// before: 640 / 768 / 896 / 1024 -> 87.6 / 86-88 / 86.2 / 87.6 ms at n = 10k
+#define TM_B_DEF 640
 #endif
 constexpr int TM_B = TM_B_DEF;                  // shared-memory queue capacity (scan state in smem)
 constexpr int TM_BMAX = 2 * TM_B;               // ... when the scan state lives in global memory (large n):
