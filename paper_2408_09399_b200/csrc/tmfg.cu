@@ -50,7 +50,12 @@ constexpr int TM_FG_WARPS = TM_WARPS - TM_BG_WARPS;
 constexpr int TM_FG_T = TM_FG_WARPS * 32;
 constexpr int TM_EPW = 1;                       // entries refreshed per warp
 constexpr int TM_NEW_WARPS = 4;                 // warps that build new-face entries
-constexpr int TM_K = TM_EPW * (TM_FG_WARPS - TM_NEW_WARPS);  // top-K speculated per round
+constexpr int TM_CH = TM_FG_WARPS - TM_NEW_WARPS;  // window entries per replay chunk (one per window warp)
+#ifndef TM_WPE_DEF
+#define TM_WPE_DEF 2
+#endif
+constexpr int TM_WPE = TM_WPE_DEF;               // window entries per warp (one per half-warp): replay chunks per round
+constexpr int TM_K = TM_WPE * TM_CH;             // top-K speculated per round
 #ifndef TM_MERGE_WARPS_DEF
 #define TM_MERGE_WARPS_DEF 28   // (the kernel picks per instantiation: see tm_merge_warps)
 #endif
@@ -74,7 +79,8 @@ constexpr int TM_BMAX = 2 * TM_B;               // ... when the scan state lives
 template <bool SMEM_ST>
 __host__ __device__ constexpr int tm_qb() { return SMEM_ST ? TM_B : TM_BMAX; }
 constexpr int TM_BATCH = TM_K + 8;
-static_assert(TM_K <= 32, "replay_warp maps one queue position per lane");
+static_assert(TM_CH <= 32, "replay_warp maps one queue position of a chunk per lane");
+static_assert(TM_WPE == 1 || TM_WPE == 2, "window_refresh2 serves one entry per half-warp");
 
 struct Ent {
     double g;
@@ -584,6 +590,109 @@ __device__ __forceinline__ bool window_refresh(const TmArgs &A, const uint32_t *
     return true;
 }
 
+// Two window entries per warp, one per half-warp (entry of half h at queue position base + h * TM_CH):
+// window_refresh's logic with lanes 16 h + (0..8) on the scan-state words and 16 h + (9..11) on the
+// refresh cache, so a round speculates over TM_K = 2 TM_CH queue positions in the latency of one
+// refresh.  Returns the halves (bits 0..1) whose entry needs a scan (nothing written for them).
+template <bool SMEM_ST>
+__device__ __forceinline__ unsigned window_refresh2(const TmArgs &A, const uint32_t *bits, unsigned long long *vst,
+                                                    const RcEnt *rcache, const Ent *cur, int base, int cntL,
+                                                    Ent *Lref, int *Lstale, int *Lcomp, int (*Lmc)[3],
+                                                    unsigned *rc_hits) {
+    const int lane = threadIdx.x & 31;
+    const int h = lane >> 4, l = lane & 15;
+    const int i = base + h * TM_CH;
+    const bool valid = i < cntL;
+    const Ent *hp = cur + (valid ? i : base);
+    const int2 fc = *reinterpret_cast<const int2 *>(&hp->fid);   // (fid, cand)
+    const bool stale = valid && is_ins(bits, fc.y);
+    if (!__any_sync(0xffffffffu, stale)) {
+        if (valid && l == 0) { Lstale[i] = 0; Lcomp[i] = 0; }
+        return 0u;
+    }
+    const int4 fa = *reinterpret_cast<const int4 *>(&hp->a);     // (a, b, c, opt)
+    const int a = fa.x, b = fa.y, c = fa.z, fid = fc.x;
+    const RcEnt &rc = rcache[fid & (TM_RC - 1)];
+    const int l9 = l < 9 ? l : 0;
+    const int ci = l9 / 3, vi = l9 - 3 * ci;
+    int xc = c, w = c;   // selects, not branches
+    xc = ci == 1 ? b : xc;
+    xc = ci == 0 ? a : xc;
+    w = vi == 1 ? b : w;
+    w = vi == 0 ? a : w;
+    const bool rcl = l >= 9 && l < 12;
+    int id1 = -1, id2 = -1;
+    bool rc_ok, fast_ok;
+    int u;
+    if (SMEM_ST) {
+        if (stale) {
+            if (rcl) {
+                id1 = rc.fid == fid ? rc.m[l - 9] : -1;
+            } else {
+                const VSt r = vst_unpack(vst[xc]);
+                id1 = r.mc;
+                id2 = r.mc2;
+            }
+        }
+        const bool i1 = id1 < 0 || is_ins(bits, max(id1, 0));
+        const bool i2 = id2 < 0 || is_ins(bits, max(id2, 0));
+        u = !i1 ? id1 : (!i2 ? id2 : -1);
+        const unsigned okb = (__ballot_sync(0xffffffffu, u >= 0) >> (16 * h)) & 0xffffu;
+        rc_ok = (okb & 0xe00u) == 0xe00u;
+        fast_ok = (okb & 0x1ffu) == 0x1ffu;
+    } else {
+        id1 = (stale && l < 3 && rc.fid == fid) ? rc.m[l] : -1;
+        const bool okc = id1 >= 0 && !is_ins(bits, id1);
+        rc_ok = ((__ballot_sync(0xffffffffu, okc) >> (16 * h)) & 7u) == 7u;
+        u = -1;
+        if (stale && !rc_ok) {
+            const VSt r = vst_unpack(A.gvst[xc]);
+            const bool i1 = r.mc < 0 || is_ins(bits, max(r.mc, 0));
+            const bool i2 = r.mc2 < 0 || is_ins(bits, max(r.mc2, 0));
+            u = !i1 ? r.mc : (!i2 ? r.mc2 : -1);
+        }
+        fast_ok = ((__ballot_sync(0xffffffffu, u >= 0) >> (16 * h)) & 0x1ffu) == 0x1ffu;
+    }
+    const bool need_S = stale && !rc_ok && fast_ok;
+    const bool slow = stale && !rc_ok && !fast_ok;
+    const double sv = (need_S && l < 9) ? __ldg(A.S + (int64_t)w * A.n + u) : 0.0;
+    const double s1 = __shfl_down_sync(0xffffffffu, sv, 1);
+    const double s2 = __shfl_down_sync(0xffffffffu, sv, 2);
+    const double g = __dadd_rn(__dadd_rn(sv, s1), s2);   // (S[a,u] + S[b,u]) + S[c,u]  (tmfg.py:273)
+    const double g1 = __shfl_down_sync(0xffffffffu, g, 3), g2 = __shfl_down_sync(0xffffffffu, g, 6);
+    const int u1 = __shfl_down_sync(0xffffffffu, u, 3), u2 = __shfl_down_sync(0xffffffffu, u, 6);
+    if (need_S && l < 9 && vi == 0) Lmc[i][ci] = u;
+    if (valid && l == 0 && !slow) {
+        Lstale[i] = stale;
+        Lcomp[i] = need_S;
+        if (stale) {
+            Ent x;
+            if (rc_ok) {
+                x.g = rc.g;
+                x.cand = rc.cand;
+#if TM_PROFILE
+                atomicAdd(rc_hits, 1u);
+#endif
+            } else {
+                double best_g = g;   // (mc[a], mc[b], mc[c]) order: g desc, u asc (tmfg.py:272-276)
+                int best_v = u;
+                if (g1 > best_g || (g1 == best_g && u1 < best_v)) { best_g = g1; best_v = u1; }
+                if (g2 > best_g || (g2 == best_g && u2 < best_v)) { best_g = g2; best_v = u2; }
+                x.g = best_g;
+                x.cand = best_v;
+            }
+            x.fid = fid;
+            x.a = a;
+            x.b = b;
+            x.c = c;
+            x.opt = 0;
+            Lref[i] = x;
+        }
+    }
+    const unsigned sb = __ballot_sync(0xffffffffu, slow && l == 0);
+    return (sb & 1u) | ((sb >> 15) & 2u);
+}
+
 __device__ __forceinline__ void sort3(int &x, int &y, int &z) {
     int t;
     if (y < x) { t = x; x = y; y = t; }
@@ -944,8 +1053,8 @@ __device__ __forceinline__ bool kgt(double g1, int f1, double g2, int f2) {
     return (g1 > g2) | ((g1 == g2) & (f1 < f2));
 }
 
-// Replays the lazy heap's pops for one round (one lane per queue position,
-// TM_K <= 32).  Entries L[0..Lc) are the queue head in pop order; Lstale/Lref
+// Replays the lazy heap's pops for one round (chunks of TM_CH window positions, one lane per
+// position).  Entries L[0..Lc) are the queue head in pop order; Lstale/Lref
 // say which are stale and their refreshed entry under the current inserted
 // set; NE are the fresh entries of the faces made by the last insertion (not
 // queued yet).  Sequentially: pop the max of (L[i], best refreshed so far, best
@@ -973,79 +1082,97 @@ __device__ void replay_warp(const TmArgs &A, Ctl &ctl, const Ent *L, const Ent *
         }
     }
     const bool have_ne = ni >= 0;
-    // this lane's queue position
-    const bool v = lane < Lc;
-    const bool st = v && Lstale[lane];
-    const double hg = v ? L[lane].g : 0.0;
-    const int hf = v ? L[lane].fid : 0;
-    const double rg = st ? Lref[lane].g : 0.0;
-    const int rf = st ? Lref[lane].fid : 0;
-    // inclusive prefix max of refreshed entries, carrying their position
-    double ig = rg;
-    int ifd = rf, iix = lane;
-    bool iok = st;
+    // The window is replayed in chunks of TM_CH positions (one lane per position); a chunk in which
+    // nothing fresh pops hands the best of its refreshed entries on to the next as the carry
+    // (cg, cf, cix): every one of its entries popped stale and pushed its refreshed entry.
+    double cg = 0.0;
+    int cf = 0, cix = -1;
+    bool cok = false;
+    int istar = Lc;               // window position of the first fresh pop (Lc: none)
+    int kind = 0, widx = -1;      // 1 = queue entry, 2 = refreshed entry, 3 = new entry
+    int ginc = 0;
+    for (int c0 = 0; c0 < Lc; c0 += TM_CH) {
+        const int pos = c0 + lane;
+        const bool v = lane < TM_CH && pos < Lc;
+        const bool st = v && Lstale[pos];
+        const double hg = v ? L[pos].g : 0.0;
+        const int hf = v ? L[pos].fid : 0;
+        const double rg = st ? Lref[pos].g : 0.0;
+        const int rf = st ? Lref[pos].fid : 0;
+        // inclusive prefix max of the chunk's refreshed entries, carrying their window position
+        double ig = rg;
+        int ifd = rf, iix = pos;
+        bool iok = st;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const double g2 = __shfl_up_sync(0xffffffffu, ig, o);
-        const int f2 = __shfl_up_sync(0xffffffffu, ifd, o);
-        const int x2 = __shfl_up_sync(0xffffffffu, iix, o);
-        const bool k2 = __shfl_up_sync(0xffffffffu, (int)iok, o) != 0;
-        const bool take = (lane >= o) & k2 & ((!iok) | kgt(g2, f2, ig, ifd));
-        ig = take ? g2 : ig;
-        ifd = take ? f2 : ifd;
-        iix = take ? x2 : iix;
-        iok = iok | take;
-    }
-    const double eg = __shfl_up_sync(0xffffffffu, ig, 1);
-    const int ef = __shfl_up_sync(0xffffffffu, ifd, 1);
-    const int eix = __shfl_up_sync(0xffffffffu, iix, 1);
-    const bool eok = (lane > 0) & (__shfl_up_sync(0xffffffffu, (int)iok, 1) != 0);
-    const bool c = v & ((!st) | (eok & kgt(eg, ef, hg, hf)) | (have_ne & kgt(ng, nf, hg, hf)));
-    const unsigned bc = __ballot_sync(0xffffffffu, c);
-#if TM_PROFILE
-    const long long rp1 = clock64() + (bc & 0u);
-#endif
-    const int istar = bc ? __ffs(bc) - 1 : Lc;
-    // tmfg.py:425-431 counters over the stale pops j < istar (+ the check_invariants assertion)
-    const bool rose = st & (lane < istar) & (rg > __dadd_rn(hg, 1e-12));
-    const int ginc = __popc(__ballot_sync(0xffffffffu, rose));
-    if (A.check) {
-        const unsigned bb = __ballot_sync(0xffffffffu, rose && Lref[lane].opt);
-        if (bb) {
-            if (lane == __ffs(bb) - 1) {
-                ctl.bad = 2;
-                A.stats[4] = rf;
-                A.stats[5] = __double_as_longlong(hg);
-                A.stats[6] = __double_as_longlong(rg);
-                ctl.winner = 0;
-                ctl.exhausted = 0;
-                ctl.removed = 0;
-                ctl.nbuf_new = 0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const double g2 = __shfl_up_sync(0xffffffffu, ig, o);
+            const int f2 = __shfl_up_sync(0xffffffffu, ifd, o);
+            const int x2 = __shfl_up_sync(0xffffffffu, iix, o);
+            const bool k2 = __shfl_up_sync(0xffffffffu, (int)iok, o) != 0;
+            const bool take = (lane >= o) & k2 & ((!iok) | kgt(g2, f2, ig, ifd));
+            ig = take ? g2 : ig;
+            ifd = take ? f2 : ifd;
+            iix = take ? x2 : iix;
+            iok = iok | take;
+        }
+        // exclusive prefix, then the carry of the earlier chunks
+        double eg = __shfl_up_sync(0xffffffffu, ig, 1);
+        int ef = __shfl_up_sync(0xffffffffu, ifd, 1);
+        int eix = __shfl_up_sync(0xffffffffu, iix, 1);
+        bool eok = (lane > 0) & (__shfl_up_sync(0xffffffffu, (int)iok, 1) != 0);
+        if (cok && (!eok || kgt(cg, cf, eg, ef))) { eg = cg; ef = cf; eix = cix; eok = true; }
+        const bool c = v & ((!st) | (eok & kgt(eg, ef, hg, hf)) | (have_ne & kgt(ng, nf, hg, hf)));
+        const unsigned bc = __ballot_sync(0xffffffffu, c);
+        const int nv = min(TM_CH, Lc - c0);
+        const int il = bc ? __ffs(bc) - 1 : nv;   // stale pops of this chunk
+        // tmfg.py:425-431 counters over the stale pops (+ the check_invariants assertion)
+        const bool rose = st & (lane < il) & (rg > __dadd_rn(hg, 1e-12));
+        ginc += __popc(__ballot_sync(0xffffffffu, rose));
+        if (A.check) {
+            const unsigned bb = __ballot_sync(0xffffffffu, rose && Lref[pos].opt);
+            if (bb) {
+                if (lane == __ffs(bb) - 1) {
+                    ctl.bad = 2;
+                    A.stats[4] = rf;
+                    A.stats[5] = __double_as_longlong(hg);
+                    A.stats[6] = __double_as_longlong(rg);
+                    ctl.winner = 0;
+                    ctl.exhausted = 0;
+                    ctl.removed = 0;
+                    ctl.nbuf_new = 0;
+                }
+                __syncwarp();
+                return;
             }
-            __syncwarp();
-            return;
         }
+        if (bc) {
+            // the winner: evaluated by the lane at the first fresh pop
+            int k_l = 1, w_l = pos;
+            double tg = hg;
+            int tf = hf;
+            if (have_ne & kgt(ng, nf, tg, tf)) { tg = ng; tf = nf; k_l = 3; w_l = ni; }
+            if (eok & kgt(eg, ef, tg, tf)) { k_l = 2; w_l = eix; }
+            kind = __shfl_sync(0xffffffffu, k_l, il);
+            widx = __shfl_sync(0xffffffffu, w_l, il);
+            istar = c0 + il;
+            break;
+        }
+        // nothing fresh popped: the chunk's best refreshed entry joins the carry
+        const double ag = __shfl_sync(0xffffffffu, ig, 31);
+        const int af = __shfl_sync(0xffffffffu, ifd, 31);
+        const int ax = __shfl_sync(0xffffffffu, iix, 31);
+        const bool aok = __shfl_sync(0xffffffffu, (int)iok, 31) != 0;
+        if (aok && (!cok || kgt(ag, af, cg, cf))) { cg = ag; cf = af; cix = ax; cok = true; }
     }
-    // the winner: evaluated by the lane at istar (or from the full prefix max)
+#if TM_PROFILE
+    const long long rp1 = clock64() + (istar & 0);
+#endif
     const bool more = (ctl.size > Lc) || (ctl.pool_count > 0);
-    int kind = 0, widx = -1;   // 1 = queue entry, 2 = refreshed entry, 3 = new entry
-    {
-        int k_l = 1, w_l = lane;
-        double tg = hg;
-        int tf = hf;
-        if (have_ne & kgt(ng, nf, tg, tf)) { tg = ng; tf = nf; k_l = 3; w_l = ni; }
-        if (eok & kgt(eg, ef, tg, tf)) { k_l = 2; w_l = eix; }
-        if (istar < Lc) {
-            kind = __shfl_sync(0xffffffffu, k_l, istar);
-            widx = __shfl_sync(0xffffffffu, w_l, istar);
-        } else if (!more) {
-            const double ag = __shfl_sync(0xffffffffu, ig, 31);
-            const int af = __shfl_sync(0xffffffffu, ifd, 31);
-            const int ax = __shfl_sync(0xffffffffu, iix, 31);
-            const bool aok = __shfl_sync(0xffffffffu, (int)iok, 31) != 0;
-            if (have_ne && ((!aok) | kgt(ng, nf, ag, af))) { kind = 3; widx = ni; }
-            else if (aok) { kind = 2; widx = ax; }
-        }
+    if (istar >= Lc && !more) {
+        // the whole queue popped stale and nothing is left behind it: the best of the refreshed
+        // and new entries is the next pop, and it is fresh
+        if (have_ne && ((!cok) | kgt(ng, nf, cg, cf))) { kind = 3; widx = ni; }
+        else if (cok) { kind = 2; widx = cix; }
     }
     const int npop = istar < Lc ? istar : Lc;   // stale pops
     if (lane == 0) {
@@ -1068,28 +1195,39 @@ __device__ void replay_warp(const TmArgs &A, Ctl &ctl, const Ent *L, const Ent *
     const bool pm = ctl.pool_has_max;
     const double pg = ctl.pool_max.g;
     const int pf = ctl.pool_max.fid;
-    const bool br = st & (lane < npop) & !((kind == 2) & (widx == lane));
-    const bool bn = (lane < nec) & !((kind == 3) & (widx == lane));
-    const double nlg = bn ? NE[lane].g : 0.0;
-    const int nlf = bn ? NE[lane].fid : 0;
-    const bool fr = br & ((!pm) | kgt(rg, rf, pg, pf));
-    const bool fnn = bn & ((!pm) | kgt(nlg, nlf, pg, pf));
-    const bool pr = br & !fr, pn = bn & !fnn;
     const unsigned lt = (1u << lane) - 1u;
-    const unsigned bfr = __ballot_sync(0xffffffffu, fr), bfn = __ballot_sync(0xffffffffu, fnn);
-    const unsigned bpr = __ballot_sync(0xffffffffu, pr), bpn = __ballot_sync(0xffffffffu, pn);
-    const int nfr = __popc(bfr);
-    const int nbuf = nfr + __popc(bfn);
-    // keys of the buffer-bound entries (src >= 0: Lref index, src < 0: ~NE index)
-    if (fr) { const int o = __popc(bfr & lt); kg[o] = rg; kf[o] = rf; ksrc[o] = lane; }
-    if (fnn) { const int o = nfr + __popc(bfn & lt); kg[o] = nlg; kf[o] = nlf; ksrc[o] = ~lane; }
     const int pc = ctl.pool_count;
-    const int npr = __popc(bpr);
-    if (pr) pool_put(A, &ctl.pool_minkey, pc + __popc(bpr & lt), Lref[lane]);
-    if (pn) pool_put(A, &ctl.pool_minkey, pc + npr + __popc(bpn & lt), NE[lane]);
+    int nk = 0, npool = 0;   // buffer-bound keys listed, pool entries written
+    for (int c0 = 0; c0 < npop; c0 += TM_CH) {
+        const int pos = c0 + lane;
+        const bool br = lane < TM_CH && pos < npop && Lstale[pos] && !((kind == 2) & (widx == pos));
+        const double rg = br ? Lref[pos].g : 0.0;
+        const int rf = br ? Lref[pos].fid : 0;
+        const bool fr = br & ((!pm) | kgt(rg, rf, pg, pf));
+        const bool pr = br & !fr;
+        const unsigned bfr = __ballot_sync(0xffffffffu, fr), bpr = __ballot_sync(0xffffffffu, pr);
+        // keys of the buffer-bound entries (src >= 0: Lref index, src < 0: ~NE index)
+        if (fr) { const int o = nk + __popc(bfr & lt); kg[o] = rg; kf[o] = rf; ksrc[o] = pos; }
+        if (pr) pool_put(A, &ctl.pool_minkey, pc + npool + __popc(bpr & lt), Lref[pos]);
+        nk += __popc(bfr);
+        npool += __popc(bpr);
+    }
+    {
+        const bool bn = (lane < nec) & !((kind == 3) & (widx == lane));
+        const double nlg = bn ? NE[lane].g : 0.0;
+        const int nlf = bn ? NE[lane].fid : 0;
+        const bool fnn = bn & ((!pm) | kgt(nlg, nlf, pg, pf));
+        const bool pn = bn & !fnn;
+        const unsigned bfn = __ballot_sync(0xffffffffu, fnn), bpn = __ballot_sync(0xffffffffu, pn);
+        if (fnn) { const int o = nk + __popc(bfn & lt); kg[o] = nlg; kf[o] = nlf; ksrc[o] = ~lane; }
+        if (pn) pool_put(A, &ctl.pool_minkey, pc + npool + __popc(bpn & lt), NE[lane]);
+        nk += __popc(bfn);
+        npool += __popc(bpn);
+    }
+    const int nbuf = nk;
     __syncwarp();
     if (lane == 0) {
-        ctl.pool_count = pc + npr + __popc(bpn);
+        ctl.pool_count = pc + npool;
         ctl.nbuf_new = nbuf;
     }
 #if TM_PROFILE
@@ -1494,77 +1632,56 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
                     }
                 }
             } else {
-                int base = TM_EPW * (warp - TM_NEW_WARPS);
-                int cntL = ctl.L_count;
-                // one entry per warp: flags, refresh cache and the scan-free refresh in one lean pass
-                if (TM_EPW == 1 && !A.check && base < cntL &&
-                    window_refresh<SMEM_ST>(A, bits, vst, rcache, cur + base, base, Lref, Lstale, Lcomp, Lmc, my_iters,
-                                            &ctl.rc_hit))
-                    cntL = 0;   // handled
-                int idx[TM_EPW];
-                int cnt = 0;
-                int fids[TM_EPW];
-                int fvv[TM_EPW][3];
-#pragma unroll
-                for (int q = 0; q < TM_EPW; q++) {
-                    int i = base + q;
-                    if (i < cntL) {
-                        Ent h = cur[i];
-                        bool stale = is_ins(bits, h.cand);
-                        // refresh cache (written only between rounds, so this read is stable):
-                        // a refreshed entry stays exact while its three max-corr candidates
-                        // are still uninserted (each is a monotone fact).  Decided on lane 0.
-                        int hit = 0;
-                        if (lane == 0) {
-                            Lstale[i] = stale;
-                            Lcomp[i] = 0;
-                            if (stale && !A.check) {
-                                const RcEnt &rc = rcache[h.fid & (TM_RC - 1)];
-                                if (rc.fid == h.fid && rc.m[0] >= 0 && rc.m[1] >= 0 && rc.m[2] >= 0 &&
-                                    !is_ins(bits, rc.m[0]) && !is_ins(bits, rc.m[1]) && !is_ins(bits, rc.m[2])) {
-                                    Ent x = h;
-                                    x.g = rc.g;
-                                    x.cand = rc.cand;
-                                    x.opt = 0;
-                                    Lref[i] = x;
-                                    hit = 1;
+                // window warp j serves queue positions j and j + TM_CH (one per half-warp) on the lean
+                // path; what needs a scan (or check_invariants mode) goes through warp_entries
+                const int j = warp - TM_NEW_WARPS;
+                const int cntL = ctl.L_count;
+                unsigned todo = 0u;
+                if (A.check) {
+                    todo = (j < cntL ? 1u : 0u) | ((TM_WPE > 1 && j + TM_CH < cntL) ? 2u : 0u);
+                } else if (j < cntL) {
+                    if (TM_WPE == 2)
+                        todo = window_refresh2<SMEM_ST>(A, bits, vst, rcache, cur, j, cntL, Lref, Lstale, Lcomp, Lmc,
+                                                        &ctl.rc_hit);
+                    else
+                        todo = window_refresh<SMEM_ST>(A, bits, vst, rcache, cur + j, j, Lref, Lstale, Lcomp, Lmc,
+                                                       my_iters, &ctl.rc_hit) ? 0u : 1u;
+                }
+                for (int hh = 0; hh < TM_WPE; hh++) {
+                    if (!((todo >> hh) & 1u)) continue;
+                    const int i = j + hh * TM_CH;
+                    const Ent h = cur[i];
+                    const bool stale = is_ins(bits, h.cand);
+                    // refresh cache (written only between rounds, so this read is stable):
+                    // a refreshed entry stays exact while its three max-corr candidates
+                    // are still uninserted (each is a monotone fact).  Decided on lane 0.
+                    int hit = 0;
+                    if (lane == 0) {
+                        Lstale[i] = stale;
+                        Lcomp[i] = 0;
+                        if (stale && !A.check) {
+                            const RcEnt &rc = rcache[h.fid & (TM_RC - 1)];
+                            if (rc.fid == h.fid && rc.m[0] >= 0 && rc.m[1] >= 0 && rc.m[2] >= 0 &&
+                                !is_ins(bits, rc.m[0]) && !is_ins(bits, rc.m[1]) && !is_ins(bits, rc.m[2])) {
+                                Ent x = h;
+                                x.g = rc.g;
+                                x.cand = rc.cand;
+                                x.opt = 0;
+                                Lref[i] = x;
+                                hit = 1;
 #if TM_PROFILE
-                                    atomicAdd(&ctl.rc_hit, 1u);
+                                atomicAdd(&ctl.rc_hit, 1u);
 #endif
-                                }
                             }
-                        }
-                        hit = __shfl_sync(0xffffffffu, hit, 0);
-                        if (stale && !hit) {
-                            // constant slot when one entry per warp: a cnt-indexed write would
-                            // put these arrays in local memory
-                            const int sl = TM_EPW == 1 ? 0 : cnt;
-                            idx[sl] = i;
-                            fids[sl] = h.fid;
-                            fvv[sl][0] = h.a;
-                            fvv[sl][1] = h.b;
-                            fvv[sl][2] = h.c;
-                            cnt++;
                         }
                     }
-                }
-                if (cnt) {
-                    if (TM_EPW == 1) {
+                    hit = __shfl_sync(0xffffffffu, hit, 0);
+                    if (stale && !hit) {
+                        int fids[1] = {h.fid};
+                        int fvv[1][3] = {{h.a, h.b, h.c}};
                         // the refreshed entry and its max-corrs straight into the window arrays
-                        warp_entries<SMEM_ST>(A, bits, vst, 1, fvv, fids, &Lref[idx[0]], my_iters, Lmc[idx[0]]);
-                        if (lane == 0) Lcomp[idx[0]] = 1;
-                    } else {
-                        warp_entries<SMEM_ST>(A, bits, vst, cnt, fvv, fids, Lout[warp - TM_NEW_WARPS], my_iters,
-                                              nullptr);
-                        const int *mcs = &g_went[threadIdx.x >> 5][3 * TM_EPW];   // the refreshed max-corrs
-                        if (lane == 0)
-                            for (int q = 0; q < cnt; q++) {
-                                Lref[idx[q]] = Lout[warp - TM_NEW_WARPS][q];
-                                Lmc[idx[q]][0] = mcs[3 * q];
-                                Lmc[idx[q]][1] = mcs[3 * q + 1];
-                                Lmc[idx[q]][2] = mcs[3 * q + 2];
-                                Lcomp[idx[q]] = 1;
-                            }
+                        warp_entries<SMEM_ST>(A, bits, vst, 1, fvv, fids, &Lref[i], my_iters, Lmc[i]);
+                        if (lane == 0) Lcomp[i] = 1;
                     }
                 }
             }
