@@ -1198,31 +1198,24 @@ __device__ void replay_warp(const TmArgs &A, Ctl &ctl, const Ent *L, const Ent *
     const unsigned lt = (1u << lane) - 1u;
     const int pc = ctl.pool_count;
     int nk = 0, npool = 0;   // buffer-bound keys listed, pool entries written
-    for (int c0 = 0; c0 < npop; c0 += TM_CH) {
+    static_assert(TM_CH + 4 <= 32, "the new entries ride on the first chunk's spare lanes");
+    for (int c0 = 0; c0 < max(npop, 1); c0 += TM_CH) {
         const int pos = c0 + lane;
+        const int nk_l = lane - TM_CH;   // lanes TM_CH.. of the first chunk: the new entries
+        const bool bn = c0 == 0 && nk_l >= 0 && nk_l < nec && !((kind == 3) & (widx == nk_l));
         const bool br = lane < TM_CH && pos < npop && Lstale[pos] && !((kind == 2) & (widx == pos));
-        const double rg = br ? Lref[pos].g : 0.0;
-        const int rf = br ? Lref[pos].fid : 0;
-        const bool fr = br & ((!pm) | kgt(rg, rf, pg, pf));
-        const bool pr = br & !fr;
+        const Ent *src = bn ? &NE[nk_l] : &Lref[pos];
+        const bool any = br | bn;
+        const double rg = any ? src->g : 0.0;
+        const int rf = any ? src->fid : 0;
+        const bool fr = any & ((!pm) | kgt(rg, rf, pg, pf));
+        const bool pr = any & !fr;
         const unsigned bfr = __ballot_sync(0xffffffffu, fr), bpr = __ballot_sync(0xffffffffu, pr);
         // keys of the buffer-bound entries (src >= 0: Lref index, src < 0: ~NE index)
-        if (fr) { const int o = nk + __popc(bfr & lt); kg[o] = rg; kf[o] = rf; ksrc[o] = pos; }
-        if (pr) pool_put(A, &ctl.pool_minkey, pc + npool + __popc(bpr & lt), Lref[pos]);
+        if (fr) { const int o = nk + __popc(bfr & lt); kg[o] = rg; kf[o] = rf; ksrc[o] = bn ? ~nk_l : pos; }
+        if (pr) pool_put(A, &ctl.pool_minkey, pc + npool + __popc(bpr & lt), *src);
         nk += __popc(bfr);
         npool += __popc(bpr);
-    }
-    {
-        const bool bn = (lane < nec) & !((kind == 3) & (widx == lane));
-        const double nlg = bn ? NE[lane].g : 0.0;
-        const int nlf = bn ? NE[lane].fid : 0;
-        const bool fnn = bn & ((!pm) | kgt(nlg, nlf, pg, pf));
-        const bool pn = bn & !fnn;
-        const unsigned bfn = __ballot_sync(0xffffffffu, fnn), bpn = __ballot_sync(0xffffffffu, pn);
-        if (fnn) { const int o = nk + __popc(bfn & lt); kg[o] = nlg; kf[o] = nlf; ksrc[o] = ~lane; }
-        if (pn) pool_put(A, &ctl.pool_minkey, pc + npool + __popc(bpn & lt), NE[lane]);
-        nk += __popc(bfn);
-        npool += __popc(bpn);
     }
     const int nbuf = nk;
     __syncwarp();
@@ -1237,6 +1230,7 @@ __device__ void replay_warp(const TmArgs &A, Ctl &ctl, const Ent *L, const Ent *
         const double g = kg[k];
         const int f = kf[k];
         int r = 0;
+#pragma unroll 4
         for (int j = 0; j < nbuf; j++) r += kgt(kg[j], kf[j], g, f);
         const int sidx = ksrc[k];
         tobuf[r] = sidx >= 0 ? Lref[sidx] : NE[~sidx];
