@@ -56,6 +56,17 @@ constexpr int TM_CH = TM_FG_WARPS - TM_NEW_WARPS;  // window entries per replay 
 #endif
 constexpr int TM_WPE = TM_WPE_DEF;               // window entries per warp (one per half-warp): replay chunks per round
 constexpr int TM_K = TM_WPE * TM_CH;             // top-K speculated per round
+// After a round without a winner (every window entry popped stale: the lazy heap's stale streaks,
+// 60-800 pops per insertion at the end of config 5) the next window is TM_PASSES times as wide:
+// each window warp makes TM_PASSES passes of its two entries (nearly all refresh-cache hits then).
+// Only with the scan state in global memory (large n): at n = 10k the wider arrays cost more
+// than the 5 % of rounds they save (66.2 -> 67.6 ms), at n = 50k they pay (430 -> 418 ms).
+#ifndef TM_PASSES_DEF
+#define TM_PASSES_DEF 2
+#endif
+constexpr int TM_PASSES = TM_PASSES_DEF;
+template <bool SMEM_ST>
+__host__ __device__ constexpr int tm_kmax() { return SMEM_ST ? TM_K : TM_PASSES * TM_K; }
 #ifndef TM_MERGE_WARPS_DEF
 #define TM_MERGE_WARPS_DEF 28   // (the kernel picks per instantiation: see tm_merge_warps)
 #endif
@@ -78,7 +89,7 @@ constexpr int TM_BMAX = 2 * TM_B;               // ... when the scan state lives
 // the queue can then take the room, and a longer queue means fewer O(pool) refills
 template <bool SMEM_ST>
 __host__ __device__ constexpr int tm_qb() { return SMEM_ST ? TM_B : TM_BMAX; }
-constexpr int TM_BATCH = TM_K + 8;
+constexpr int TM_BATCH = TM_K + 8;   // (largest re-queued run of a narrow round; kernels size theirs from tm_kmax)
 static_assert(TM_CH <= 32, "replay_warp maps one queue position of a chunk per lane");
 static_assert(TM_WPE == 1 || TM_WPE == 2, "window_refresh2 serves one entry per half-warp");
 
@@ -143,6 +154,7 @@ struct Ctl {
     long long rf_t[4];   // refill phases: select, take, place, hole fill (TM_PROFILE)
     unsigned rc_hit;     // refresh-cache hits (TM_PROFILE)
     long long it_total, it_maxsum;
+    int wide;        // the last round had no winner: this round's window is TM_PASSES times as wide
 };
 
 struct TmArgs {
@@ -1063,7 +1075,7 @@ __device__ __forceinline__ bool kgt(double g1, int f1, double g2, int f2) {
 // the first i where L[i] is fresh or is beaten by the running max of the
 // refreshed entries or by the best new entry: a prefix max + a ballot.
 __device__ void replay_warp(const TmArgs &A, Ctl &ctl, const Ent *L, const Ent *Lref, const int *Lstale,
-                            const Ent *NE, Ent *batch, Ent *tobuf, double *kg, int *kf, int *ksrc, double *tkg,
+                            const Ent *NE, Ent *tobuf, double *kg, int *kf, int *ksrc, double *tkg,
                             int *tkf) {
     const int lane = threadIdx.x & 31;
 #if TM_PROFILE
@@ -1488,24 +1500,29 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
     const int n = A.n;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     __shared__ Ctl ctl;
-    __shared__ Ent Lref[TM_K];
+    constexpr int KM = tm_kmax<SMEM_ST>();   // widest window
+    constexpr int BT = KM + 8;               // longest re-queued run (+ new entries)
+    // static shared memory must stay under 48 KB: with the wide window (scan state in global
+    // memory) the refreshed entries and the re-queued run move to the dynamic part
+    __shared__ Ent Lref_s[SMEM_ST ? KM : 1];
+    __shared__ Ent tobuf_s[SMEM_ST ? BT : 1];
     __shared__ Ent Lout[TM_WARPS - TM_NEW_WARPS][TM_EPW];
-    __shared__ int Lstale[TM_K];
+    __shared__ int Lstale[KM];
     __shared__ Ent NE[4];
-    __shared__ Ent batch[TM_BATCH];
-    __shared__ Ent tobuf[TM_BATCH];
     __shared__ Ent red_e[TM_WARPS];
-    __shared__ double rk_g[TM_BATCH];
-    __shared__ int rk_f[TM_BATCH], rk_src[TM_BATCH];
-    __shared__ double tk_g[TM_BATCH];   // tobuf's keys (gain, fid), sorted
-    __shared__ int tk_f[TM_BATCH];
+    __shared__ double rk_g[BT];
+    __shared__ int rk_f[BT], rk_src[BT];
+    __shared__ double tk_g[BT];   // tobuf's keys (gain, fid), sorted
+    __shared__ int tk_f[BT];
     __shared__ int red_ok[TM_WARPS];
     __shared__ RcEnt rcache[TM_RC];
     __shared__ int rc_claim[TM_RC];   // round that last wrote the slot: one writer per slot per round
-    __shared__ int Lmc[TM_K][3];
-    __shared__ int Lcomp[TM_K];
+    __shared__ int Lmc[KM][3];
+    __shared__ int Lcomp[KM];
 
-    Ent *buf0 = reinterpret_cast<Ent *>(tm_smem);
+    Ent *Lref = SMEM_ST ? Lref_s : reinterpret_cast<Ent *>(tm_smem);
+    Ent *tobuf = SMEM_ST ? tobuf_s : Lref + KM;
+    Ent *buf0 = SMEM_ST ? reinterpret_cast<Ent *>(tm_smem) : tobuf + BT;
     Ent *buf1 = buf0 + QB;
     uint32_t *bits = reinterpret_cast<uint32_t *>(buf1 + QB);
     const int nwords = (n + 31) >> 5;
@@ -1566,6 +1583,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
         ctl.nf = 4;
         ctl.ne_count = (n > 4) ? 4 : 0;
         ctl.L_count = 0;
+        ctl.wide = 0;
         ctl.pops = ctl.refreshes = ctl.gain_inc = 0;
         ctl.pool_count = 0;
         ctl.pool_minkey = ~0ull;
@@ -1628,8 +1646,12 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
             } else {
                 // window warp j serves queue positions j and j + TM_CH (one per half-warp) on the lean
                 // path; what needs a scan (or check_invariants mode) goes through warp_entries
-                const int j = warp - TM_NEW_WARPS;
+                const int j0 = warp - TM_NEW_WARPS;
                 const int cntL = ctl.L_count;
+#pragma unroll
+                for (int ps = 0; ps < KM / TM_K; ps++) {   // one pass; TM_PASSES in a wide round
+                const int j = j0 + ps * TM_K;
+                if (j >= cntL) break;
                 unsigned todo = 0u;
                 if (A.check) {
                     todo = (j < cntL ? 1u : 0u) | ((TM_WPE > 1 && j + TM_CH < cntL) ? 2u : 0u);
@@ -1678,6 +1700,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
                         if (lane == 0) Lcomp[i] = 1;
                     }
                 }
+                }
             }
         }
 #if TM_PROFILE
@@ -1707,7 +1730,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
         // it, so the first to claim a slot writes it.  The winner's bit is set while
         // the speculative refreshes run: they stay exact (every fact they use is
         // monotone) and the cache's candidate check rejects what the winner voids.
-        if (warp == 0) replay_warp(A, ctl, sel ? buf1 : buf0, Lref, Lstale, NE, batch, tobuf, rk_g, rk_f, rk_src, tk_g, tk_f);
+        if (warp == 0) replay_warp(A, ctl, sel ? buf1 : buf0, Lref, Lstale, NE, tobuf, rk_g, rk_f, rk_src, tk_g, tk_f);
         else if (!A.check && (warp == 1 || warp >= MW)) {
             const int round = (int)ctl.rounds;
             if (warp == 1) {
@@ -1861,7 +1884,12 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
                 ctl.size = total;
                 ctl.sel = sel ^ 1;
                 ctl.need_refill = total < TM_K && ctl.pool_count > 0;
-                ctl.L_count = min(TM_K, total);
+                if (KM > TM_K) {
+                    ctl.wide = !ctl.winner;
+                    ctl.L_count = min(ctl.wide ? KM : TM_K, total);
+                } else {
+                    ctl.L_count = min(TM_K, total);
+                }
                 // ================= insert the winner (tmfg.py:94-143 bookkeeping)
                 ctl.ne_count = 0;
                 if (ctl.winner) {
@@ -1922,7 +1950,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
         // ================= refill the shared buffer from the pool when short
         if (ctl.need_refill) {
             refill<TM_FG_T, QB>(A, ctl, sel ? buf1 : buf0, sel ? buf0 : buf1, red_e, red_ok, tid);
-            if (tid == 0) ctl.L_count = min(TM_K, ctl.size);
+            if (tid == 0) ctl.L_count = min((KM > TM_K && ctl.wide) ? KM : TM_K, ctl.size);
 #if TM_PROFILE
             tc1 = fg_sync_clock();
             if (tid == 0) { ctl.t_refill += tc1 - tc0; tc0 = tc1; }
@@ -2005,6 +2033,7 @@ __global__ void __launch_bounds__(TM_T, 1) tmfg_heap_kernel(const __grid_constan
 
 size_t tm_smem_bytes(int64_t n, bool smem_st) {
     size_t b = (size_t)2 * (smem_st ? tm_qb<true>() : tm_qb<false>()) * sizeof(Ent);
+    if (!smem_st) b += (size_t)(2 * tm_kmax<false>() + 8) * sizeof(Ent);   // Lref + tobuf (wide window)
     b += (size_t)(((n + 31) / 32 + 1) & ~1LL) * 4;
     if (smem_st) b += (size_t)n * 8;
     b += (size_t)(smem_st ? tm_qb<true>() : tm_qb<false>()) * sizeof(short);   // merge scratch
