@@ -423,15 +423,23 @@ int build(Ctx &cx, const int64_t *vb_dev, const int64_t *vc_dev, int64_t *lefts,
         groups3.reserve(ng);
         for (size_t c = 0; c < ng; c++) groups3.push_back(Span{cflat.data() + coff[c], coff[c + 1] - coff[c]});
         HPROF("cmem");
-        // layer 3 (the n = 50k critical path: one large group max + NN-chain) ahead of layers 1-2
+        // the side stream forks from the caller's stream here, before any layer is queued on it
         HC(side3.open(cx.st, true));
         HPROF("open3");
         j3.st = side3.st;
-        HR(launch_group_linkages(cx, j3, {groups3}));
     }
+    // The layer with the largest matrix is the critical path (its NN-chain is serial in the
+    // matrix size): layer 3 at n = 50k (one 5,906-group matrix), layer 2 at n = 10k (1,056 groups
+    // against a few hundred converging groups).  Its group maxima are queued first, so its chain
+    // starts before the other layer's group maxima occupy the GPU.
+    size_t m2max = 0;
+    for (const auto &sp : subproblems) m2max = std::max(m2max, sp.size());
+    const bool l3_first = layer3 && conv_ids.size() >= m2max;
+    if (layer3 && l3_first) HR(launch_group_linkages(cx, j3, {groups3}));
     HPROF("tL3");
     j2.st = cx.st;
     if (!subproblems.empty()) HR(launch_group_linkages(cx, j2, subproblems));
+    if (layer3 && !l3_first) HR(launch_group_linkages(cx, j3, {groups3}));
     // layer 1 last: its linkages are never the critical path (layer 2 is at n = 10k, layer 3
     // at n = 50k), so its host preparation overlaps their device work
     if (!multi.empty()) {   // ---- layer 1: complete linkage inside every bubble group (dbht.py:247-262)
