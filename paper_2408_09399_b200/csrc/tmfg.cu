@@ -616,13 +616,14 @@ __device__ __forceinline__ unsigned window_refresh2(const TmArgs &A, const uint3
     const int i = base + h * TM_CH;
     const bool valid = i < cntL;
     const Ent *hp = cur + (valid ? i : base);
-    const int2 fc = *reinterpret_cast<const int2 *>(&hp->fid);   // (fid, cand)
+    // (fid, cand) and (a, b, c, opt) in flight together: one dependent shared-memory step less
+    const int2 fc = *reinterpret_cast<const int2 *>(&hp->fid);
+    const int4 fa = *reinterpret_cast<const int4 *>(&hp->a);
     const bool stale = valid && is_ins(bits, fc.y);
     if (!__any_sync(0xffffffffu, stale)) {
         if (valid && l == 0) { Lstale[i] = 0; Lcomp[i] = 0; }
         return 0u;
     }
-    const int4 fa = *reinterpret_cast<const int4 *>(&hp->a);     // (a, b, c, opt)
     const int a = fa.x, b = fa.y, c = fa.z, fid = fc.x;
     const RcEnt &rc = rcache[fid & (TM_RC - 1)];
     const int l9 = l < 9 ? l : 0;
