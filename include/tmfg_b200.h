@@ -103,8 +103,10 @@ int tg_initial_clique_screened(const double *S, int64_t n, const double *screen,
  * {pops, refreshes, gain_increases, status, assert_fid, assert_old_gain_bits,
  *  assert_new_gain_bits, then kernel self-profile counters (rounds, refills,
  *  per-phase cycles; see tools/tmfg_profile.py)}.  status 0 = ok, 2 = the check_invariants
- * assertion of tmfg.py:429 fired (check != 0 only).  Persistent single-CTA
- * kernel; check != 0 adds the brute-force optimality test of tmfg.py:377-399. */
+ * assertion of tmfg.py:429 fired (check != 0 only).  One persistent thread-block
+ * cluster (the leader CTA runs the insertion rounds, the other CTAs keep the per-vertex
+ * scan state current and prefetch S into L2); check != 0 adds the brute-force optimality
+ * test of tmfg.py:377-399. */
 size_t tg_tmfg_workspace_bytes(int64_t n);
 int tg_tmfg_heap(const double *S, const int32_t *order, int64_t n, const int32_t *clique, int32_t *trace_out,
                  int32_t *host_fid_out, int32_t *edges_out, int32_t *faces_out, int64_t *stats_out, int32_t check,

@@ -1,4 +1,6 @@
-// tmfg.cu -- the lazy-gain (heap) TMFG insertion loop as one persistent CTA.
+// tmfg.cu -- the lazy-gain (heap) TMFG insertion loop as one persistent thread-block cluster
+// (the leader CTA runs the rounds below; helper CTAs keep the per-vertex scan state two
+// candidates deep and one prefetches the S values of the queue head into L2).
 //
 // Replaces tmfg.py:344-436 build_tmfg_heap with its helpers tmfg.py:94-144
 // (_GraphAccum), 147-182 (TmfgState, refresh_max_corr), 266-277
@@ -17,12 +19,15 @@
 //     replayed exactly by a short scan (a stale pop pushes a fresh entry; the
 //     first fresh thing on top wins).
 //
-// One round = [parallel] refresh the top-K stale entries and build the entries
+// One round = [parallel] refresh the stale entries among the top K = 56 of the queue (two
+// per window warp on the lean path, window_refresh2; a scan only when a vertex's scan-state
+// word certifies no uninserted candidate) and build the entries
 // of the 3 faces created by the last insertion (cursor scans: one 128-byte
 // warp load of order[w] + a ballot against the inserted bitmap in shared
 // memory; gains: 9 fp64 loads of S, summed (S[a,u]+S[b,u])+S[c,u] with
-// __dadd_rn) -> [one thread] replay the pops -> [block] update the queue and
-// insert the winner.  About two dependent global-load latencies per insertion.
+// __dadd_rn) -> [one warp] replay the pops, chunk of 28 window positions by chunk -> [block]
+// update the queue and insert the winner.  About two dependent global-load latencies per
+// insertion.
 //
 // Priority queue: the top B entries live sorted in shared memory (double
 // buffered, merge-path insertion); the rest sit unsorted in a global pool whose
