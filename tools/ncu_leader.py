@@ -2,7 +2,7 @@
 source lines only the leader runs (round loop, window refresh, replay), and the hottest lines."""
 import csv, sys, collections
 rows = list(csv.reader(open(sys.argv[1])))
-ranges = [(430, 600), (860, 1045), (1380, 1740)]   # fast refresh, replay_warp, the round loop
+ranges = [tuple(int(x) for x in r.split("-")) for r in sys.argv[3].split(",")] if len(sys.argv) > 3 else [(440, 740), (1075, 1270), (1620, 1960)]   # lean refresh, replay_warp, the round loop (line ranges of tmfg.cu at HEAD)
 hdr = None; path = None
 reasons = collections.Counter(); lines = collections.Counter(); src = {}; inst = collections.Counter()
 for r in rows:
